@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""Benchmark: BFS GTEPS per source on one B200 (+ expansion-kernel roofline), BASELINE.json.
+
+A "step" is one full traversal s3bfs_run(source) -- every row of SURVEY.md s.8(a) -- on the
+workload BASELINE.json's metric is quoted on: R-MAT scale 24, edge factor 16 (configs[3]),
+cycling over its 16 seeded non-isolated sources.  The graph (2.08 GB of col_indices) is
+resident in HBM before timing; the L2 is also flushed (256 MB write) before every step,
+outside that step's CUDA-event pair.
+
+Legs (all printed in ONE JSON line by rank 0):
+  value        device-timed GTEPS = sum over steps and ranks of m_c/2 / max-over-ranks time
+  e2e          the same through the C ABI with the result read back to pinned host memory
+  roofline     k_explore (the dominant kernel): algorithmic bytes / CUDA-event duration, from
+               a host-loop pass with per-launch events
+  cpu_baseline the oracle (serial C BFS) on a bounded sample of the same sources, 1 core
+--impl reference times the oracle alone as the reference arm (rank 0 only).
+Multi-GPU (torchrun): independent traversals per rank (replicas, weak scaling); the only
+collectives are the timing barrier and the max-over-ranks reduction.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "BFS GTEPS per source on 1 B200; expansion-kernel HBM GB/s as % of peak"
+CONFIG_INDEX = {"er": 0, "grid": 1, "rmat20": 2, "rmat24": 3, "tail": 4}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="s3bfs", choices=["s3bfs", "reference"])
+    ap.add_argument("--config", default="rmat24", choices=list(CONFIG_INDEX))
+    ap.add_argument("--oracle-sources", type=int, default=4,
+                    help="sources checked bit-exactly against (and timed on) the oracle")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--detail-out", default="")
+    ap.add_argument("--loop-mode", type=int, default=0)
+    ap.add_argument("--tier0", type=int, default=0)
+    ap.add_argument("--grain", type=int, default=0)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+            time.sleep(0.3)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def launches_from_stats(st) -> int:
+    """Kernel launches of one traversal in graph mode: k_init, one k_dispatch per WHILE
+    iteration, one k_small per tier-0 run, k_explore + k_compact per tier-1 level."""
+    tiers = [int(t) for t in st["tier"] if t in (0, 1)]
+    segs0 = sum(1 for i, t in enumerate(tiers) if t == 0 and (i == 0 or tiers[i - 1] != 0))
+    t1 = tiers.count(1)
+    iterations = segs0 + t1 + 1
+    return 1 + iterations + segs0 + 2 * t1
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import graphgen
+    import oracle
+    g = graphgen.make_config(args.config)
+    srcs = g.sources
+    budget_s = 150.0
+    warm = min(args.warmup, 1)
+    for i in range(warm):
+        oracle.bfs(g.row_offsets, g.col_indices, srcs[i % len(srcs)])
+    done, edges, t_tot = 0, 0, 0.0
+    for k in range(args.steps):
+        s = srcs[k % len(srcs)]
+        t0 = time.perf_counter()
+        lv, _ = oracle.bfs(g.row_offsets, g.col_indices, s)
+        dt = time.perf_counter() - t0
+        _, _, m_c, _ = oracle.level_profile(g.row_offsets, lv)
+        done += 1
+        edges += m_c // 2
+        t_tot += dt
+        if t_tot > budget_s:
+            break
+    gteps = edges / t_tot / 1e9
+    sample = (f"oracle_bfs (serial FIFO BFS, C -O3, 1 thread) on {args.config}: {done} of "
+              f"{args.steps} steps (150 s budget), warmup {warm}")
+    line = {"impl": "reference", "metric": METRIC, "value": gteps, "unit": "GTEPS",
+            "n_gpus": args.gpus, "steps": done, "warmup": warm,
+            "ms_per_step": t_tot / done * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32", "data": "synthetic (seeded graphgen)",
+            "config": {"workload": args.config, "baseline_config": CONFIG_INDEX[args.config],
+                       "n": g.n, "nnz": g.nnz},
+            "cpu_baseline": {"value": gteps, "unit": "GTEPS", "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": gteps, "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import graphgen
+    import paper_2209_08764_b200 as pkg
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    threads = max(1, (os.cpu_count() or 8) // max(world, 1))
+    g = graphgen.make_config(args.config, threads=threads)
+    ro = torch.from_numpy(g.row_offsets).to(dev)
+    col = torch.from_numpy(g.col_indices).to(dev)
+    deg = (ro[1:] - ro[:-1]).to(torch.int64)
+    opts = pkg.Options(loop_mode=args.loop_mode, tier0_max_edges=args.tier0,
+                       edges_per_cta=args.grain)
+    bfs = pkg.S3BFS(ro, col, opts)
+    info = bfs.info()
+    n = g.n
+    level = torch.empty(n, dtype=torch.int32, device=dev)
+    parent = torch.empty(n, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sp = int(stream.cuda_stream)
+    lp, pp = int(level.data_ptr()), int(parent.data_ptr())
+
+    # ---- untimed: per-source edge counts (m_c from the traversal's own levels), launches,
+    # and bit-exact oracle checks + CPU baseline on a bounded sample of sources ------------
+    srcs = g.sources
+    my_srcs = [srcs[(rank + world * k) % len(srcs)] for k in range(len(srcs))]
+    per = {}
+    for s in sorted(set(my_srcs)):
+        pkg.s3bfs_run_ptr(bfs.handle, s, lp, pp, sp)
+        st = bfs.level_stats()
+        m_c = int(deg[level >= 0].sum().item())
+        per[s] = {"m_c": m_c, "levels": int(len(st)), "launches": launches_from_stats(st),
+                  "stats": st}
+    verified = {"sources": 0, "levels_bit_exact": True, "parents_valid": True}
+    cpu_times, cpu_edges = [], []
+    if rank == 0 and args.oracle_sources > 0:
+        import oracle
+        for s in srcs[: args.oracle_sources]:
+            pkg.s3bfs_run_ptr(bfs.handle, s, lp, pp, sp)
+            torch.cuda.synchronize()
+            lv, pa = level.cpu().numpy(), parent.cpu().numpy()
+            t0 = time.perf_counter()
+            ref, _ = oracle.bfs(g.row_offsets, g.col_indices, s)
+            cpu_times.append(time.perf_counter() - t0)
+            _, _, m_c, _ = oracle.level_profile(g.row_offsets, ref)
+            cpu_edges.append(m_c // 2)
+            ok = bool(np.array_equal(lv, ref))
+            code, _ = oracle.check_bfs(g.row_offsets, g.col_indices, s, lv, pa)
+            verified["sources"] += 1
+            verified["levels_bit_exact"] &= ok
+            verified["parents_valid"] &= code == 0
+            if m_c != per[s]["m_c"]:
+                verified["levels_bit_exact"] = False
+        if not (verified["levels_bit_exact"] and verified["parents_valid"]):
+            print(f"VERIFICATION FAILED: {verified}", file=sys.stderr, flush=True)
+
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def one_step(k, ev0=None, ev1=None):
+        s = my_srcs[k % len(my_srcs)]
+        if not args.no_flush:
+            flush_buf.fill_(k & 255)
+        if ev0 is not None:
+            ev0.record(stream)
+        pkg.s3bfs_run_ptr(bfs.handle, s, lp, pp, sp)
+        if ev1 is not None:
+            ev1.record(stream)
+        return s
+
+    for k in range(args.warmup):
+        one_step(k)
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        done_srcs = [one_step(k, *evs[k]) for k in range(args.steps)]
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    my_ms = float(sum(step_ms))
+    my_edges = sum(per[s]["m_c"] // 2 for s in done_srcs)
+    my_launches = sum(per[s]["launches"] for s in done_srcs)
+    t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
+    e = torch.tensor([my_edges], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(e, op=dist.ReduceOp.SUM)
+    max_ms, tot_edges = float(t.item()), float(e.item())
+    value = tot_edges / (max_ms / 1e3) / 1e9
+    per_step_gteps = [per[s]["m_c"] / 2 / (ms / 1e3) / 1e9 for s, ms in zip(done_srcs, step_ms)]
+    hmean = len(per_step_gteps) / sum(1.0 / x for x in per_step_gteps)
+
+    # ---- e2e: through the C ABI, result read back to pinned host memory every step --------
+    h_level = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    h_parent = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    e2e_steps = min(args.steps, 16)
+    e2e_ms, e2e_edges = 0.0, 0
+    for k in range(e2e_steps):
+        if not args.no_flush:
+            flush_buf.fill_(k & 255)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        s = my_srcs[k % len(my_srcs)]
+        pkg.s3bfs_run_ptr(bfs.handle, s, lp, pp, sp)
+        h_level.copy_(level, non_blocking=True)
+        h_parent.copy_(parent, non_blocking=True)
+        b.record(stream)
+        b.synchronize()
+        e2e_ms += a.elapsed_time(b)
+        e2e_edges += per[s]["m_c"] // 2
+    te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    ee = torch.tensor([e2e_edges], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ee, op=dist.ReduceOp.SUM)
+    e2e_value = float(ee.item()) / (float(te.item()) / 1e3) / 1e9
+
+    # ---- roofline of k_explore: per-launch CUDA events (host-loop pass, same kernels) -----
+    roof = None
+    detail = {}
+    if rank == 0:
+        hb = pkg.S3BFS(ro, col, pkg.Options(loop_mode=2, time_kernels=1,
+                                            tier0_max_edges=args.tier0,
+                                            edges_per_cta=args.grain))
+        ex_ms, ex_launch, alg_bytes, cm_ms, sm_ms = 0.0, 0, 0, 0.0, 0.0
+        step_ms_hl = 0.0
+        for s in srcs:
+            flush_buf.fill_(1)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            hb.run(s, level, parent)
+            kt = pkg.s3bfs_get_kernel_times(hb.handle)
+            step_ms_hl += (time.perf_counter() - t0) * 1e3
+            st = hb.level_stats()
+            t1 = st[st["tier"] == 1]
+            # SURVEY s.8(d): Kd = 4 B/arc col stream + 4 B/arc status + 16 B per discovery
+            alg_bytes += int(8 * t1["e_l"].astype(np.int64).sum()
+                             + 16 * t1["candidates"].astype(np.int64).sum())
+            ex_ms += kt["explore_ms"]
+            ex_launch += kt["explore_launches"]
+            cm_ms += kt["compact_ms"]
+            sm_ms += kt["small_ms"]
+        hb.close()
+        peak, peak_src = peaks()
+        achieved = alg_bytes / ex_launch / (ex_ms / ex_launch / 1e3) / 1e9 if ex_ms else 0.0
+        # the same kernel inside the captured loop (globaltimer, CTA-0 start stamps)
+        in_graph_ms = sum(float(((p["stats"]["t_explore_end_ns"] - p["stats"]["t_explore_begin_ns"])
+                                 [p["stats"]["tier"] == 1]).sum()) / 1e6 for p in per.values())
+        step_total = sum(float(p["stats"]["t_end_ns"][-1] - p["stats"]["t_begin_ns"][0]) / 1e6
+                         for p in per.values())
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get(args.config)
+            except Exception:  # noqa: BLE001
+                traffic = None
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "kernel": "k_explore",
+                "peak_source": peak_src, "launches": ex_launch,
+                "bytes_per_launch": alg_bytes / max(ex_launch, 1),
+                "avg_launch_ms": ex_ms / max(ex_launch, 1),
+                "share_of_step_events": ex_ms / max(ex_ms + cm_ms + sm_ms, 1e-9),
+                "share_of_step_in_graph": in_graph_ms / max(step_total, 1e-9),
+                "compact_ms_total": cm_ms, "small_ms_total": sm_ms}
+        detail["roofline_pass"] = {"explore_ms": ex_ms, "compact_ms": cm_ms, "small_ms": sm_ms,
+                                   "host_loop_wall_ms": step_ms_hl}
+
+    if rank == 0:
+        cpu = None
+        if cpu_times:
+            cg = sum(cpu_edges) / sum(cpu_times) / 1e9
+            cpu = {"value": cg, "unit": "GTEPS", "cores": 1, "kind": "oracle",
+                   "sample": f"oracle_bfs (serial FIFO BFS, C -O3, 1 thread), 1 run from each of "
+                             f"the first {len(cpu_times)} of {len(srcs)} {args.config} sources "
+                             f"({sum(cpu_times):.1f} s)"}
+        line = {
+            "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int32", "data": f"synthetic (seeded graphgen {args.config}, BASELINE.json "
+                                      f"configs[{CONFIG_INDEX[args.config]}])",
+            "config": {"workload": args.config, "baseline_config": CONFIG_INDEX[args.config],
+                       "n": g.n, "nnz": g.nnz, "sources": len(srcs),
+                       "l2": "flushed (256 MB write) before every step, outside its events"
+                             if not args.no_flush else "not flushed (col 2 GB > L2)",
+                       "loop": "cuda-graph" if args.loop_mode != 2 else "host",
+                       "p_max": info["p_max"], "grain": info["edges_per_cta"],
+                       "t0": info["tier0_max_edges"]},
+            "gteps_hmean": hmean, "gteps_min": min(per_step_gteps),
+            "gteps_max": max(per_step_gteps),
+            "roofline": roof, "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "GTEPS", "h2d_bytes_per_step": 4,
+                    "d2h_bytes_per_step": 8 * n,
+                    "what": "s3bfs_run through the C ABI (source by value) + level/parent "
+                            "copied to pinned host memory, CUDA events around both"},
+            "clocks": clk.summary(), "gpu_launches": my_launches, "verified": verified,
+        }
+        print(json.dumps(line), flush=True)
+        if args.detail_out:
+            detail["per_source"] = {int(s): {"m_c": p["m_c"], "levels": p["levels"],
+                                             "launches": p["launches"],
+                                             "per_level": p["stats"].tolist()}
+                                    for s, p in per.items()}
+            detail["step_ms"] = step_ms
+            detail["per_step_gteps"] = per_step_gteps
+            with open(args.detail_out, "w") as f:
+                json.dump(detail, f, default=lambda o: o.item() if hasattr(o, "item") else str(o))
+    bfs.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,156 @@
+/*
+ * include/s3bfs.h -- C ABI of the B200-native S3BFS frontier-expansion path.
+ *
+ * The library (paper_2209_08764_b200/libs3bfs.so, sources in paper_2209_08764_b200/csrc/)
+ * runs the level-synchronous BFS of PAPER.md Figure 1, "Parallel-BFS(s, P) ... Returns
+ * d[0:n-1]", on one B200 (sm_100a).  "P:n" below = /root/reference/PAPER.md line n;
+ * "Fig1 Lk" = item k of the Figure 1 enumerate (SURVEY.md section 0 maps items to lines);
+ * "S:n" = /root/reference/SPEC.md line n (interfaces only).  DESIGN.md lists every reading.
+ *
+ * Per level the path runs, entirely on the device:
+ *   (a) frontier degree gather            Fig1 L12-L13
+ *   (b) exclusive prefix sum of degrees   Fig1 L14-L15, Blelloch
+ *   (c) equal-work edge split (search)    Fig1 L17
+ *   (d) explore + level/parent/owner      Fig1 L18, benign race, no atomics
+ *   (e) owner dedup + compaction          Fig1 L19-L29
+ *   (f) level-adaptive launch sizing      P_l = min(P, W) (Fig1 L11, L16)
+ * (a)+(b) are fused into (e)'s write-out of the next frontier; (c) is fused into (d).
+ *
+ * Conventions (all entry points):
+ *   - Graph: int32 CSR out-adjacency, row_offsets[n+1], col_indices[nnz].  Every
+ *     arc (u, v) is explored from u.  Multigraphs and self-loops are allowed (DESIGN R14).
+ *   - Output: level[v] = hop distance d(s, v), -1 if unreachable (DESIGN R1, the paper's
+ *     d <- infinity, Fig1 L3); parent[s] = s, parent[v] = some u with (u, v) an arc and
+ *     level[u] = level[v] - 1, parent[v] = -1 if unreachable (DESIGN R2; not in the paper).
+ *   - Errors: every call returns an s3bfs_status; nothing throws or aborts across the ABI.
+ *     s3bfs_last_error() gives the detail of the last failure on a handle.
+ *   - Asynchrony: s3bfs_run only ENQUEUES work on `stream`; results are valid once the caller
+ *     synchronises that stream.  One traversal at a time per handle.
+ */
+#ifndef S3BFS_H_
+#define S3BFS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* CUDA stream handle as an opaque pointer (identical to cudaStream_t; NULL = legacy stream).
+ * Declared here so this header needs no CUDA include. */
+typedef void *s3bfs_stream_t;
+
+typedef struct s3bfs_ctx *s3bfs_handle; /* opaque */
+
+typedef enum {
+  S3BFS_OK = 0,
+  S3BFS_ERR_INVALID_ARGUMENT = 1, /* null / non-device pointer, n <= 0, nnz out of range,
+                                     source not in [0, n) */
+  S3BFS_ERR_UNSUPPORTED = 2,      /* device is not compute capability 10.x, or a size the
+                                     int32 index words cannot address */
+  S3BFS_ERR_OUT_OF_MEMORY = 3,    /* workspace allocation failed */
+  S3BFS_ERR_CUDA = 4,             /* a CUDA runtime/driver error; detail in s3bfs_last_error */
+  S3BFS_ERR_INVALID_GRAPH = 5     /* validate_csr found a CSR invariant violated */
+} s3bfs_status;
+
+/* Options.  A zero-initialised struct (or NULL) selects every default.  Mirrors the
+ * paper's tunables: P (max cores) and GRAINSIZE, and the work-insensitive
+ * comparison variant. */
+typedef struct {
+  int32_t edges_per_cta;   /* grain of (f): P_l = min(P_max, ceil(e_l / grain)).  0 -> 16384 */
+  int32_t tier0_max_edges; /* T0: a level with e_l <= T0 (and n_l <= 8192) runs in the
+                              single-CTA tier.  0 -> 8192 (the maximum); < 0 -> tier 0 off */
+  int32_t loop_mode;       /* 0/1: level loop captured in a CUDA graph (WHILE + IF nodes);
+                              2: host-driven loop (one device->host read per level; run then
+                              blocks until the traversal ends) */
+  int32_t collect_stats;   /* 0/1: per-level statistics on; -1: off */
+  int32_t validate_csr;    /* 1: s3bfs_create checks row_offsets/col_indices on the device */
+  int32_t variant;         /* 0: work-sensitive (paper's S3BFS); 1: work-insensitive -- every
+                              level uses the full grid P_max and tier 0 is off */
+  int32_t max_ctas;        /* cap on P_max (the paper's P); 0 -> SMs x resident CTAs/SM */
+  int32_t debug_poison;    /* 1: fill the internal Owner array with garbage at create, to
+                              prove it is never read before written (DESIGN R3) */
+  int32_t time_kernels;    /* 1 (host-loop mode only): bracket every kernel launch with CUDA
+                              events on the run's stream; read by s3bfs_get_kernel_times */
+  int32_t reserved[7];
+} s3bfs_options;
+
+/* One record per BFS level (the SPEC LevelStats analogue).  n_l = |frontier|
+ * (Fig1 L9), e_l = sum of its degrees (Fig1 L15), tier 0 = single CTA, 1 = full kernels,
+ * 2 = a last level with e_l = 0 (nothing explored), grid = CTAs used (P_l), candidates =
+ * discoveries incl. benign-race duplicates, kept = n_{l+1} after owner dedup.  Times are
+ * %globaltimer ns: level start (= previous level's end, so launch gaps count) and end; for
+ * tier 1 also k_explore's start (its CTA 0) and k_compact's start (its CTA 0), whose
+ * difference is the exploration kernel's duration inside the captured loop (0 for tier 0). */
+typedef struct {
+  int32_t level, n_l, e_l, tier, grid, candidates, kept, pad;
+  uint64_t t_begin_ns, t_end_ns;
+  uint64_t t_explore_begin_ns, t_explore_end_ns;
+} s3bfs_level_stat;
+
+/* Create a traversal context over a CSR graph already resident in device memory.
+ * row_offsets: device, n+1 int32, BORROWED (caller keeps it alive and unmodified until
+ * destroy).  col_indices: device, nnz int32, borrowed (may be NULL iff nnz == 0).
+ * Requires 1 <= n, 0 <= nnz <= INT32_MAX - workspace slack.  The handle owns its
+ * workspace (Owner[n], two frontier buffers, candidate buffer, control block, stats).
+ * May synchronise `stream`.  On failure *out is set to NULL. */
+s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_t *row_offsets,
+                          const int32_t *col_indices, const s3bfs_options *opts,
+                          s3bfs_stream_t stream);
+
+/* Parallel-BFS(s, P): enqueue one traversal from `source` on `stream`.
+ * level, parent: device, n int32 each, caller-owned, FULLY overwritten.
+ * Errors: INVALID_ARGUMENT for source outside [0, n) or null/non-device outputs. */
+s3bfs_status s3bfs_run(s3bfs_handle h, int32_t source, int32_t *level, int32_t *parent,
+                       s3bfs_stream_t stream);
+
+/* Free the handle and its workspace (synchronises the last run's stream).  NULL is a no-op. */
+s3bfs_status s3bfs_destroy(s3bfs_handle h);
+
+/* Static description of a status code. */
+const char *s3bfs_status_string(s3bfs_status s);
+
+/* Detail string of the last error on h (valid until the next call on h). */
+s3bfs_status s3bfs_last_error(s3bfs_handle h, const char **msg);
+
+/* Copy the last run's per-level records (synchronises the stream of that run).
+ * Writes min(cap, levels) records to out (host memory) and the level count to *num_levels. */
+s3bfs_status s3bfs_get_level_stats(s3bfs_handle h, s3bfs_level_stat *out, int32_t cap,
+                                   int32_t *num_levels);
+
+/* Device-side tunables the handle resolved (for reports): P_max, grain, T0, CTA sizes. */
+typedef struct {
+  int32_t num_sms, p_max, edges_per_cta, tier0_max_edges;
+  int32_t kd_threads, kd_tile_edges, ksmall_threads, ksmall_max_frontier;
+  int64_t workspace_bytes;
+} s3bfs_info;
+s3bfs_status s3bfs_get_info(s3bfs_handle h, s3bfs_info *out);
+
+/* CUDA-event kernel times of the last run (options.time_kernels = 1 and loop_mode = 2;
+ * otherwise all zero).  Synchronises the run's stream. */
+typedef struct {
+  double explore_ms, compact_ms, small_ms;  /* summed over launches */
+  int32_t explore_launches, compact_launches, small_launches, pad;
+} s3bfs_kernel_times;
+s3bfs_status s3bfs_get_kernel_times(s3bfs_handle h, s3bfs_kernel_times *out);
+
+/* ---- test-only entry points (same kernels the traversal uses) ------------------------ */
+
+/* (b) alone: single-pass decoupled-look-back exclusive scan (Fig1 L14; DESIGN R5).
+ * in: device, n int32; out: device, n+1 int32 with out[0] = 0, out[i+1] = out[i] + in[i]
+ * (two's-complement wrap).  n == 0 writes out[0] = 0.  Enqueued on `stream`. */
+s3bfs_status s3bfs_debug_exclusive_scan(const int32_t *in, int32_t *out, int32_t n,
+                                        s3bfs_stream_t stream);
+
+/* (c) alone: Find-StartExpPoint (Fig1 L17) by the device search (DESIGN R8).
+ * excl: device, n_l+1 int32 exclusive degree scan (excl[n_l] = e_l > 0).  For worker
+ * w < p_l with s_w = w*chunk < e_l: out_u[w] = the u with excl[u] <= s_w < excl[u+1],
+ * out_off[w] = s_w - excl[u]; workers with s_w >= e_l get -1.  out_*: device, p_l int32. */
+s3bfs_status s3bfs_debug_find_start_points(const int32_t *excl, int32_t n_l, int32_t chunk,
+                                           int32_t p_l, int32_t *out_u, int32_t *out_off,
+                                           s3bfs_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* S3BFS_H_ */

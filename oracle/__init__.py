@@ -30,7 +30,7 @@ def build(force: bool = False) -> str:
     """Compile liboracle.so (gcc -O3).  Building the checker is not using it."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O3", "-march=native", "-std=c11", "-shared", "-fPIC",
+        subprocess.check_call(["gcc", "-O3", "-std=c11", "-shared", "-fPIC",
                                "-Wall", "-Wextra", "-o", tmp, _SRC])
         os.replace(tmp, _LIB)
     return _LIB

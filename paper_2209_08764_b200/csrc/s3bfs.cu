@@ -1,0 +1,451 @@
+// paper_2209_08764_b200/csrc/s3bfs.cu -- host side of the C ABI declared in include/s3bfs.h.
+//
+// Owns the workspace, resolves the (f) tunables (P_max from the occupancy of the level
+// kernels on this device, the grain, T0), and builds the captured level loop:
+//
+//   s3bfs_run:  k_init (Fig1 L1-L8)  ->  graph { WHILE(n_l > 0) {              Fig1 L9
+//                                          k_dispatch;                        (f)
+//                                          IF(tier 0) { k_small }             (f) tier 0
+//                                          IF(tier 1) { k_explore; k_compact }  (c)(d) / (e)(a)(b)
+//                                      } }
+//
+// The host crosses the host/device boundary once per traversal (enqueue); the level loop,
+// P_l and every per-level decision stay on the device (SURVEY.md s.8(a) row f, H6).
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "s3bfs_kernels.cuh"
+
+using namespace s3bfs;
+
+struct s3bfs_ctx {
+  int dev = 0, num_sms = 0;
+  int32_t n = 0;
+  int64_t nnz = 0;
+  const int32_t *ro = nullptr, *col = nullptr;
+  s3bfs_options opt{};
+  Params P{};
+  void *ws = nullptr;
+  size_t ws_bytes = 0;
+  int64_t cand_cap = 0;
+  size_t ks_smem = 0;
+  int loop_graph = 1;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t last_stream = nullptr;
+  bool ran = false;
+  Ctl *h_ctl = nullptr;  // pinned, host-loop mode
+  bool time_kernels = false;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  s3bfs_kernel_times kt{};
+  std::string err;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+s3bfs_status fail(s3bfs_ctx *h, s3bfs_status s, const std::string &msg) {
+  if (h) h->err = msg;
+  g_err = msg;
+  return s;
+}
+
+s3bfs_status cuda_fail(s3bfs_ctx *h, cudaError_t e, const char *what) {
+  std::string m = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return fail(h, e == cudaErrorMemoryAllocation ? S3BFS_ERR_OUT_OF_MEMORY : S3BFS_ERR_CUDA, m);
+}
+
+#define CK(h, call)                                      \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return cuda_fail(h, e_, #call); \
+  } while (0)
+
+bool is_device_ptr(const void *p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+int init_grid(const s3bfs_ctx *h) {
+  long long want = ((long long)h->n / 4 + 255) / 256;
+  long long cap = (long long)h->num_sms * 8;
+  if (want < 1) want = 1;
+  return (int)(want < cap ? want : cap);
+}
+
+s3bfs_status build_graph(s3bfs_ctx *h) {
+  cudaGraph_t g = nullptr;
+  CK(h, cudaGraphCreate(&g, 0));
+  h->graph = g;
+  cudaGraphConditionalHandle hw, h0, h1;
+  CK(h, cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault));
+  CK(h, cudaGraphConditionalHandleCreate(&h0, g, 0, cudaGraphCondAssignDefault));
+  CK(h, cudaGraphConditionalHandleCreate(&h1, g, 0, cudaGraphCondAssignDefault));
+  h->P.h_while = hw;
+  h->P.h_t0 = h0;
+  h->P.h_t1 = h1;
+  h->P.use_graph = 1;
+
+  cudaGraphNodeParams wp = {};
+  wp.type = cudaGraphNodeTypeConditional;
+  wp.conditional.handle = hw;
+  wp.conditional.type = cudaGraphCondTypeWhile;
+  wp.conditional.size = 1;
+  cudaGraphNode_t wnode;
+  CK(h, cudaGraphAddNode(&wnode, g, nullptr, 0, &wp));
+  cudaGraph_t body = wp.conditional.phGraph_out[0];
+
+  void *args[] = {&h->P};
+  auto kparams = [&](void *fn, int grid, int block, size_t smem) {
+    cudaKernelNodeParams k = {};
+    k.func = fn;
+    k.gridDim = dim3(grid);
+    k.blockDim = dim3(block);
+    k.sharedMemBytes = (unsigned)smem;
+    k.kernelParams = args;
+    return k;
+  };
+  cudaGraphNode_t nd, n0, n1;
+  cudaKernelNodeParams kd = kparams((void *)k_dispatch, 1, 1, 0);
+  CK(h, cudaGraphAddKernelNode(&nd, body, nullptr, 0, &kd));
+
+  cudaGraphNodeParams ip0 = {};
+  ip0.type = cudaGraphNodeTypeConditional;
+  ip0.conditional.handle = h0;
+  ip0.conditional.type = cudaGraphCondTypeIf;
+  ip0.conditional.size = 1;
+  CK(h, cudaGraphAddNode(&n0, body, &nd, 1, &ip0));
+  cudaGraph_t b0 = ip0.conditional.phGraph_out[0];
+  cudaGraphNode_t ks;
+  cudaKernelNodeParams kks = kparams((void *)k_small, 1, KS_THREADS, h->ks_smem);
+  CK(h, cudaGraphAddKernelNode(&ks, b0, nullptr, 0, &kks));
+
+  cudaGraphNodeParams ip1 = {};
+  ip1.type = cudaGraphNodeTypeConditional;
+  ip1.conditional.handle = h1;
+  ip1.conditional.type = cudaGraphCondTypeIf;
+  ip1.conditional.size = 1;
+  CK(h, cudaGraphAddNode(&n1, body, &n0, 1, &ip1));
+  cudaGraph_t b1 = ip1.conditional.phGraph_out[0];
+  cudaGraphNode_t kx, kc;
+  cudaKernelNodeParams kkx = kparams((void *)k_explore, h->P.p_max, KD_THREADS, 0);
+  CK(h, cudaGraphAddKernelNode(&kx, b1, nullptr, 0, &kkx));
+  cudaKernelNodeParams kkc = kparams((void *)k_compact, h->P.p_max, KD_THREADS, 0);
+  CK(h, cudaGraphAddKernelNode(&kc, b1, &kx, 1, &kkc));
+
+  CK(h, cudaGraphInstantiate(&h->exec, g, 0));
+  return S3BFS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *s3bfs_status_string(s3bfs_status s) {
+  switch (s) {
+    case S3BFS_OK: return "ok";
+    case S3BFS_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case S3BFS_ERR_UNSUPPORTED: return "unsupported";
+    case S3BFS_ERR_OUT_OF_MEMORY: return "out of memory";
+    case S3BFS_ERR_CUDA: return "CUDA error";
+    case S3BFS_ERR_INVALID_GRAPH: return "invalid CSR graph";
+  }
+  return "unknown status";
+}
+
+s3bfs_status s3bfs_last_error(s3bfs_handle h, const char **msg) {
+  if (!msg) return S3BFS_ERR_INVALID_ARGUMENT;
+  *msg = h ? h->err.c_str() : g_err.c_str();
+  return S3BFS_OK;
+}
+
+s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_t *row_offsets,
+                          const int32_t *col_indices, const s3bfs_options *opts,
+                          s3bfs_stream_t stream_) {
+  if (!out) return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (n <= 0) return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "n must be >= 1");
+  if (nnz < 0 || nnz > INT32_MAX) return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "nnz out of [0, INT32_MAX]");
+  if (!row_offsets || (nnz > 0 && !col_indices))
+    return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "null graph pointer");
+  if (!is_device_ptr(row_offsets) || (nnz > 0 && !is_device_ptr(col_indices)))
+    return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "graph arrays must be device memory");
+  cudaStream_t stream = (cudaStream_t)stream_;
+
+  s3bfs_ctx *h = new (std::nothrow) s3bfs_ctx;
+  if (!h) return fail(nullptr, S3BFS_ERR_OUT_OF_MEMORY, "host allocation failed");
+  auto bail = [&](s3bfs_status s) {
+    g_err = h->err;
+    s3bfs_destroy(h);
+    return s;
+  };
+  h->n = n;
+  h->nnz = nnz;
+  h->ro = row_offsets;
+  h->col = col_indices;
+  if (opts) h->opt = *opts;
+  cudaError_t e;
+  if ((e = cudaGetDevice(&h->dev)) != cudaSuccess) return bail(cuda_fail(h, e, "cudaGetDevice"));
+  cudaDeviceProp prop;
+  if ((e = cudaGetDeviceProperties(&prop, h->dev)) != cudaSuccess)
+    return bail(cuda_fail(h, e, "cudaGetDeviceProperties"));
+  if (prop.major != 10)
+    return bail(fail(h, S3BFS_ERR_UNSUPPORTED,
+                     "needs a compute capability 10.x device (sm_100a build), got " +
+                         std::to_string(prop.major) + "." + std::to_string(prop.minor)));
+  h->num_sms = prop.multiProcessorCount;
+
+  // ---- (f) tunables ----
+  int occ_x = 0, occ_c = 0;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_x, k_explore, KD_THREADS, 0)) != cudaSuccess)
+    return bail(cuda_fail(h, e, "occupancy(k_explore)"));
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, k_compact, KD_THREADS, 0)) != cudaSuccess)
+    return bail(cuda_fail(h, e, "occupancy(k_compact)"));
+  int occ = occ_x < occ_c ? occ_x : occ_c;
+  if (occ < 1) occ = 1;
+  int p_max = h->num_sms * occ;  // every CTA resident: the look-back never waits on a CTA
+  if (h->opt.max_ctas > 0 && h->opt.max_ctas < p_max) p_max = h->opt.max_ctas;
+  const int grain = h->opt.edges_per_cta > 0 ? h->opt.edges_per_cta : 16384;
+  int t0 = h->opt.tier0_max_edges == 0 ? KS_ECAP : h->opt.tier0_max_edges;
+  if (t0 > KS_ECAP) t0 = KS_ECAP;
+  if (h->opt.variant == 1) t0 = -1;
+  h->loop_graph = h->opt.loop_mode == 2 ? 0 : 1;
+  const int collect = h->opt.collect_stats >= 0 ? 1 : 0;
+
+  // ---- workspace (one allocation) ----
+  h->cand_cap = nnz + (int64_t)p_max * (KD_TILE + 1) + 64;
+  if (h->cand_cap >= INT32_MAX)
+    return bail(fail(h, S3BFS_ERR_UNSUPPORTED, "nnz too large for int32 candidate slots"));
+  const int stats_cap = n + 1 < (1 << 16) ? n + 1 : (1 << 16);
+  const size_t nb = (size_t)n * 4, nb1 = (size_t)(n + 1) * 4;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return o; };
+  const size_t o_owner = take(nb);
+  size_t o_f[2], o_frs[2], o_fex[2];
+  for (int i = 0; i < 2; ++i) { o_f[i] = take(nb); o_frs[i] = take(nb); o_fex[i] = take(nb1 + 16); }
+  const size_t o_cand = take((size_t)h->cand_cap * 4);
+  const size_t o_wcnt = take((size_t)p_max * KD_WARPS * 4);
+  const size_t o_status = take((size_t)p_max * 8);
+  const size_t o_ctl = take(sizeof(Ctl));
+  const size_t o_stats = take((size_t)stats_cap * sizeof(s3bfs_level_stat));
+  h->ws_bytes = off;
+  if ((e = cudaMalloc(&h->ws, h->ws_bytes)) != cudaSuccess) return bail(cuda_fail(h, e, "cudaMalloc(workspace)"));
+  char *base = (char *)h->ws;
+  Params &P = h->P;
+  P.ro = row_offsets;
+  P.col = col_indices;
+  P.n = n;
+  P.ctl = (Ctl *)(base + o_ctl);
+  P.owner = (int32_t *)(base + o_owner);
+  for (int i = 0; i < 2; ++i) {
+    P.f[i] = (int32_t *)(base + o_f[i]);
+    P.frs[i] = (int32_t *)(base + o_frs[i]);
+    P.fex[i] = (int32_t *)(base + o_fex[i]);
+  }
+  P.cand = (int32_t *)(base + o_cand);
+  P.wcnt = (int32_t *)(base + o_wcnt);
+  P.status = (unsigned long long *)(base + o_status);
+  P.stats = (s3bfs_level_stat *)(base + o_stats);
+  P.stats_cap = stats_cap;
+  P.p_max = p_max;
+  P.grain = grain;
+  P.t0 = t0;
+  P.variant = h->opt.variant == 1 ? 1 : 0;
+  P.collect_stats = collect;
+  P.use_graph = 0;
+  if ((e = cudaMemsetAsync(P.ctl, 0, sizeof(Ctl), stream)) != cudaSuccess) return bail(cuda_fail(h, e, "memset(ctl)"));
+  if ((e = cudaMemsetAsync(P.status, 0, (size_t)p_max * 8, stream)) != cudaSuccess) return bail(cuda_fail(h, e, "memset(status)"));
+  if (h->opt.debug_poison) {
+    k_poison<<<h->num_sms * 4, 256, 0, stream>>>(P.owner, n, (int)h->cand_cap);
+    if ((e = cudaGetLastError()) != cudaSuccess) return bail(cuda_fail(h, e, "k_poison"));
+  }
+
+  h->ks_smem = (size_t)(3 * KS_NCAP + 4 + KS_ECAP) * 4;
+  if ((e = cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->ks_smem)) != cudaSuccess)
+    return bail(cuda_fail(h, e, "cudaFuncSetAttribute(k_small)"));
+
+  if (h->opt.validate_csr) {
+    int *d_err = nullptr;
+    int h_err = 0;
+    if ((e = cudaMallocAsync((void **)&d_err, 4, stream)) != cudaSuccess) return bail(cuda_fail(h, e, "cudaMallocAsync"));
+    cudaMemsetAsync(d_err, 0, 4, stream);
+    k_validate<<<h->num_sms * 8, 256, 0, stream>>>(row_offsets, col_indices, n, nnz, d_err);
+    cudaMemcpyAsync(&h_err, d_err, 4, cudaMemcpyDeviceToHost, stream);
+    cudaFreeAsync(d_err, stream);
+    if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) return bail(cuda_fail(h, e, "validate_csr"));
+    if (h_err) {
+      std::string m = "CSR invalid:";
+      if (h_err & 1) m += " row_offsets[0] != 0;";
+      if (h_err & 2) m += " row_offsets decreasing;";
+      if (h_err & 4) m += " row_offsets[n] != nnz;";
+      if (h_err & 8) m += " column index out of [0, n);";
+      return bail(fail(h, S3BFS_ERR_INVALID_GRAPH, m));
+    }
+  }
+  if (h->loop_graph) {
+    s3bfs_status s = build_graph(h);
+    if (s != S3BFS_OK) return bail(s);
+  } else {
+    if ((e = cudaMallocHost((void **)&h->h_ctl, sizeof(Ctl))) != cudaSuccess) return bail(cuda_fail(h, e, "cudaMallocHost"));
+    if (h->opt.time_kernels) {
+      h->time_kernels = true;
+      for (auto &ev : h->ev)
+        if ((e = cudaEventCreate(&ev)) != cudaSuccess) return bail(cuda_fail(h, e, "cudaEventCreate"));
+    }
+  }
+  if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) return bail(cuda_fail(h, e, "create sync"));
+  *out = h;
+  return S3BFS_OK;
+}
+
+s3bfs_status s3bfs_run(s3bfs_handle h, int32_t source, int32_t *level, int32_t *parent,
+                       s3bfs_stream_t stream_) {
+  if (!h) return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "handle is NULL");
+  if (source < 0 || source >= h->n)
+    return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "source " + std::to_string(source) + " not in [0, n)");
+  if (!level || !parent) return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "level/parent is NULL");
+  if (!is_device_ptr(level) || !is_device_ptr(parent))
+    return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "level/parent must be device memory");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  k_init<<<init_grid(h), 256, 0, stream>>>(h->P, source, level, parent);
+  CK(h, cudaGetLastError());
+  h->last_stream = stream;
+  h->ran = true;
+  if (h->loop_graph) {
+    CK(h, cudaGraphLaunch(h->exec, stream));
+    return S3BFS_OK;
+  }
+  // host-driven loop: one control-block read per level (debug / timing mode)
+  h->kt = s3bfs_kernel_times{};
+  int pending = -1;  // tier of the launch whose events are not yet read
+  for (;;) {
+    CK(h, cudaMemcpyAsync(h->h_ctl, h->P.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, stream));
+    CK(h, cudaStreamSynchronize(stream));
+    if (pending >= 0) {
+      float a = 0.f, b = 0.f;
+      if (pending == TIER_SMALL) {
+        CK(h, cudaEventElapsedTime(&a, h->ev[0], h->ev[1]));
+        h->kt.small_ms += a;
+        h->kt.small_launches++;
+      } else {
+        CK(h, cudaEventElapsedTime(&a, h->ev[0], h->ev[1]));
+        CK(h, cudaEventElapsedTime(&b, h->ev[1], h->ev[2]));
+        h->kt.explore_ms += a;
+        h->kt.compact_ms += b;
+        h->kt.explore_launches++;
+        h->kt.compact_launches++;
+      }
+      pending = -1;
+    }
+    const Ctl c = *h->h_ctl;
+    if (c.tier == TIER_DONE) break;
+    if (h->time_kernels) CK(h, cudaEventRecord(h->ev[0], stream));
+    if (c.tier == TIER_SMALL) {
+      k_small<<<1, KS_THREADS, h->ks_smem, stream>>>(h->P);
+      if (h->time_kernels) CK(h, cudaEventRecord(h->ev[1], stream));
+    } else {
+      k_explore<<<c.p_l, KD_THREADS, 0, stream>>>(h->P);
+      if (h->time_kernels) CK(h, cudaEventRecord(h->ev[1], stream));
+      k_compact<<<c.p_l, KD_THREADS, 0, stream>>>(h->P);
+      if (h->time_kernels) CK(h, cudaEventRecord(h->ev[2], stream));
+    }
+    CK(h, cudaGetLastError());
+    if (h->time_kernels) pending = c.tier;
+  }
+  return S3BFS_OK;
+}
+
+s3bfs_status s3bfs_destroy(s3bfs_handle h) {
+  if (!h) return S3BFS_OK;
+  if (h->ran && h->last_stream) cudaStreamSynchronize(h->last_stream);
+  else cudaDeviceSynchronize();
+  if (h->exec) cudaGraphExecDestroy(h->exec);
+  if (h->graph) cudaGraphDestroy(h->graph);
+  if (h->ws) cudaFree(h->ws);
+  if (h->h_ctl) cudaFreeHost(h->h_ctl);
+  for (auto &ev : h->ev)
+    if (ev) cudaEventDestroy(ev);
+  delete h;
+  return S3BFS_OK;
+}
+
+s3bfs_status s3bfs_get_level_stats(s3bfs_handle h, s3bfs_level_stat *out, int32_t cap,
+                                   int32_t *num_levels) {
+  if (!h || !num_levels || cap < 0 || (cap > 0 && !out)) return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "bad arguments");
+  *num_levels = 0;
+  if (!h->ran) return S3BFS_OK;
+  CK(h, cudaStreamSynchronize(h->last_stream));
+  Ctl c;
+  CK(h, cudaMemcpy(&c, h->P.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+  *num_levels = c.num_levels;
+  int k = c.num_levels < cap ? c.num_levels : cap;
+  if (k > h->P.stats_cap) k = h->P.stats_cap;
+  if (k > 0) CK(h, cudaMemcpy(out, h->P.stats, (size_t)k * sizeof(s3bfs_level_stat), cudaMemcpyDeviceToHost));
+  return S3BFS_OK;
+}
+
+s3bfs_status s3bfs_get_kernel_times(s3bfs_handle h, s3bfs_kernel_times *out) {
+  if (!h || !out) return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (h->ran) CK(h, cudaStreamSynchronize(h->last_stream));
+  *out = h->kt;
+  return S3BFS_OK;
+}
+
+s3bfs_status s3bfs_get_info(s3bfs_handle h, s3bfs_info *out) {
+  if (!h || !out) return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "bad arguments");
+  out->num_sms = h->num_sms;
+  out->p_max = h->P.p_max;
+  out->edges_per_cta = h->P.grain;
+  out->tier0_max_edges = h->P.t0;
+  out->kd_threads = KD_THREADS;
+  out->kd_tile_edges = KD_TILE;
+  out->ksmall_threads = KS_THREADS;
+  out->ksmall_max_frontier = KS_NCAP;
+  out->workspace_bytes = (int64_t)h->ws_bytes;
+  return S3BFS_OK;
+}
+
+s3bfs_status s3bfs_debug_exclusive_scan(const int32_t *in, int32_t *out, int32_t n,
+                                        s3bfs_stream_t stream_) {
+  if (n < 0 || !out || (n > 0 && !in)) return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "bad arguments");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (n == 0) {
+    cudaError_t e = cudaMemsetAsync(out, 0, 4, stream);
+    return e == cudaSuccess ? S3BFS_OK : cuda_fail(nullptr, e, "memset");
+  }
+  const int tiles = (int)(((long long)n + SCAN_TILE - 1) / SCAN_TILE);
+  unsigned long long *status = nullptr;
+  cudaError_t e = cudaMallocAsync((void **)&status, (size_t)tiles * 8, stream);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaMallocAsync(status)");
+  cudaMemsetAsync(status, 0, (size_t)tiles * 8, stream);
+  k_scan_u32<<<tiles, SCAN_THREADS, 0, stream>>>(in, out, n, status);
+  e = cudaGetLastError();
+  cudaFreeAsync(status, stream);
+  return e == cudaSuccess ? S3BFS_OK : cuda_fail(nullptr, e, "k_scan_u32");
+}
+
+s3bfs_status s3bfs_debug_find_start_points(const int32_t *excl, int32_t n_l, int32_t chunk,
+                                           int32_t p_l, int32_t *out_u, int32_t *out_off,
+                                           s3bfs_stream_t stream_) {
+  if (!excl || n_l < 1 || chunk < 1 || p_l < 0 || (p_l > 0 && (!out_u || !out_off)))
+    return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (p_l == 0) return S3BFS_OK;
+  const int threads = 256;
+  const long long blocks = ((long long)p_l * 32 + threads - 1) / threads;
+  k_find_start<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream_>>>(excl, n_l, chunk, p_l, out_u, out_off);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? S3BFS_OK : cuda_fail(nullptr, e, "k_find_start");
+}
+
+}  // extern "C"

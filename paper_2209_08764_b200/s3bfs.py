@@ -1,0 +1,249 @@
+"""Thin ctypes binding over libs3bfs.so (include/s3bfs.h) -- argument marshalling only.
+
+Every step of the traversal runs in the CUDA kernels of ``csrc/``; this module converts
+torch tensors to device pointers and torch streams to ``cudaStream_t``.  There is no CPU
+fallback: if the library is missing or fails to load, every call raises.
+Names follow the C ABI (``s3bfs_create`` / ``s3bfs_run`` / ``s3bfs_destroy`` ...).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import build as _build
+
+LIB_PATH = _build.LIB
+_lib = None
+
+S3BFS_OK = 0
+STATUS_NAMES = {0: "ok", 1: "invalid argument", 2: "unsupported", 3: "out of memory",
+                4: "CUDA error", 5: "invalid CSR graph"}
+
+EXPORTED = ("s3bfs_create", "s3bfs_run", "s3bfs_destroy", "s3bfs_status_string",
+            "s3bfs_last_error", "s3bfs_get_level_stats", "s3bfs_get_info", "s3bfs_get_kernel_times",
+            "s3bfs_debug_exclusive_scan", "s3bfs_debug_find_start_points")
+
+
+class S3BFSError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str = ""):
+        self.status = status
+        super().__init__(f"{where}: {STATUS_NAMES.get(status, status)}"
+                         + (f" -- {detail}" if detail else ""))
+
+
+class Options(ctypes.Structure):
+    """s3bfs_options (zero = defaults)."""
+    _fields_ = [("edges_per_cta", ctypes.c_int32), ("tier0_max_edges", ctypes.c_int32),
+                ("loop_mode", ctypes.c_int32), ("collect_stats", ctypes.c_int32),
+                ("validate_csr", ctypes.c_int32), ("variant", ctypes.c_int32),
+                ("max_ctas", ctypes.c_int32), ("debug_poison", ctypes.c_int32),
+                ("time_kernels", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+
+
+class LevelStat(ctypes.Structure):
+    _fields_ = [("level", ctypes.c_int32), ("n_l", ctypes.c_int32), ("e_l", ctypes.c_int32),
+                ("tier", ctypes.c_int32), ("grid", ctypes.c_int32),
+                ("candidates", ctypes.c_int32), ("kept", ctypes.c_int32),
+                ("pad", ctypes.c_int32), ("t_begin_ns", ctypes.c_uint64),
+                ("t_end_ns", ctypes.c_uint64), ("t_explore_begin_ns", ctypes.c_uint64),
+                ("t_explore_end_ns", ctypes.c_uint64)]
+
+
+class KernelTimes(ctypes.Structure):
+    _fields_ = [("explore_ms", ctypes.c_double), ("compact_ms", ctypes.c_double),
+                ("small_ms", ctypes.c_double), ("explore_launches", ctypes.c_int32),
+                ("compact_launches", ctypes.c_int32), ("small_launches", ctypes.c_int32),
+                ("pad", ctypes.c_int32)]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("num_sms", ctypes.c_int32), ("p_max", ctypes.c_int32),
+                ("edges_per_cta", ctypes.c_int32), ("tier0_max_edges", ctypes.c_int32),
+                ("kd_threads", ctypes.c_int32), ("kd_tile_edges", ctypes.c_int32),
+                ("ksmall_threads", ctypes.c_int32), ("ksmall_max_frontier", ctypes.c_int32),
+                ("workspace_bytes", ctypes.c_int64)]
+
+
+def load(build_if_missing: bool = True):
+    """Load libs3bfs.so (building it in-tree first if absent/stale and nvcc exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if build_if_missing:
+        try:
+            _build.build()
+        except Exception as exc:  # noqa: BLE001 -- fall through to the loud load failure
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(f"libs3bfs.so missing and the build failed: {exc}") from exc
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"libs3bfs.so not found at {LIB_PATH}: run __graft_entry__.build()")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    lib.s3bfs_create.argtypes = [ctypes.POINTER(vp), i32, i64, vp, vp, ctypes.POINTER(Options), vp]
+    lib.s3bfs_run.argtypes = [vp, i32, vp, vp, vp]
+    lib.s3bfs_destroy.argtypes = [vp]
+    lib.s3bfs_status_string.argtypes = [ctypes.c_int]
+    lib.s3bfs_status_string.restype = ctypes.c_char_p
+    lib.s3bfs_last_error.argtypes = [vp, ctypes.POINTER(ctypes.c_char_p)]
+    lib.s3bfs_get_level_stats.argtypes = [vp, ctypes.POINTER(LevelStat), i32, ctypes.POINTER(i32)]
+    lib.s3bfs_get_info.argtypes = [vp, ctypes.POINTER(Info)]
+    lib.s3bfs_get_kernel_times.argtypes = [vp, ctypes.POINTER(KernelTimes)]
+    lib.s3bfs_debug_exclusive_scan.argtypes = [vp, vp, i32, vp]
+    lib.s3bfs_debug_find_start_points.argtypes = [vp, i32, i32, i32, vp, vp, vp]
+    for name in EXPORTED:
+        if name != "s3bfs_status_string":
+            getattr(lib, name).restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def _detail(handle) -> str:
+    msg = ctypes.c_char_p()
+    load().s3bfs_last_error(handle, ctypes.byref(msg))
+    return (msg.value or b"").decode(errors="replace")
+
+
+def _check(rc: int, where: str, handle=None) -> None:
+    if rc != S3BFS_OK:
+        raise S3BFSError(rc, where, _detail(handle))
+
+
+def _ptr(t) -> int:
+    """Device pointer of a CUDA tensor (raises for CPU tensors: no host fallback)."""
+    if t is None:
+        return 0
+    if not t.is_cuda:
+        raise ValueError("tensor must live on a CUDA device")
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return int(t.data_ptr())
+
+
+def _stream(stream) -> int:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def s3bfs_create(row_offsets, col_indices, options: Options | None = None, stream=None):
+    """s3bfs_create over int32 device tensors (borrowed: keep them alive). Returns a handle."""
+    import torch
+    for name, t in (("row_offsets", row_offsets), ("col_indices", col_indices)):
+        if t.dtype != torch.int32:
+            raise ValueError(f"{name} must be int32")
+    h = ctypes.c_void_p()
+    n = row_offsets.numel() - 1
+    nnz = col_indices.numel()
+    opts = ctypes.byref(options) if options is not None else None
+    col_p = _ptr(col_indices) if nnz else 0
+    rc = load().s3bfs_create(ctypes.byref(h), n, nnz, _ptr(row_offsets), col_p, opts,
+                             _stream(stream))
+    _check(rc, "s3bfs_create")
+    return h
+
+
+def s3bfs_run(handle, source: int, level, parent, stream=None) -> None:
+    """Enqueue Parallel-BFS(source); level/parent: int32 device tensors [n]."""
+    _check(load().s3bfs_run(handle, int(source), _ptr(level), _ptr(parent), _stream(stream)),
+           "s3bfs_run", handle)
+
+
+def s3bfs_run_ptr(handle, source: int, level_ptr: int, parent_ptr: int, stream_ptr: int) -> None:
+    """Raw-pointer form of s3bfs_run (for timed loops)."""
+    _check(load().s3bfs_run(handle, int(source), level_ptr, parent_ptr, stream_ptr),
+           "s3bfs_run", handle)
+
+
+def s3bfs_destroy(handle) -> None:
+    if handle:
+        _check(load().s3bfs_destroy(handle), "s3bfs_destroy")
+
+
+def s3bfs_status_string(status: int) -> str:
+    return load().s3bfs_status_string(int(status)).decode()
+
+
+def s3bfs_get_level_stats(handle, cap: int = 1 << 16) -> np.ndarray:
+    """Per-level records of the last run as a numpy structured array."""
+    buf = (LevelStat * cap)()
+    num = ctypes.c_int32()
+    _check(load().s3bfs_get_level_stats(handle, buf, cap, ctypes.byref(num)),
+           "s3bfs_get_level_stats", handle)
+    k = min(num.value, cap)
+    dt = np.dtype([("level", "i4"), ("n_l", "i4"), ("e_l", "i4"), ("tier", "i4"),
+                   ("grid", "i4"), ("candidates", "i4"), ("kept", "i4"), ("pad", "i4"),
+                   ("t_begin_ns", "u8"), ("t_end_ns", "u8"), ("t_explore_begin_ns", "u8"),
+                   ("t_explore_end_ns", "u8")])
+    out = np.frombuffer(bytes(buf)[: k * ctypes.sizeof(LevelStat)], dtype=dt).copy()
+    if num.value > cap:
+        raise S3BFSError(0, "s3bfs_get_level_stats", f"{num.value} levels > cap {cap}")
+    return out
+
+
+def s3bfs_get_info(handle) -> dict:
+    info = Info()
+    _check(load().s3bfs_get_info(handle, ctypes.byref(info)), "s3bfs_get_info", handle)
+    return {f: getattr(info, f) for f, _ in Info._fields_}
+
+
+def s3bfs_get_kernel_times(handle) -> dict:
+    kt = KernelTimes()
+    _check(load().s3bfs_get_kernel_times(handle, ctypes.byref(kt)), "s3bfs_get_kernel_times",
+           handle)
+    return {f: getattr(kt, f) for f, _ in KernelTimes._fields_ if f != "pad"}
+
+
+def s3bfs_debug_exclusive_scan(inp, out, stream=None) -> None:
+    n = inp.numel()
+    if out.numel() != n + 1:
+        raise ValueError("out must have n+1 entries")
+    _check(load().s3bfs_debug_exclusive_scan(_ptr(inp) if n else 0, _ptr(out), n,
+                                             _stream(stream)), "s3bfs_debug_exclusive_scan")
+
+
+def s3bfs_debug_find_start_points(excl, chunk: int, p_l: int, out_u, out_off,
+                                  stream=None) -> None:
+    n_l = excl.numel() - 1
+    _check(load().s3bfs_debug_find_start_points(_ptr(excl), n_l, int(chunk), int(p_l),
+                                                _ptr(out_u), _ptr(out_off), _stream(stream)),
+           "s3bfs_debug_find_start_points")
+
+
+class S3BFS:
+    """Convenience owner of a handle over device CSR tensors (kept alive here)."""
+
+    def __init__(self, row_offsets, col_indices, options: Options | None = None, stream=None):
+        self.row_offsets = row_offsets
+        self.col_indices = col_indices
+        self.n = row_offsets.numel() - 1
+        self.handle = s3bfs_create(row_offsets, col_indices, options, stream)
+
+    def run(self, source: int, level=None, parent=None, stream=None):
+        import torch
+        dev = self.row_offsets.device
+        if level is None:
+            level = torch.empty(self.n, dtype=torch.int32, device=dev)
+        if parent is None:
+            parent = torch.empty(self.n, dtype=torch.int32, device=dev)
+        s3bfs_run(self.handle, source, level, parent, stream)
+        return level, parent
+
+    def level_stats(self) -> np.ndarray:
+        return s3bfs_get_level_stats(self.handle)
+
+    def info(self) -> dict:
+        return s3bfs_get_info(self.handle)
+
+    def close(self) -> None:
+        if self.handle:
+            s3bfs_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
