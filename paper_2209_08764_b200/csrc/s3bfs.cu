@@ -235,6 +235,8 @@ s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32
   size_t o_f[2], o_frs[2], o_fex[2];
   for (int i = 0; i < 2; ++i) { o_f[i] = take(nb); o_frs[i] = take(nb); o_fex[i] = take(nb1 + 16); }
   const size_t o_cand = take((size_t)h->cand_cap * 4);
+  const size_t o_crd = take((size_t)h->cand_cap * 8);
+  const size_t o_bm = take(((size_t)n + 31) / 32 * 4);
   const size_t o_wcnt = take((size_t)p_max * KD_WARPS * 4);
   const size_t o_status = take((size_t)p_max * 8);
   const size_t o_ctl = take(sizeof(Ctl));
@@ -254,6 +256,8 @@ s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32
     P.fex[i] = (int32_t *)(base + o_fex[i]);
   }
   P.cand = (int32_t *)(base + o_cand);
+  P.cand_rd = (int2 *)(base + o_crd);
+  P.bm = (uint32_t *)(base + o_bm);
   P.wcnt = (int32_t *)(base + o_wcnt);
   P.status = (unsigned long long *)(base + o_status);
   P.stats = (s3bfs_level_stat *)(base + o_stats);

@@ -29,9 +29,7 @@ namespace s3bfs {
 // ---- compile-time geometry --------------------------------------------------------------
 constexpr int KD_THREADS = 512;                 // k_explore / k_compact CTA size
 constexpr int KD_WARPS = KD_THREADS / 32;
-constexpr int KD_ITEMS = 8;                     // edge slots per thread per tile
-constexpr int KD_TILE = KD_THREADS * KD_ITEMS;  // 4096 edges per tile
-constexpr int KD_MASKW = KD_TILE / 32;          // row-start mask words per tile
+constexpr int KD_TILE = 4096;                   // candidate-buffer slack per CTA (edges)
 constexpr int KS_THREADS = 1024;                // k_small CTA size
 constexpr int KS_ECAP = 8192;                   // T0 maximum (edges per tier-0 level)
 constexpr int KS_NCAP = KS_ECAP;                // frontier capacity of tier 0 (kept <= e_l)
@@ -71,6 +69,8 @@ struct Params {
   int32_t *owner;
   int32_t *f[2], *frs[2], *fex[2];  // frontier ids, their row starts, exclusive degree scan
   int32_t *cand;
+  int2 *cand_rd;          // (row start, degree) of kept candidates, pass 1 -> pass 2 of k_compact
+  uint32_t *bm;           // visited bitmap: bit v set => level[v] != -1 (a filter; level[] rules)
   int32_t *wcnt;
   unsigned long long *status;
   s3bfs_level_stat *stats;
@@ -92,6 +92,36 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 __device__ __forceinline__ int ld_weak(const int32_t *p) {
   int v;
   asm volatile("ld.global.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+// L2 eviction policies (createpolicy): the adjacency is streamed once per level and must not
+// evict the status array, which every arc probes at random.
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long policy_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// read-only stream (col_indices): non-coherent, no L1 allocation, L2 evict-first
+__device__ __forceinline__ int ldg_stream(const int32_t *p, unsigned long long pol) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+               : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+// status probe of level[] (racing array, weak load) with an L2 evict-last hint
+__device__ __forceinline__ int ld_status(const int32_t *p, unsigned long long pol) {
+  int v;
+  asm volatile("ld.global.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_status_u32(const uint32_t *p, unsigned long long pol) {
+  uint32_t v;
+  asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
   return v;
 }
 __device__ __forceinline__ void st_weak(int32_t *p, int v) {
@@ -245,11 +275,10 @@ __device__ void decide(const Params &P, Ctl *c, int32_t n_l, int32_t e_l) {
   if (pt < 1) pt = 1;
   const long long chunk = ((long long)e_l + pt - 1) / pt;
   const long long p_l = ((long long)e_l + chunk - 1) / chunk;
-  const long long nt = (chunk + KD_TILE - 1) / KD_TILE;
   c->tier = TIER_LARGE;
   c->p_l = (int32_t)p_l;
   c->chunk = (int32_t)chunk;
-  c->wcap = (int32_t)(nt * KD_ITEMS * 32);
+  c->wcap = (int32_t)((chunk + KD_WARPS - 1) / KD_WARPS);  // edges (and candidates) per warp
 }
 
 // ---- init (Fig1 L1-L8) ----------------------------------------------------------------------
@@ -280,6 +309,9 @@ __global__ void k_init(Params P, int32_t s, int32_t *level, int32_t *parent) {
     level[i] = (i == s) ? 0 : -1;
     parent[i] = (i == s) ? s : -1;
   }
+  const long long nw = ((long long)n + 31) >> 5;  // visited bitmap: only the source
+  for (long long i = gtid; i < nw; i += gstride)
+    P.bm[i] = (i == (s >> 5)) ? (1u << (s & 31)) : 0u;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     Ctl *c = P.ctl;
     const int r0 = P.ro[s], r1 = P.ro[s + 1];
@@ -309,31 +341,28 @@ __global__ void k_dispatch(Params P) {
 }
 
 // ---- (c)+(d): k_explore ----------------------------------------------------------------------
-// CTA b < P_l owns global edges [b*chunk, min((b+1)*chunk, e_l)) of the level (the paper's
-// worker with an (almost) equal share, Fig1 L16-L17).  It walks them in tiles of
-// KD_TILE edges.  Per tile: the frontier vertices overlapping the tile are written at their
-// first slot (sx = vertex id x, sb = row_start(x) - excl(u)), a ballot builds a row-start bit
-// mask, and every edge slot finds its vertex as the nearest start at or before it (one
-// broadcast LDS per warp).  Slot s of thread t is i*KD_THREADS + t, so a warp's 32 lanes read
-// 32 consecutive col entries: coalesced streaming of the adjacency (Fig1 L18).
+// CTA b < P_l owns global edges [b*chunk, min((b+1)*chunk, e_l)) of the level, split evenly
+// over its warps: each warp is one of the paper's workers with an (almost) equal share of the
+// level's edges (Fig1 L16-L17).  A warp finds its start vertex with the 32-ary search
+// (c), then walks its edges in groups of 32 -- lane i takes edge e+i, so a group reads 32
+// consecutive col entries (coalesced streaming, Fig1 L18).  Edge -> frontier vertex mapping
+// uses a register window of 32 consecutive frontier vertices (their degree-scan entries,
+// ids and row starts): a 5-step shuffle search per lane, no shared memory, no CTA barrier,
+// so warps progress independently and keep KX_GROUPS groups of loads in flight.
 // Discovery (EXPLORE-VERTEX): if level[v] == -1 then level[v] = l+1, parent[v] = x,
 // Owner[v] = slot, cand[slot] = v -- plain stores, the paper's benign race, no atomics.
 // The candidate slot is a unique id (R4), so Owner dedup keeps exactly one copy even when
 // two lanes of one warp discover v together.
-__global__ void __launch_bounds__(KD_THREADS, 2) k_explore(Params P) {
+constexpr int KX_GROUPS = 8;
+constexpr int KX_MIN_BLOCKS = 2;
+__global__ void __launch_bounds__(KD_THREADS, KX_MIN_BLOCKS) k_explore(Params P) {
   Ctl *c = P.ctl;
   if (c->tier != TIER_LARGE) return;
   const int b = blockIdx.x;
   const int p_l = c->p_l;
   if (b >= p_l) return;
-  __shared__ int32_t sx[KD_TILE];
-  __shared__ int32_t sb[KD_TILE];
-  __shared__ uint32_t smask[KD_MASKW];
-  __shared__ int32_t slast[KD_MASKW];
-  __shared__ int32_t s_ucur, s_unext;
-
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int n_l = c->n_l, e_l = c->e_l, chunk = c->chunk, cur = c->cur;
+  const int n_l = c->n_l, e_l = c->e_l, chunk = c->chunk, cur = c->cur, wcap = c->wcap;
   const int new_level = c->level + 1;  // Fig1 L10: discoveries get l+1 (R11)
   int32_t *__restrict__ level = c->level_out;
   int32_t *__restrict__ parent = c->parent_out;
@@ -343,6 +372,7 @@ __global__ void __launch_bounds__(KD_THREADS, 2) k_explore(Params P) {
   const int32_t *__restrict__ col = P.col;
   int32_t *__restrict__ owner = P.owner;
   int32_t *__restrict__ cand = P.cand;
+  const uint32_t *__restrict__ bm = P.bm;
 
   if (tid == 0) {
     P.status[b] = 0ull;  // reset k_compact's look-back word for this level
@@ -350,104 +380,69 @@ __global__ void __launch_bounds__(KD_THREADS, 2) k_explore(Params P) {
   }
   const int E0 = b * chunk;
   const int E1 = min(E0 + chunk, e_l);
-  const int segbase = (b * KD_WARPS + warp) * c->wcap;
+  const int e_begin = min(E0 + warp * wcap, E1);
+  const int e_end = min(e_begin + wcap, E1);
+  const int segbase = (b * KD_WARPS + warp) * wcap;
+  const unsigned long long pol_stream = policy_evict_first();
+  const unsigned long long pol_status = policy_evict_last();
   int wcount = 0;
-
-  if (warp == 0) {
-    const int u = warp_search(fex, n_l, E0);
-    if (lane == 0) s_ucur = u;
-  }
-  for (int s = tid * 4; s < KD_TILE; s += KD_THREADS * 4)
-    *reinterpret_cast<int4 *>(sx + s) = make_int4(-1, -1, -1, -1);
-  __syncthreads();
-
-  for (int t0 = E0; t0 < E1; t0 += KD_TILE) {
-    const int t1 = min(t0 + KD_TILE, E1);
-    // 1. place the frontier vertices of this tile at their first slot
-    for (int ubase = s_ucur;; ubase += KD_THREADS) {
-      const int u = ubase + tid;
-      bool past = true;
-      if (u < n_l) {
-        const int a = __ldg(fex + u), e = __ldg(fex + u + 1);
-        past = a >= t1;
-        if (!past) {
-          if (e > a && e > t0) {
-            const int s = max(a, t0) - t0;
-            sx[s] = __ldg(fx + u);
-            sb[s] = __ldg(frs + u) - a;
-          }
-          // the last vertex starting before t1 (unique: a < t1 <= e): the next tile's walk
-          // starts here, which also covers zero-degree vertices sitting at t1
-          if (e >= t1) s_unext = u;
+  if (e_begin < e_end) {
+    int u0 = warp_search(fex, n_l, e_begin);  // Find-StartExpPoint (c)
+    int wex, wx, wb, lim;
+    auto load_window = [&](int base) {
+      const int u = base + lane;
+      wex = (u < n_l) ? __ldg(fex + u) : 0x7fffffff;
+      wx = (u < n_l) ? __ldg(fx + u) : 0;
+      wb = (u < n_l) ? __ldg(frs + u) - wex : 0;
+      lim = __ldg(fex + min(base + 32, n_l));
+    };
+    load_window(u0);
+    int e = e_begin;
+    while (e < e_end) {
+      while (lim <= e) {  // window exhausted (also skips runs of zero-degree vertices, C9)
+        u0 += 32;
+        load_window(u0);
+      }
+      const int bend = min(e_end, lim);
+      int v[KX_GROUPS], xv[KX_GROUPS];
+#pragma unroll
+      for (int g = 0; g < KX_GROUPS; ++g) {
+        const int my_e = e + g * 32 + lane;
+        int j = 0;  // largest window slot with excl <= my_e
+#pragma unroll
+        for (int s = 16; s >= 1; s >>= 1) {
+          const int cj = __shfl_sync(0xffffffffu, wex, j + s);
+          if (cj <= my_e) j += s;
         }
+        xv[g] = __shfl_sync(0xffffffffu, wx, j);
+        const int pos = __shfl_sync(0xffffffffu, wb, j) + my_e;
+        v[g] = (my_e < bend) ? ldg_stream(col + pos, pol_stream) : -1;
       }
-      if (__syncthreads_or(past)) break;
-    }
-    // 2. row-start mask (one ballot per 32 slots) and the last start before each word
-    for (int w = warp; w < KD_MASKW; w += KD_WARPS) {
-      const unsigned m = __ballot_sync(0xffffffffu, sx[w * 32 + lane] != -1);
-      if (lane == 0) smask[w] = m;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      constexpr int WPL = KD_MASKW / 32;
-      int hb[WPL];
-      int lmax = -1;
+      // status: the visited bitmap first (2 MB at scale 24: stays in L2), level[] only when the
+      // bit is clear (unvisited, or discovered earlier in this same level)
+      uint32_t bw[KX_GROUPS];
 #pragma unroll
-      for (int j = 0; j < WPL; ++j) {
-        const int w = lane * WPL + j;
-        const unsigned m = smask[w];
-        hb[j] = m ? (w * 32 + 31 - __clz(m)) : -1;
-        lmax = max(lmax, hb[j]);
+      for (int g = 0; g < KX_GROUPS; ++g)
+        bw[g] = (v[g] >= 0) ? ld_status_u32(bm + (v[g] >> 5), pol_status) : 0xffffffffu;
+      int lv[KX_GROUPS];
+#pragma unroll
+      for (int g = 0; g < KX_GROUPS; ++g)
+        lv[g] = ((bw[g] >> (v[g] & 31)) & 1u) ? 0 : ld_status(level + v[g], pol_status);
+#pragma unroll
+      for (int g = 0; g < KX_GROUPS; ++g) {
+        const bool disc = lv[g] == -1;
+        const unsigned m = __ballot_sync(0xffffffffu, disc);
+        if (disc) {
+          const int slot = segbase + wcount + __popc(m & lanemask_lt());
+          st_weak(level + v[g], new_level);
+          st_weak(parent + v[g], xv[g]);
+          st_weak(owner + v[g], slot);
+          cand[slot] = v[g];
+        }
+        wcount += __popc(m);
       }
-      int run = lmax;  // exclusive max-scan across lanes
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, run, o);
-        if (lane >= o) run = max(run, y);
-      }
-      int ex = __shfl_up_sync(0xffffffffu, run, 1);
-      if (lane == 0) ex = -1;
-#pragma unroll
-      for (int j = 0; j < WPL; ++j) {
-        slast[lane * WPL + j] = ex;
-        ex = max(ex, hb[j]);
-      }
+      e = min(e + KX_GROUPS * 32, bend);
     }
-    if (tid == 0) s_ucur = s_unext;
-    __syncthreads();
-    // 3. stream the tile's edges: col loads first, then status loads (memory-level parallelism)
-    int v[KD_ITEMS], xv[KD_ITEMS];
-#pragma unroll
-    for (int i = 0; i < KD_ITEMS; ++i) {
-      const int s = i * KD_THREADS + tid;
-      const int e = t0 + s;
-      const int w = s >> 5;
-      const unsigned m = smask[w] & (0xffffffffu >> (31 - (s & 31)));
-      const int p = m ? (w * 32 + 31 - __clz(m)) : slast[w];
-      xv[i] = sx[p];
-      v[i] = (e < t1) ? __ldg(col + (sb[p] + e)) : -1;
-    }
-    int lv[KD_ITEMS];
-#pragma unroll
-    for (int i = 0; i < KD_ITEMS; ++i) lv[i] = (v[i] >= 0) ? ld_weak(level + v[i]) : 0;
-#pragma unroll
-    for (int i = 0; i < KD_ITEMS; ++i) {
-      const bool disc = lv[i] == -1;
-      const unsigned m = __ballot_sync(0xffffffffu, disc);
-      if (disc) {
-        const int slot = segbase + wcount + __popc(m & lanemask_lt());
-        st_weak(level + v[i], new_level);
-        st_weak(parent + v[i], xv[i]);
-        st_weak(owner + v[i], slot);
-        cand[slot] = v[i];
-      }
-      wcount += __popc(m);
-    }
-    __syncthreads();  // all reads of sx/sb/smask/slast for this tile are done
-    for (int s = tid * 4; s < KD_TILE; s += KD_THREADS * 4)
-      *reinterpret_cast<int4 *>(sx + s) = make_int4(-1, -1, -1, -1);
-    __syncthreads();
   }
   if (lane == 0) P.wcnt[b * KD_WARPS + warp] = wcount;
 }
@@ -476,18 +471,27 @@ __global__ void __launch_bounds__(KD_THREADS, 2) k_compact(Params P) {
   const int cnt = P.wcnt[b * KD_WARPS + warp];
   if (b == 0 && tid == 0) c->t_kx_end = globaltimer();
 
+  int2 *__restrict__ crd = P.cand_rd;
   int kept = 0, dsum = 0;
   for (int k0 = 0; k0 < cnt; k0 += 32) {
     const int k = k0 + lane;
     bool keep = false;
-    int v = 0, d = 0;
+    int v = 0, r0 = 0, d = 0;
     if (k < cnt) {
       v = cand[seg + k];
       keep = ld_weak(owner + v) == seg + k;  // Fig1 L22: "if Owner[v] = i"
-      if (keep) d = __ldg(ro + v + 1) - __ldg(ro + v);
+      if (keep) {
+        r0 = __ldg(ro + v);
+        d = __ldg(ro + v + 1) - r0;
+        atomicOr(P.bm + (v >> 5), 1u << (v & 31));  // publish "visited" (filter only, R17)
+      }
     }
     const unsigned m = __ballot_sync(0xffffffffu, keep);
-    if (keep) cand[seg + kept + __popc(m & lanemask_lt())] = v;
+    if (keep) {
+      const int q = seg + kept + __popc(m & lanemask_lt());
+      cand[q] = v;
+      crd[q] = make_int2(r0, d);
+    }
     kept += __popc(m);
     dsum += d;
   }
@@ -523,8 +527,9 @@ __global__ void __launch_bounds__(KD_THREADS, 2) k_compact(Params P) {
     int v = 0, r0 = 0, d = 0;
     if (k < kept) {
       v = cand[seg + k];
-      r0 = __ldg(ro + v);
-      d = __ldg(ro + v + 1) - r0;
+      const int2 rd = crd[seg + k];
+      r0 = rd.x;
+      d = rd.y;
     }
     const int inc = warp_incl_scan(d);
     if (k < kept) {
@@ -657,6 +662,10 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
 #pragma unroll
     for (int i = 0; i < KS_IPT; ++i) {
       if (kv[i] >= 0) {
+        // visited bit: plain read-modify-write, no atomic -- a racing update can only lose a
+        // bit (the filter then falls back to level[]), never set one wrongly
+        uint32_t *wp = P.bm + (kv[i] >> 5);
+        *(volatile uint32_t *)wp = *(volatile uint32_t *)wp | (1u << (kv[i] & 31));
         sf[kpos] = kv[i];
         srs[kpos] = kr[i];
         sex[kpos] = dpos;
