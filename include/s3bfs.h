@@ -72,7 +72,10 @@ typedef struct {
                               prove it is never read before written (DESIGN R3) */
   int32_t time_kernels;    /* 1 (host-loop mode only): bracket every kernel launch with CUDA
                               events on the run's stream; read by s3bfs_get_kernel_times */
-  int32_t reserved[7];
+  int32_t reorder;         /* 0/1: create builds an internal copy of the graph relabelled by
+                              descending degree (outputs stay in caller ids); -1: traverse the
+                              caller's arrays directly (no copy) */
+  int32_t reserved[6];
 } s3bfs_options;
 
 /* One record per BFS level (the SPEC LevelStats analogue).  n_l = |frontier|
@@ -92,7 +95,9 @@ typedef struct {
  * row_offsets: device, n+1 int32, BORROWED (caller keeps it alive and unmodified until
  * destroy).  col_indices: device, nnz int32, borrowed (may be NULL iff nnz == 0).
  * Requires 1 <= n, 0 <= nnz <= INT32_MAX - workspace slack.  The handle owns its
- * workspace (Owner[n], two frontier buffers, candidate buffer, control block, stats).
+ * workspace (per-vertex records, two frontier buffers, candidate buffer, visited bitmap, claim
+ * tags, control block, stats) and, unless opts->reorder < 0, a degree-ordered internal copy
+ * of the graph (4 nnz + 8 n more bytes), built here on `stream`.
  * May synchronise `stream`.  On failure *out is set to NULL. */
 s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_t *row_offsets,
                           const int32_t *col_indices, const s3bfs_options *opts,

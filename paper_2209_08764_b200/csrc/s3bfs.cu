@@ -18,6 +18,8 @@
 #include <new>
 #include <string>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "s3bfs_kernels.cuh"
 
 using namespace s3bfs;
@@ -30,6 +32,8 @@ struct s3bfs_ctx {
   s3bfs_options opt{};
   Params P{};
   void *ws = nullptr;
+  void *graph2 = nullptr;  // degree-ordered internal CSR + id maps
+  size_t graph2_bytes = 0;
   size_t ws_bytes = 0;
   int64_t cand_cap = 0;
   size_t ks_smem = 0;
@@ -84,6 +88,65 @@ int init_grid(const s3bfs_ctx *h) {
   return (int)(want < cap ? want : cap);
 }
 
+int finalize_grid(const s3bfs_ctx *h) {
+  long long want = ((long long)h->n + 255) / 256;
+  long long cap = (long long)h->num_sms * 8;
+  return (int)(want < cap ? (want < 1 ? 1 : want) : cap);
+}
+
+// Degree-ordered internal copy (DESIGN.md s.7): internal id i = rank of the vertex in a stable
+// sort by descending degree, so the hottest vertices get the smallest ids and their visited
+// bits share a few L1-resident bitmap lines.  Create-time preprocessing, off the traversal
+// path (CUB's radix sort is the library primitive for the sort).
+s3bfs_status build_reordered(s3bfs_ctx *h, cudaStream_t st) {
+  const int n = h->n;
+  const long long nnz = h->nnz;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return o; };
+  const size_t o_col2 = take((size_t)nnz * 4 + 16);
+  const size_t o_n2o = take((size_t)n * 4), o_o2n = take((size_t)n * 4);
+  h->graph2_bytes = off;
+  CK(h, cudaMalloc(&h->graph2, off));
+  char *g = (char *)h->graph2;
+  int32_t *col2 = (int32_t *)(g + o_col2);
+  int32_t *n2o = (int32_t *)(g + o_n2o), *o2n = (int32_t *)(g + o_o2n);
+  int32_t *deg = nullptr, *deg_sorted = nullptr, *iota = nullptr, *ro2 = nullptr;
+  void *tmp = nullptr;
+  size_t tmp_bytes = 0;
+  CK(h, cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, deg, deg_sorted, iota,
+                                                  n2o, n, 0, 32, st));
+  CK(h, cudaMallocAsync((void **)&deg, (size_t)n * 4, st));
+  CK(h, cudaMallocAsync((void **)&deg_sorted, (size_t)n * 4, st));
+  CK(h, cudaMallocAsync((void **)&iota, (size_t)n * 4, st));
+  CK(h, cudaMallocAsync((void **)&ro2, (size_t)(n + 1) * 4, st));
+  CK(h, cudaMallocAsync(&tmp, tmp_bytes, st));
+  const int grid = h->num_sms * 8;
+  k_degrees<<<grid, 256, 0, st>>>(h->ro, n, deg, iota);
+  CK(h, cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, deg, deg_sorted, iota, n2o, n,
+                                                  0, 32, st));
+  k_inverse_perm<<<grid, 256, 0, st>>>(n2o, n, o2n, h->ro, deg);  // deg <- internal degrees
+  // ro2 = exclusive scan of the internal degrees: the look-back scan kernel (b)
+  const int tiles = (int)(((long long)n + SCAN_TILE - 1) / SCAN_TILE);
+  unsigned long long *status = nullptr;
+  CK(h, cudaMallocAsync((void **)&status, (size_t)tiles * 8, st));
+  CK(h, cudaMemsetAsync(status, 0, (size_t)tiles * 8, st));
+  k_scan_u32<<<tiles, SCAN_THREADS, 0, st>>>(deg, ro2, n, status);
+  k_relabel_rows<<<h->num_sms * 16, 256, 0, st>>>(h->ro, h->col, n2o, o2n, ro2, n, col2);
+  k_build_vinfo<<<grid, 256, 0, st>>>(ro2, n, h->P.vinfo);
+  CK(h, cudaGetLastError());
+  cudaFreeAsync(status, st);
+  cudaFreeAsync(tmp, st);
+  cudaFreeAsync(ro2, st);
+  cudaFreeAsync(iota, st);
+  cudaFreeAsync(deg_sorted, st);
+  cudaFreeAsync(deg, st);
+  CK(h, cudaStreamSynchronize(st));
+  h->P.col = col2;
+  h->P.n2o = n2o;
+  h->P.o2n = o2n;
+  return S3BFS_OK;
+}
+
 s3bfs_status build_graph(s3bfs_ctx *h) {
   cudaGraph_t g = nullptr;
   CK(h, cudaGraphCreate(&g, 0));
@@ -107,6 +170,15 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
   cudaGraph_t body = wp.conditional.phGraph_out[0];
 
   void *args[] = {&h->P};
+  {  // after the loop: d[0:n-1] and parent in caller ids
+    cudaKernelNodeParams kf = {};
+    kf.func = (void *)k_finalize;
+    kf.gridDim = dim3(finalize_grid(h));
+    kf.blockDim = dim3(256);
+    kf.kernelParams = args;
+    cudaGraphNode_t fnode;
+    CK(h, cudaGraphAddKernelNode(&fnode, g, &wnode, 1, &kf));
+  }
   auto kparams = [&](void *fn, int grid, int block, size_t smem) {
     cudaKernelNodeParams k = {};
     k.func = fn;
@@ -224,19 +296,22 @@ s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32
   const int collect = h->opt.collect_stats >= 0 ? 1 : 0;
 
   // ---- workspace (one allocation) ----
-  h->cand_cap = nnz + (int64_t)p_max * (KD_TILE + 1) + 64;
+  h->cand_cap = nnz + (int64_t)p_max * (KD_WARPS + 1 + KD_SLACK) + 64;
   if (h->cand_cap >= INT32_MAX)
     return bail(fail(h, S3BFS_ERR_UNSUPPORTED, "nnz too large for int32 candidate slots"));
   const int stats_cap = n + 1 < (1 << 16) ? n + 1 : (1 << 16);
   const size_t nb = (size_t)n * 4, nb1 = (size_t)(n + 1) * 4;
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return o; };
-  const size_t o_owner = take(nb);
+  const size_t o_vinfo = take((size_t)n * 16);
+  const size_t o_lp = take((size_t)n * 8);
   size_t o_f[2], o_frs[2], o_fex[2];
   for (int i = 0; i < 2; ++i) { o_f[i] = take(nb); o_frs[i] = take(nb); o_fex[i] = take(nb1 + 16); }
   const size_t o_cand = take((size_t)h->cand_cap * 4);
   const size_t o_crd = take((size_t)h->cand_cap * 8);
-  const size_t o_bm = take(((size_t)n + 31) / 32 * 4);
+  const size_t bm_bytes = ((size_t)n + 127) / 128 * 16;  // 16 B padded (vector clears)
+  const size_t o_bm = take(bm_bytes);
+  const size_t o_claim = take(((size_t)n + 15) / 16 * 16);
   const size_t o_wcnt = take((size_t)p_max * KD_WARPS * 4);
   const size_t o_status = take((size_t)p_max * 8);
   const size_t o_ctl = take(sizeof(Ctl));
@@ -245,11 +320,11 @@ s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32
   if ((e = cudaMalloc(&h->ws, h->ws_bytes)) != cudaSuccess) return bail(cuda_fail(h, e, "cudaMalloc(workspace)"));
   char *base = (char *)h->ws;
   Params &P = h->P;
-  P.ro = row_offsets;
   P.col = col_indices;
   P.n = n;
   P.ctl = (Ctl *)(base + o_ctl);
-  P.owner = (int32_t *)(base + o_owner);
+  P.vinfo = (int4 *)(base + o_vinfo);
+  P.lp = (int2 *)(base + o_lp);
   for (int i = 0; i < 2; ++i) {
     P.f[i] = (int32_t *)(base + o_f[i]);
     P.frs[i] = (int32_t *)(base + o_frs[i]);
@@ -258,6 +333,7 @@ s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32
   P.cand = (int32_t *)(base + o_cand);
   P.cand_rd = (int2 *)(base + o_crd);
   P.bm = (uint32_t *)(base + o_bm);
+  P.claim = (uint8_t *)(base + o_claim);
   P.wcnt = (int32_t *)(base + o_wcnt);
   P.status = (unsigned long long *)(base + o_status);
   P.stats = (s3bfs_level_stat *)(base + o_stats);
@@ -268,17 +344,8 @@ s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32
   P.variant = h->opt.variant == 1 ? 1 : 0;
   P.collect_stats = collect;
   P.use_graph = 0;
-  if ((e = cudaMemsetAsync(P.ctl, 0, sizeof(Ctl), stream)) != cudaSuccess) return bail(cuda_fail(h, e, "memset(ctl)"));
-  if ((e = cudaMemsetAsync(P.status, 0, (size_t)p_max * 8, stream)) != cudaSuccess) return bail(cuda_fail(h, e, "memset(status)"));
-  if (h->opt.debug_poison) {
-    k_poison<<<h->num_sms * 4, 256, 0, stream>>>(P.owner, n, (int)h->cand_cap);
-    if ((e = cudaGetLastError()) != cudaSuccess) return bail(cuda_fail(h, e, "k_poison"));
-  }
-
-  h->ks_smem = (size_t)(3 * KS_NCAP + 4 + KS_ECAP) * 4;
-  if ((e = cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->ks_smem)) != cudaSuccess)
-    return bail(cuda_fail(h, e, "cudaFuncSetAttribute(k_small)"));
-
+  P.n2o = nullptr;
+  P.o2n = nullptr;
   if (h->opt.validate_csr) {
     int *d_err = nullptr;
     int h_err = 0;
@@ -297,6 +364,25 @@ s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32
       return bail(fail(h, S3BFS_ERR_INVALID_GRAPH, m));
     }
   }
+  if (h->opt.reorder >= 0) {
+    s3bfs_status rs = build_reordered(h, stream);
+    if (rs != S3BFS_OK) return bail(rs);
+  } else {
+    k_build_vinfo<<<h->num_sms * 8, 256, 0, stream>>>(row_offsets, n, P.vinfo);
+    if ((e = cudaGetLastError()) != cudaSuccess) return bail(cuda_fail(h, e, "k_build_vinfo"));
+  }
+  if ((e = cudaMemsetAsync(P.ctl, 0, sizeof(Ctl), stream)) != cudaSuccess) return bail(cuda_fail(h, e, "memset(ctl)"));
+  if ((e = cudaMemsetAsync(P.status, 0, (size_t)p_max * 8, stream)) != cudaSuccess) return bail(cuda_fail(h, e, "memset(status)"));
+  if (h->opt.debug_poison) {
+    k_poison<<<h->num_sms * 4, 256, 0, stream>>>(P.vinfo, n, (int)h->cand_cap);
+    cudaMemsetAsync(P.lp, 0x5a, (size_t)n * 8, stream);  // {d, parent} garbage until written
+    if ((e = cudaGetLastError()) != cudaSuccess) return bail(cuda_fail(h, e, "k_poison"));
+  }
+
+  h->ks_smem = (size_t)(3 * KS_NCAP + 4 + 2 * KS_ECAP) * 4;
+  if ((e = cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->ks_smem)) != cudaSuccess)
+    return bail(cuda_fail(h, e, "cudaFuncSetAttribute(k_small)"));
+
   if (h->loop_graph) {
     s3bfs_status s = build_graph(h);
     if (s != S3BFS_OK) return bail(s);
@@ -353,7 +439,11 @@ s3bfs_status s3bfs_run(s3bfs_handle h, int32_t source, int32_t *level, int32_t *
       pending = -1;
     }
     const Ctl c = *h->h_ctl;
-    if (c.tier == TIER_DONE) break;
+    if (c.tier == TIER_DONE) {
+      k_finalize<<<finalize_grid(h), 256, 0, stream>>>(h->P);
+      CK(h, cudaGetLastError());
+      break;
+    }
     if (h->time_kernels) CK(h, cudaEventRecord(h->ev[0], stream));
     if (c.tier == TIER_SMALL) {
       k_small<<<1, KS_THREADS, h->ks_smem, stream>>>(h->P);
@@ -377,6 +467,7 @@ s3bfs_status s3bfs_destroy(s3bfs_handle h) {
   if (h->exec) cudaGraphExecDestroy(h->exec);
   if (h->graph) cudaGraphDestroy(h->graph);
   if (h->ws) cudaFree(h->ws);
+  if (h->graph2) cudaFree(h->graph2);
   if (h->h_ctl) cudaFreeHost(h->h_ctl);
   for (auto &ev : h->ev)
     if (ev) cudaEventDestroy(ev);
@@ -413,10 +504,10 @@ s3bfs_status s3bfs_get_info(s3bfs_handle h, s3bfs_info *out) {
   out->edges_per_cta = h->P.grain;
   out->tier0_max_edges = h->P.t0;
   out->kd_threads = KD_THREADS;
-  out->kd_tile_edges = KD_TILE;
+  out->kd_tile_edges = KX_GROUPS * 32;
   out->ksmall_threads = KS_THREADS;
   out->ksmall_max_frontier = KS_NCAP;
-  out->workspace_bytes = (int64_t)h->ws_bytes;
+  out->workspace_bytes = (int64_t)(h->ws_bytes + h->graph2_bytes);
   return S3BFS_OK;
 }
 

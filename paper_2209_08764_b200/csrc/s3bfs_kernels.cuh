@@ -3,19 +3,26 @@
 // "P:n" = /root/reference/PAPER.md line n; "Fig1 Lk" = item k of Figure 1;
 // "R<k>" = reading k in DESIGN.md.  This file shares nothing with oracle/ (test-only code).
 //
+// Vertex ids.  s3bfs_create builds an internal copy of the graph whose vertices are relabelled
+// by descending degree (DESIGN.md s.7): the hottest vertices get the smallest internal ids, so
+// their visited bits share a few L1-resident lines of the bitmap.  Every traversal kernel works
+// in internal ids; k_finalize writes the caller's level[]/parent[] in caller ids at the end.
+// With reordering off (opts.reorder < 0) n2o/o2n are NULL and the two id spaces coincide.
+//
 // Kernels (one level = one pass of (a)-(e)):
-//   k_init     Fig1 L1-L8   level/parent <- -1, level[s] = 0, parent[s] = s, frontier = [s]
-//   k_explore  (c)+(d)      Fig1 L17-L18: equal edge chunks per CTA ("(almost) equal
-//                           division"), start vertex by a 32-ary warp search of the degree
-//                           scan (R8), tile-wise edge->vertex map, coalesced col streaming,
-//                           plain-store labelling with the benign race -- no
-//                           atomic instruction anywhere in this kernel.
+//   k_init     Fig1 L1-L8   visited bitmap <- {s}, claim tags <- 0, frontier = [s], d[s] = 0
+//   k_explore  (c)+(d)      Fig1 L17-L18: equal edge slices per warp, start vertex by a
+//                           32-ary warp search of the degree scan (R8), coalesced col stream,
+//                           visited test (bitmap, then a per-level claim tag), d/parent/Owner
+//                           labelling with plain stores -- the benign race, no atomic
+//                           instruction.
 //   k_compact  (e)+(a)+(b)  Fig1 L19-L29 + L12-L15 of the NEXT level: keep cand[k] iff
 //                           Owner[cand[k]] == k, decoupled look-back scan of (kept, degree-sum)
 //                           pairs across CTAs, write f_next / row starts / degree scan.
 //   k_small    tier 0 (f)   one CTA runs whole levels (a)-(e) in shared memory while the level
 //                           stays tiny (P:22 -- "never use more cores than necessary").
 //   k_dispatch (f)          graph mode: selects the tier of the next WHILE iteration.
+//   k_finalize              d[0:n-1] and parent in caller ids ("Returns d[0:n-1]").
 //   k_scan_u32 (b) alone    test entry: the same look-back scan over a plain int32 array.
 //   k_find_start (c) alone  test entry: the same warp search, one warp per worker.
 #pragma once
@@ -26,10 +33,28 @@
 
 namespace s3bfs {
 
-// ---- compile-time geometry --------------------------------------------------------------
-constexpr int KD_THREADS = 512;                 // k_explore / k_compact CTA size
+// ---- compile-time geometry (the -D switches exist for scripts/kx_micro.py experiments) -----
+#ifndef S3BFS_KD_THREADS
+#define S3BFS_KD_THREADS 512
+#endif
+#ifndef S3BFS_KD_MINB
+#define S3BFS_KD_MINB (1024 / S3BFS_KD_THREADS)
+#endif
+#ifndef S3BFS_KX_GROUPS
+#define S3BFS_KX_GROUPS 8
+#endif
+#ifndef S3BFS_KX_FAST
+#define S3BFS_KX_FAST 1   // uniform-row fast path
+#endif
+#ifndef S3BFS_BM_NC
+#define S3BFS_BM_NC 1     // bitmap probes through the non-coherent (read-only) path
+#endif
+constexpr int KD_THREADS = S3BFS_KD_THREADS;    // k_explore / k_compact CTA size
+constexpr int KD_MIN_BLOCKS = S3BFS_KD_MINB;    // CTAs per SM the register budget targets
 constexpr int KD_WARPS = KD_THREADS / 32;
-constexpr int KD_TILE = 4096;                   // candidate-buffer slack per CTA (edges)
+constexpr int KD_SLACK = 64;                    // candidate-buffer slack per CTA
+constexpr int KX_GROUPS = S3BFS_KX_GROUPS;      // 32-edge groups per batch and warp
+constexpr int KC_GROUPS = 4;                    // 32-candidate groups per k_compact round
 constexpr int KS_THREADS = 1024;                // k_small CTA size
 constexpr int KS_ECAP = 8192;                   // T0 maximum (edges per tier-0 level)
 constexpr int KS_NCAP = KS_ECAP;                // frontier capacity of tier 0 (kept <= e_l)
@@ -50,7 +75,7 @@ struct Ctl {
   int32_t tier;       // TIER_SMALL / TIER_LARGE / TIER_DONE
   int32_t p_l;        // P_l = CTAs of this level (Fig1 L16)
   int32_t chunk;      // edges per CTA (ceil(e_l / P_l))
-  int32_t wcap;       // candidate capacity per warp
+  int32_t wcap;       // edges (= candidate capacity) per warp
   int32_t n_next, e_next;   // written by the last k_compact CTA in tile order
   uint32_t done_ctr;        // last-CTA election in k_compact (not the discovery path)
   int32_t num_levels;       // stats records written
@@ -63,14 +88,19 @@ struct Ctl {
 };
 
 struct Params {
-  const int32_t *ro, *col;
+  const int32_t *col;           // internal adjacency (degree-ordered copy, or the caller's)
+  int4 *vinfo;                  // per internal vertex: {row start, degree, -, Owner (Fig1 L3;
+                                //  never initialised, R3)} -- one sector per k_compact probe
+  int2 *lp;                     // per internal vertex: {d, parent (internal id)}, valid where
+                                //  the visited bit is set
+  const int32_t *n2o, *o2n;     // internal -> caller ids and back (NULL: identity)
   int32_t n;
   Ctl *ctl;
-  int32_t *owner;
-  int32_t *f[2], *frs[2], *fex[2];  // frontier ids, their row starts, exclusive degree scan
-  int32_t *cand;
-  int2 *cand_rd;          // (row start, degree) of kept candidates, pass 1 -> pass 2 of k_compact
-  uint32_t *bm;           // visited bitmap: bit v set => level[v] != -1 (a filter; level[] rules)
+  int32_t *f[2], *frs[2], *fex[2];  // frontier: internal ids, row starts, exclusive degree scan
+  int32_t *cand;                // candidate per slot (k_explore), compacted by k_compact
+  int2 *cand_rd;                // (row start, degree) of kept candidates, pass 1 -> pass 2
+  uint32_t *bm;                 // visited bitmap: bit set => visited (exact at level start)
+  uint8_t *claim;               // per-vertex tag of the level that discovered it (k_explore)
   int32_t *wcnt;
   unsigned long long *status;
   s3bfs_level_stat *stats;
@@ -86,16 +116,8 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// Status reads of the racing arrays (level[], owner[]): weak loads, L1-cacheable.  Within one
-// kernel launch a stale -1 only re-discovers v at the SAME level (benign, R18); L1 is
-// invalidated at every launch, so staleness never crosses a level boundary.
-__device__ __forceinline__ int ld_weak(const int32_t *p) {
-  int v;
-  asm volatile("ld.global.s32 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
-}
 // L2 eviction policies (createpolicy): the adjacency is streamed once per level and must not
-// evict the status array, which every arc probes at random.
+// evict the visited bitmap / claim tags, which every arc probes at random.
 __device__ __forceinline__ unsigned long long policy_evict_first() {
   unsigned long long p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -106,17 +128,18 @@ __device__ __forceinline__ unsigned long long policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
-// read-only stream (col_indices): non-coherent, no L1 allocation, L2 evict-first
+// read-only stream (col_indices): non-coherent, L1-allocating (neighbouring 32-edge groups of
+// one warp share a boundary line), L2 evict-first
 __device__ __forceinline__ int ldg_stream(const int32_t *p, unsigned long long pol) {
   int v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
-               : "=r"(v) : "l"(p), "l"(pol));
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
   return v;
 }
-// status probe of level[] (racing array, weak load) with an L2 evict-last hint
-__device__ __forceinline__ int ld_status(const int32_t *p, unsigned long long pol) {
-  int v;
-  asm volatile("ld.global.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+// the visited bitmap inside k_explore: read-only there (written by earlier kernels only); the
+// hot vertices' words stay L1-resident thanks to the degree order
+__device__ __forceinline__ uint32_t ldg_status_u32(const uint32_t *p, unsigned long long pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
   return v;
 }
 __device__ __forceinline__ uint32_t ld_status_u32(const uint32_t *p, unsigned long long pol) {
@@ -124,8 +147,26 @@ __device__ __forceinline__ uint32_t ld_status_u32(const uint32_t *p, unsigned lo
   asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
   return v;
 }
+// claim tags: L2-coherent byte loads/stores (no stale L1 line hides another SM's claim)
+__device__ __forceinline__ int ld_cg_u8(const uint8_t *p) {
+  unsigned v;
+  asm volatile("ld.global.cg.u8 %0, [%1];" : "=r"(v) : "l"(p));
+  return (int)v;
+}
+__device__ __forceinline__ void st_u8(uint8_t *p, int v) {
+  asm volatile("st.global.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void st_weak(int32_t *p, int v) {
   asm volatile("st.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_weak_v2(int2 *p, int a, int b) {
+  asm volatile("st.global.v2.s32 [%0], {%1, %2};" ::"l"(p), "r"(a), "r"(b) : "memory");
+}
+__device__ __forceinline__ int4 ld_weak_v4(const int4 *p) {
+  int4 r;
+  asm volatile("ld.global.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
 }
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
   unsigned long long v;
@@ -142,6 +183,9 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
+}
+__device__ __forceinline__ int32_t *owner_of(int4 *vinfo, int v) {
+  return reinterpret_cast<int32_t *>(vinfo + v) + 3;
 }
 
 __device__ __forceinline__ int warp_incl_scan(int x) {
@@ -282,43 +326,31 @@ __device__ void decide(const Params &P, Ctl *c, int32_t n_l, int32_t e_l) {
 }
 
 // ---- init (Fig1 L1-L8) ----------------------------------------------------------------------
-// level[v] <- -1 (d <- infinity, R1), parent[v] <- -1; level[s] = 0, parent[s] = s (R2).
-// Owner is NOT initialised (R3: every read of Owner[v] follows a write in the same level).
+// d <- infinity is the cleared visited bitmap (R1): only the source's bit is set, with
+// {d, parent} = {0, s} (R2).  Claim tags <- 0.  Owner is NOT initialised (R3).  The caller's
+// level/parent arrays are written once, by k_finalize.
 __global__ void k_init(Params P, int32_t s, int32_t *level, int32_t *parent) {
   const int n = P.n;
   const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long gstride = (long long)gridDim.x * blockDim.x;
-  const bool vec = ((((uintptr_t)level) | ((uintptr_t)parent)) & 15) == 0;
-  long long done = 0;
-  if (vec) {
-    const long long n4 = n >> 2;
-    for (long long i = gtid; i < n4; i += gstride) {
-      int4 lv = make_int4(-1, -1, -1, -1), pv = lv;
-      const long long b = i << 2;
-      if (s >= b && s < b + 4) {
-        const int j = (int)(s - b);
-        (&lv.x)[j] = 0;
-        (&pv.x)[j] = s;
-      }
-      reinterpret_cast<int4 *>(level)[i] = lv;
-      reinterpret_cast<int4 *>(parent)[i] = pv;
-    }
-    done = n4 << 2;
+  const int si = P.o2n ? __ldg(P.o2n + s) : s;  // the source's internal id
+  const long long nw4 = ((long long)n + 127) >> 7;  // bitmap as uint4 (16 B padded)
+  for (long long i = gtid; i < nw4; i += gstride) {
+    uint4 w = make_uint4(0, 0, 0, 0);
+    if (i == (si >> 7)) (&w.x)[(si >> 5) & 3] = 1u << (si & 31);
+    reinterpret_cast<uint4 *>(P.bm)[i] = w;
   }
-  for (long long i = done + gtid; i < n; i += gstride) {
-    level[i] = (i == s) ? 0 : -1;
-    parent[i] = (i == s) ? s : -1;
-  }
-  const long long nw = ((long long)n + 31) >> 5;  // visited bitmap: only the source
-  for (long long i = gtid; i < nw; i += gstride)
-    P.bm[i] = (i == (s >> 5)) ? (1u << (s & 31)) : 0u;
+  const long long nc = ((long long)n + 15) >> 4;  // claim tags <- 0 (16 B padded)
+  for (long long i = gtid; i < nc; i += gstride)
+    reinterpret_cast<uint4 *>(P.claim)[i] = make_uint4(0, 0, 0, 0);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     Ctl *c = P.ctl;
-    const int r0 = P.ro[s], r1 = P.ro[s + 1];
-    P.f[0][0] = s;        // Fig1 L7: CurLevelVertices <- [s]
-    P.frs[0][0] = r0;
+    const int4 vs = P.vinfo[si];
+    P.lp[si] = make_int2(0, si);
+    P.f[0][0] = si;       // Fig1 L7: CurLevelVertices <- [s]
+    P.frs[0][0] = vs.x;
     P.fex[0][0] = 0;      // exclusive degree scan of the frontier (R5)
-    P.fex[0][1] = r1 - r0;
+    P.fex[0][1] = vs.y;
     c->level = 0;         // Fig1 L8
     c->cur = 0;
     c->source = s;
@@ -328,7 +360,7 @@ __global__ void k_init(Params P, int32_t s, int32_t *level, int32_t *parent) {
     c->done_ctr = 0;
     c->cand_acc = 0;
     c->t_prev = globaltimer();
-    decide(P, c, 1, r1 - r0);
+    decide(P, c, 1, vs.y);
   }
 }
 
@@ -344,18 +376,20 @@ __global__ void k_dispatch(Params P) {
 // CTA b < P_l owns global edges [b*chunk, min((b+1)*chunk, e_l)) of the level, split evenly
 // over its warps: each warp is one of the paper's workers with an (almost) equal share of the
 // level's edges (Fig1 L16-L17).  A warp finds its start vertex with the 32-ary search
-// (c), then walks its edges in groups of 32 -- lane i takes edge e+i, so a group reads 32
-// consecutive col entries (coalesced streaming, Fig1 L18).  Edge -> frontier vertex mapping
-// uses a register window of 32 consecutive frontier vertices (their degree-scan entries,
-// ids and row starts): a 5-step shuffle search per lane, no shared memory, no CTA barrier,
-// so warps progress independently and keep KX_GROUPS groups of loads in flight.
-// Discovery (EXPLORE-VERTEX): if level[v] == -1 then level[v] = l+1, parent[v] = x,
-// Owner[v] = slot, cand[slot] = v -- plain stores, the paper's benign race, no atomics.
-// The candidate slot is a unique id (R4), so Owner dedup keeps exactly one copy even when
-// two lanes of one warp discover v together.
-constexpr int KX_GROUPS = 8;
-constexpr int KX_MIN_BLOCKS = 2;
-__global__ void __launch_bounds__(KD_THREADS, KX_MIN_BLOCKS) k_explore(Params P) {
+// (c), then walks its edges in batches of KX_GROUPS groups of 32 -- lane i takes edge e+i, so
+// a group reads 32 consecutive col entries (coalesced streaming, Fig1 L18).  Edge -> frontier
+// vertex mapping uses a register window of 32 consecutive frontier vertices (their
+// degree-scan entries, ids and row starts): one warp-uniform shuffle search per batch, and a
+// per-lane search only when the batch spans several rows.  No shared memory, no CTA barrier,
+// so warps progress independently.
+// Visited test (the paper's "d[v] = infinity", R1): the visited bitmap (exact at level start,
+// read-only here) and, for a clear bit, the vertex's 1-byte claim tag, which equals this
+// level's tag once some worker discovered v in this level.
+// Discovery (EXPLORE-VERTEX): claim[v] = tag, {d, parent}[v] = {l+1, x}, Owner[v] =
+// slot, cand[slot] = v -- plain stores, the paper's benign race, no atomics.  Racing
+// discoverers that all saw an old tag store the same d and a valid parent and enqueue
+// duplicates; the Owner check keeps exactly one (R4).
+__global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P) {
   Ctl *c = P.ctl;
   if (c->tier != TIER_LARGE) return;
   const int b = blockIdx.x;
@@ -363,16 +397,17 @@ __global__ void __launch_bounds__(KD_THREADS, KX_MIN_BLOCKS) k_explore(Params P)
   if (b >= p_l) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n_l = c->n_l, e_l = c->e_l, chunk = c->chunk, cur = c->cur, wcap = c->wcap;
-  const int new_level = c->level + 1;  // Fig1 L10: discoveries get l+1 (R11)
-  int32_t *__restrict__ level = c->level_out;
-  int32_t *__restrict__ parent = c->parent_out;
+  const int new_level = c->level + 1;     // Fig1 L10: discoveries get l+1 (R11)
+  const int tag = 1 + (c->level % 255);   // never 0, the per-run initial value
   const int32_t *__restrict__ fx = P.f[cur];
   const int32_t *__restrict__ frs = P.frs[cur];
   const int32_t *__restrict__ fex = P.fex[cur];
   const int32_t *__restrict__ col = P.col;
-  int32_t *__restrict__ owner = P.owner;
+  int4 *__restrict__ vinfo = P.vinfo;
+  int2 *__restrict__ lp = P.lp;
   int32_t *__restrict__ cand = P.cand;
   const uint32_t *__restrict__ bm = P.bm;
+  uint8_t *__restrict__ claim = P.claim;
 
   if (tid == 0) {
     P.status[b] = 0ull;  // reset k_compact's look-back word for this level
@@ -386,75 +421,100 @@ __global__ void __launch_bounds__(KD_THREADS, KX_MIN_BLOCKS) k_explore(Params P)
   const unsigned long long pol_stream = policy_evict_first();
   const unsigned long long pol_status = policy_evict_last();
   int wcount = 0;
+  int u0 = 0, wex = 0, wx = 0, wb = 0, lim = 0;
+  auto load_window = [&](int base) {
+    const int u = base + lane;
+    wex = (u < n_l) ? __ldg(fex + u) : 0x7fffffff;
+    wx = (u < n_l) ? __ldg(fx + u) : 0;
+    wb = (u < n_l) ? __ldg(frs + u) - wex : 0;
+    lim = __ldg(fex + min(base + 32, n_l));
+  };
   if (e_begin < e_end) {
-    int u0 = warp_search(fex, n_l, e_begin);  // Find-StartExpPoint (c)
-    int wex, wx, wb, lim;
-    auto load_window = [&](int base) {
-      const int u = base + lane;
-      wex = (u < n_l) ? __ldg(fex + u) : 0x7fffffff;
-      wx = (u < n_l) ? __ldg(fx + u) : 0;
-      wb = (u < n_l) ? __ldg(frs + u) - wex : 0;
-      lim = __ldg(fex + min(base + 32, n_l));
-    };
+    u0 = warp_search(fex, n_l, e_begin);  // Find-StartExpPoint (c)
     load_window(u0);
-    int e = e_begin;
-    while (e < e_end) {
-      while (lim <= e) {  // window exhausted (also skips runs of zero-degree vertices, C9)
-        u0 += 32;
-        load_window(u0);
-      }
-      const int bend = min(e_end, lim);
-      int v[KX_GROUPS], xv[KX_GROUPS];
+  }
+  int e = e_begin;
+  while (e < e_end) {
+    while (lim <= e) {  // window exhausted (also skips runs of zero-degree vertices, C9)
+      u0 += 32;
+      load_window(u0);
+    }
+    const int bend = min(e_end, lim);
+    int v[KX_GROUPS], xv[KX_GROUPS];
+    int j0 = 0;  // window slot of the batch's first edge (warp-uniform)
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+      const int cj = __shfl_sync(0xffffffffu, wex, j0 + s);
+      if (cj <= e) j0 += s;
+    }
+    const int row_end = (j0 < 31) ? __shfl_sync(0xffffffffu, wex, min(j0 + 1, 31)) : lim;
+    if (S3BFS_KX_FAST && row_end >= min(e + KX_GROUPS * 32, bend)) {
+      // the whole batch lies in one frontier row (most R-MAT arcs): uniform x and base
+      const int x = __shfl_sync(0xffffffffu, wx, j0);
+      const int base = __shfl_sync(0xffffffffu, wb, j0);
 #pragma unroll
       for (int g = 0; g < KX_GROUPS; ++g) {
         const int my_e = e + g * 32 + lane;
-        int j = 0;  // largest window slot with excl <= my_e
+        xv[g] = x;
+        v[g] = (my_e < bend) ? ldg_stream(col + base + my_e, pol_stream) : -1;
+      }
+    } else {
+#pragma unroll
+      for (int g = 0; g < KX_GROUPS; ++g) {
+        const int my_e = e + g * 32 + lane;
+        int j = j0;  // largest window slot with excl <= my_e (>= j0)
 #pragma unroll
         for (int s = 16; s >= 1; s >>= 1) {
-          const int cj = __shfl_sync(0xffffffffu, wex, j + s);
-          if (cj <= my_e) j += s;
+          const int cj = __shfl_sync(0xffffffffu, wex, min(j + s, 31));
+          if (j + s <= 31 && cj <= my_e) j += s;
         }
         xv[g] = __shfl_sync(0xffffffffu, wx, j);
         const int pos = __shfl_sync(0xffffffffu, wb, j) + my_e;
         v[g] = (my_e < bend) ? ldg_stream(col + pos, pol_stream) : -1;
       }
-      // status: the visited bitmap first (2 MB at scale 24: stays in L2), level[] only when the
-      // bit is clear (unvisited, or discovered earlier in this same level)
-      uint32_t bw[KX_GROUPS];
-#pragma unroll
-      for (int g = 0; g < KX_GROUPS; ++g)
-        bw[g] = (v[g] >= 0) ? ld_status_u32(bm + (v[g] >> 5), pol_status) : 0xffffffffu;
-      int lv[KX_GROUPS];
-#pragma unroll
-      for (int g = 0; g < KX_GROUPS; ++g)
-        lv[g] = ((bw[g] >> (v[g] & 31)) & 1u) ? 0 : ld_status(level + v[g], pol_status);
-#pragma unroll
-      for (int g = 0; g < KX_GROUPS; ++g) {
-        const bool disc = lv[g] == -1;
-        const unsigned m = __ballot_sync(0xffffffffu, disc);
-        if (disc) {
-          const int slot = segbase + wcount + __popc(m & lanemask_lt());
-          st_weak(level + v[g], new_level);
-          st_weak(parent + v[g], xv[g]);
-          st_weak(owner + v[g], slot);
-          cand[slot] = v[g];
-        }
-        wcount += __popc(m);
-      }
-      e = min(e + KX_GROUPS * 32, bend);
     }
+    // visited test: the bitmap (visited before this level), then the claim tag
+    bool need[KX_GROUPS];
+#pragma unroll
+    for (int g = 0; g < KX_GROUPS; ++g) {
+      need[g] = false;
+      if (v[g] >= 0) {
+        const uint32_t w = S3BFS_BM_NC ? ldg_status_u32(bm + (v[g] >> 5), pol_status)
+                                       : ld_status_u32(bm + (v[g] >> 5), pol_status);
+        need[g] = !((w >> (v[g] & 31)) & 1u);
+      }
+    }
+    int cl[KX_GROUPS];
+#pragma unroll
+    for (int g = 0; g < KX_GROUPS; ++g) cl[g] = need[g] ? ld_cg_u8(claim + v[g]) : tag;
+#pragma unroll
+    for (int g = 0; g < KX_GROUPS; ++g) {
+      const bool disc = need[g] && cl[g] != tag;
+      const unsigned m = __ballot_sync(0xffffffffu, disc);
+      if (disc) {
+        const int slot = segbase + wcount + __popc(m & lanemask_lt());
+        st_u8(claim + v[g], tag);
+        st_weak_v2(lp + v[g], new_level, xv[g]);   // d[v] <- l, parent (Fig1 L18)
+        st_weak(owner_of(vinfo, v[g]), slot);      // Owner[v] <- i (benign race)
+        cand[slot] = v[g];                         // Q[i].Enqueue(v)
+      }
+      wcount += __popc(m);
+    }
+    e = min(e + KX_GROUPS * 32, bend);
   }
   if (lane == 0) P.wcnt[b * KD_WARPS + warp] = wcount;
 }
 
 // ---- (e)+(a)+(b): k_compact -------------------------------------------------------------------
 // CTA b handles the candidate segments its k_explore twin wrote (one per warp).
-// Pass 1 (Fig1 L20-L23): keep cand[k] iff Owner[cand[k]] == k, compacting in place, and sum
-// the kept vertices' degrees (Fig1 L13 for the next level).  Then a decoupled look-back over
-// CTAs scans the (kept, degree-sum) pairs (Fig1 L24 and L14 of the next level in one pass).
-// Pass 2 (Fig1 L25-L29): write the next frontier, its row starts and its exclusive degree
-// scan.  The last CTA to finish advances the control block (Fig1 L9-L10, L15-L16).
-__global__ void __launch_bounds__(KD_THREADS, 2) k_compact(Params P) {
+// Pass 1 (Fig1 L20-L23): keep cand[k] iff Owner[cand[k]] == k (one 16-byte vertex-record
+// probe gives Owner, row start and degree); publish the kept vertex's visited bit and
+// compact (id, row start, degree) in place -- the degree is Fig1 L13 of the next level.
+// A decoupled look-back over CTAs scans the (kept, degree-sum) pairs (Fig1 L24 and L14 of
+// the next level in one pass).  Pass 2 (Fig1 L25-L29): write the next frontier, its row
+// starts and its exclusive degree scan.  The last CTA to finish advances the control block
+// (Fig1 L9-L10, L15-L16).
+__global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P) {
   Ctl *c = P.ctl;
   if (c->tier != TIER_LARGE) return;
   const int b = blockIdx.x;
@@ -464,36 +524,40 @@ __global__ void __launch_bounds__(KD_THREADS, 2) k_compact(Params P) {
   __shared__ int s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nxt = c->cur ^ 1;
-  const int32_t *__restrict__ ro = P.ro;
-  const int32_t *__restrict__ owner = P.owner;
+  const int4 *__restrict__ vinfo = P.vinfo;
   int32_t *__restrict__ cand = P.cand;
+  int2 *__restrict__ crd = P.cand_rd;
   const int seg = (b * KD_WARPS + warp) * c->wcap;
   const int cnt = P.wcnt[b * KD_WARPS + warp];
   if (b == 0 && tid == 0) c->t_kx_end = globaltimer();
 
-  int2 *__restrict__ crd = P.cand_rd;
   int kept = 0, dsum = 0;
-  for (int k0 = 0; k0 < cnt; k0 += 32) {
-    const int k = k0 + lane;
-    bool keep = false;
-    int v = 0, r0 = 0, d = 0;
-    if (k < cnt) {
-      v = cand[seg + k];
-      keep = ld_weak(owner + v) == seg + k;  // Fig1 L22: "if Owner[v] = i"
+  for (int k0 = 0; k0 < cnt; k0 += 32 * KC_GROUPS) {
+    int v[KC_GROUPS];
+#pragma unroll
+    for (int g = 0; g < KC_GROUPS; ++g) {
+      const int k = k0 + g * 32 + lane;
+      v[g] = (k < cnt) ? cand[seg + k] : -1;
+    }
+    int4 vi[KC_GROUPS];  // {row start, degree, -, Owner}: one sector per candidate
+#pragma unroll
+    for (int g = 0; g < KC_GROUPS; ++g)
+      vi[g] = (v[g] >= 0) ? __ldg(vinfo + v[g]) : make_int4(0, 0, 0, -1);
+#pragma unroll
+    for (int g = 0; g < KC_GROUPS; ++g) {
+      const int k = k0 + g * 32 + lane;
+      const bool keep = v[g] >= 0 && vi[g].w == seg + k;  // Fig1 L22: "if Owner[v] = i"
+      const int d = keep ? vi[g].y : 0;
+      if (keep) atomicOr(P.bm + (v[g] >> 5), 1u << (v[g] & 31));  // exact visited bit (R17)
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
       if (keep) {
-        r0 = __ldg(ro + v);
-        d = __ldg(ro + v + 1) - r0;
-        atomicOr(P.bm + (v >> 5), 1u << (v & 31));  // publish "visited" (filter only, R17)
+        const int q = seg + kept + __popc(m & lanemask_lt());
+        cand[q] = v[g];
+        crd[q] = make_int2(vi[g].x, d);
       }
+      kept += __popc(m);
+      dsum += d;
     }
-    const unsigned m = __ballot_sync(0xffffffffu, keep);
-    if (keep) {
-      const int q = seg + kept + __popc(m & lanemask_lt());
-      cand[q] = v;
-      crd[q] = make_int2(r0, d);
-    }
-    kept += __popc(m);
-    dsum += d;
   }
   dsum = warp_sum(dsum);
   if (lane == 0) { s_k[warp] = kept; s_d[warp] = dsum; }
@@ -509,7 +573,10 @@ __global__ void __launch_bounds__(KD_THREADS, 2) k_compact(Params P) {
     const Pair agg{(uint32_t)__shfl_sync(0xffffffffu, ik, 31),
                    (uint32_t)__shfl_sync(0xffffffffu, id, 31)};
     const Pair ex = lookback<true>(P.status, b, agg);
-    if (lane < KD_WARPS) { s_k[lane] = (int)ex.a + ik - kk; s_d[lane] = (int)ex.b + id - dd; }
+    if (lane < KD_WARPS) {
+      s_k[lane] = (int)ex.a + ik - kk;
+      s_d[lane] = (int)ex.b + id - dd;
+    }
     if (b == p_l - 1 && lane == 0) {  // the level's totals: n_{l+1}, e_{l+1} (Fig1 L15)
       const int n_next = (int)(ex.a + agg.a), e_next = (int)(ex.b + agg.b);
       c->n_next = n_next;
@@ -565,8 +632,10 @@ __global__ void __launch_bounds__(KD_THREADS, 2) k_compact(Params P) {
 // paper's "use only as many cores as there is work" at CTA granularity.  Same
 // per-level contract as k_explore + k_compact; the owner label is the level-local edge
 // index e (unique, R4); frontier, degree scan and candidates live in shared memory.
-// Global level/parent/owner writes of this CTA are ordered for its own later reads by the
-// CTA barrier (one SM), so multi-level operation is safe.
+// The visited bitmap is exact at every level start (bits of kept vertices are published with
+// atomicOr in the compaction step, after the discovery step), and this CTA's global writes
+// are ordered for its own later reads by the CTA barrier (one SM), so multi-level operation
+// is safe.
 __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
   Ctl *c = P.ctl;
   if (c->tier != TIER_SMALL) return;
@@ -575,15 +644,14 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
   int32_t *srs = sf + KS_NCAP;        // row starts
   int32_t *sex = srs + KS_NCAP;       // exclusive degree scan, KS_NCAP + 1 entries
   int32_t *cv = sex + KS_NCAP + 4;    // candidate per level-local edge (or -1)
+  int32_t *cpv = cv + KS_ECAP;        // its discoverer
   __shared__ int32_t s_wk[KS_THREADS / 32], s_wd[KS_THREADS / 32], s_wc[KS_THREADS / 32];
   __shared__ int32_t s_tot[3];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int32_t *__restrict__ ro = P.ro;
   const int32_t *__restrict__ col = P.col;
-  int32_t *__restrict__ level = c->level_out;
-  int32_t *__restrict__ parent = c->parent_out;
-  int32_t *__restrict__ owner = P.owner;
+  int4 *__restrict__ vinfo = P.vinfo;
+  const uint32_t *__restrict__ bm = P.bm;
   int n_l = c->n_l, e_l = c->e_l, L = c->level;
   const int cur = c->cur;
   unsigned long long t_prev = c->t_prev;
@@ -604,17 +672,17 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
         const int mid = (lo + hi) >> 1;
         if (sex[mid] <= e) lo = mid; else hi = mid;
       }
-      const int x = sf[lo];
       const int v = __ldg(col + srs[lo] + (e - sex[lo]));
       int w = -1;
-      if (ld_weak(level + v) == -1) {
-        st_weak(level + v, L + 1);
-        st_weak(parent + v, x);
-        st_weak(owner + v, e);
+      // L1-bypassing read: the bits were published by atomicOr (at L2) in earlier levels of
+      // this same kernel, so an L1 line cached before that would be stale
+      if (!((__ldcg(bm + (v >> 5)) >> (v & 31)) & 1u)) {
+        st_weak(owner_of(vinfo, v), e);  // Owner[v] <- e (benign race)
         w = v;
         ++ncand;
       }
       cv[e] = w;
+      cpv[e] = sf[lo];
     }
     __syncthreads();
     // (e): owner check + next-level degree, blocked items for the scan
@@ -631,9 +699,12 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
       if (i < ipt && e < e_l) {
         const int v = cv[e];
         if (v >= 0) {
-          const int ow = ld_weak(owner + v);
-          const int r0 = __ldg(ro + v), r1 = __ldg(ro + v + 1);
-          if (ow == e) { kv[i] = v; kr[i] = r0; kd[i] = r1 - r0; }
+          const int4 vi = ld_weak_v4(vinfo + v);  // same-SM writes: L1-coherent
+          if (vi.w == e) {
+            kv[i] = v; kr[i] = vi.x; kd[i] = vi.y;
+            P.lp[v] = make_int2(L + 1, cpv[e]);         // d[v] <- l, parent (Fig1 L18)
+            atomicOr(P.bm + (v >> 5), 1u << (v & 31));  // exact visited bit (not discovery)
+          }
         }
       }
     }
@@ -662,10 +733,6 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
 #pragma unroll
     for (int i = 0; i < KS_IPT; ++i) {
       if (kv[i] >= 0) {
-        // visited bit: plain read-modify-write, no atomic -- a racing update can only lose a
-        // bit (the filter then falls back to level[]), never set one wrongly
-        uint32_t *wp = P.bm + (kv[i] >> 5);
-        *(volatile uint32_t *)wp = *(volatile uint32_t *)wp | (1u << (kv[i] & 31));
         sf[kpos] = kv[i];
         srs[kpos] = kr[i];
         sex[kpos] = dpos;
@@ -699,6 +766,65 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
     c->t_prev = t_prev;
     decide(P, c, n_l, e_l);
   }
+}
+
+// ---- d[0:n-1] in caller ids --------------------------------------------------------------
+// level[o] = d of internal vertex o2n[o] if its visited bit is set, else -1 (unreachable, R1);
+// parent[o] = the parent's caller id (R2).  Reads the internal records in caller order; the
+// caller's arrays are written exactly once, coalesced.
+__global__ void k_finalize(Params P) {
+  const Ctl *c = P.ctl;
+  int32_t *__restrict__ level = c->level_out;
+  int32_t *__restrict__ parent = c->parent_out;
+  const int n = P.n;
+  for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < n;
+       o += (long long)gridDim.x * blockDim.x) {
+    const int i = P.o2n ? __ldg(P.o2n + o) : (int)o;
+    int lv = -1, pa = -1;
+    if ((__ldg(P.bm + (i >> 5)) >> (i & 31)) & 1u) {
+      const int2 r = __ldg(P.lp + i);
+      lv = r.x;
+      pa = P.n2o ? __ldg(P.n2o + r.y) : r.y;
+    }
+    level[o] = lv;
+    parent[o] = pa;
+  }
+}
+
+// ---- create-time graph preparation (not on the traversal path) --------------------------------
+__global__ void k_degrees(const int32_t *ro, int n, int32_t *deg, int32_t *iota) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    deg[i] = ro[i + 1] - ro[i];
+    iota[i] = (int32_t)i;
+  }
+}
+__global__ void k_inverse_perm(const int32_t *n2o, int n, int32_t *o2n, const int32_t *ro,
+                               int32_t *deg2) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int o = n2o[i];
+    o2n[o] = (int32_t)i;
+    deg2[i] = ro[o + 1] - ro[o];
+  }
+}
+// one warp per internal row: col2[ro2[i] + j] = o2n[col[ro[n2o[i]] + j]]
+__global__ void k_relabel_rows(const int32_t *ro, const int32_t *col, const int32_t *n2o,
+                               const int32_t *o2n, const int32_t *ro2, int n, int32_t *col2) {
+  const int lane = threadIdx.x & 31;
+  const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long ws = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long i = w0; i < n; i += ws) {
+    const int o = n2o[i];
+    const int s = ro[o], len = ro[o + 1] - s, d = ro2[i];
+    for (int j = lane; j < len; j += 32) col2[d + j] = o2n[col[s + j]];
+  }
+}
+// vinfo[i] = {row start, degree, 0, Owner = 0} over a CSR's row offsets
+__global__ void k_build_vinfo(const int32_t *ro, int n, int4 *vinfo) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    vinfo[i] = make_int4(ro[i], ro[i + 1] - ro[i], 0, 0);
 }
 
 // ---- test entry kernels ---------------------------------------------------------------------
@@ -771,10 +897,10 @@ __global__ void k_validate(const int32_t *ro, const int32_t *col, int n, long lo
 }
 
 // debug: fill Owner with values that look like live candidate slots (R3 pin).
-__global__ void k_poison(int32_t *owner, int n, int range) {
+__global__ void k_poison(int4 *vinfo, int n, int range) {
   const long long gs = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gs)
-    owner[i] = (int32_t)(((unsigned)i * 2654435761u) % (unsigned)max(range, 1));
+    vinfo[i].w = (int32_t)(((unsigned)i * 2654435761u) % (unsigned)max(range, 1));
 }
 
 }  // namespace s3bfs

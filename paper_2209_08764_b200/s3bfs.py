@@ -39,7 +39,8 @@ class Options(ctypes.Structure):
                 ("loop_mode", ctypes.c_int32), ("collect_stats", ctypes.c_int32),
                 ("validate_csr", ctypes.c_int32), ("variant", ctypes.c_int32),
                 ("max_ctas", ctypes.c_int32), ("debug_poison", ctypes.c_int32),
-                ("time_kernels", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+                ("time_kernels", ctypes.c_int32), ("reorder", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 6)]
 
 
 class LevelStat(ctypes.Structure):

@@ -1,0 +1,117 @@
+// scripts/kx_micro.cu -- experiment harness (not product code): time k_explore, compiled with
+// a given set of -D switches, on one captured level of a real traversal.
+#include "../paper_2209_08764_b200/csrc/s3bfs_kernels.cuh"
+using namespace s3bfs;
+extern "C" int kx_micro(const int32_t *col, int n, int n_l, int e_l, int32_t *f, int32_t *frs,
+                        int32_t *fex, uint32_t *bm, uint8_t *claim, int4 *vinfo, int32_t *level,
+                        int32_t *parent, int32_t *cand, int32_t *wcnt,
+                        unsigned long long *status, int p_max, int grain, int level_no, int reps,
+                        float *ms_out, int *cands_out) {
+  Ctl *ctl = nullptr;
+  cudaMalloc(&ctl, sizeof(Ctl));
+  {  // P_max = resident CTAs, as s3bfs_create computes it
+    int dev, sms, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_explore, KD_THREADS, 0);
+    p_max = sms * (occ > 0 ? occ : 1);
+  }
+  Params P{};
+  P.col = col; P.vinfo = vinfo; P.n = n; P.ctl = ctl;
+  P.f[0] = P.f[1] = f; P.frs[0] = P.frs[1] = frs; P.fex[0] = P.fex[1] = fex;
+  P.cand = cand; P.bm = bm; P.claim = claim; P.wcnt = wcnt; P.status = status;
+  P.p_max = p_max; P.grain = grain; P.t0 = -1;
+  long long pt = ((long long)e_l + grain - 1) / grain;
+  if (pt > p_max) pt = p_max;
+  const long long chunk = ((long long)e_l + pt - 1) / pt;
+  Ctl h{};
+  h.level = level_no; h.n_l = n_l; h.e_l = e_l; h.cur = 0; h.tier = TIER_LARGE;
+  h.p_l = (int)(((long long)e_l + chunk - 1) / chunk); h.chunk = (int)chunk;
+  h.wcap = (int)((chunk + KD_WARPS - 1) / KD_WARPS);
+  h.level_out = level; h.parent_out = parent;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  float tot = 0.f;
+  int cands = 0;
+  for (int r = 0; r <= reps; ++r) {
+    cudaMemcpy(ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice);
+    cudaMemset(claim, 0, ((size_t)n + 15) / 16 * 16);
+    cudaDeviceSynchronize();
+    cudaEventRecord(a);
+    k_explore<<<h.p_l, KD_THREADS, 0>>>(P);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (r) tot += ms;  // r == 0 is the warm-up
+  }
+  int *hw = new int[h.p_l * KD_WARPS];
+  cudaMemcpy(hw, wcnt, sizeof(int) * h.p_l * KD_WARPS, cudaMemcpyDeviceToHost);
+  for (int i = 0; i < h.p_l * KD_WARPS; ++i) cands += hw[i];
+  delete[] hw;
+  *ms_out = tot / reps;
+  *cands_out = cands;
+  cudaFree(ctl);
+  return (int)cudaGetLastError();
+}
+
+// ---- raw access-pattern ceilings (experiment only) ----
+__global__ void k_stream_all(const int4 *p, long long n4, int *sink) {
+  int acc = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int4 v = __ldg(p + i);
+    acc += v.x ^ v.y ^ v.z ^ v.w;
+  }
+  if (acc == 0x7fffffff) *sink = acc;
+}
+// one warp per frontier row (grid-stride over rows), lanes stride the row
+__global__ void k_rows(const int32_t *col, const int32_t *frs, const int32_t *fex, int n_l,
+                       int *sink) {
+  const int lane = threadIdx.x & 31;
+  int acc = 0;
+  for (long long u = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n_l;
+       u += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const int s = __ldg(frs + u), d = __ldg(fex + u + 1) - __ldg(fex + u);
+    for (int j = lane; j < d; j += 32) acc += __ldg(col + s + j);
+  }
+  if (acc == 0x7fffffff) *sink = acc;
+}
+// same, plus the visited-bitmap probe per arc
+__global__ void k_rows_bm(const int32_t *col, const int32_t *frs, const int32_t *fex, int n_l,
+                          const uint32_t *bm, int *sink) {
+  const int lane = threadIdx.x & 31;
+  int acc = 0;
+  for (long long u = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n_l;
+       u += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const int s = __ldg(frs + u), d = __ldg(fex + u + 1) - __ldg(fex + u);
+    for (int j = lane; j < d; j += 32) {
+      const int v = __ldg(col + s + j);
+      acc += (__ldg(bm + (v >> 5)) >> (v & 31)) & 1;
+    }
+  }
+  if (acc == 0x7fffffff) *sink = acc;
+}
+extern "C" int kx_raw(const int32_t *col, long long nnz, const int32_t *frs, const int32_t *fex,
+                      int n_l, const uint32_t *bm, int which, int reps, float *ms_out) {
+  int *sink;
+  cudaMalloc(&sink, 4);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  float tot = 0.f;
+  int dev; cudaGetDevice(&dev);
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  for (int r = 0; r <= reps; ++r) {
+    cudaEventRecord(a);
+    if (which == 0) k_stream_all<<<sms * 8, 512>>>((const int4 *)col, nnz / 4, sink);
+    else if (which == 1) k_rows<<<sms * 4, 512>>>(col, frs, fex, n_l, sink);
+    else k_rows_bm<<<sms * 4, 512>>>(col, frs, fex, n_l, bm, sink);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    if (r) tot += ms;
+  }
+  *ms_out = tot / reps;
+  cudaFree(sink);
+  return (int)cudaGetLastError();
+}

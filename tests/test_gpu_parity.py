@@ -25,6 +25,8 @@ SETTINGS = [
     ("graph-3ctas", dict(debug_poison=1, tier0_max_edges=-1, max_ctas=3, edges_per_cta=64)),
     ("host-loop", dict(debug_poison=1, loop_mode=2, tier0_max_edges=512)),
     ("work-insensitive", dict(debug_poison=1, variant=1)),
+    ("grain-4096-T0-1", dict(debug_poison=1, tier0_max_edges=1, edges_per_cta=4096)),
+    ("no-reorder", dict(debug_poison=1, reorder=-1, tier0_max_edges=64)),
 ]
 
 
@@ -113,7 +115,7 @@ def test_random_multigraphs(seed):
     g = graphgen.from_edges(n, np.stack([src, dst], 1), symmetrize=bool(seed % 2),
                             name=f"rand{seed}")
     ro, col = to_dev(g)
-    for _, kw in SETTINGS[:5]:
+    for _, kw in SETTINGS[:5] + SETTINGS[-2:]:
         bfs = pkg.S3BFS(ro, col, pkg.Options(**kw))
         for s in rng.choice(n, 3, replace=False):
             check_traversal(g, bfs, int(s))
