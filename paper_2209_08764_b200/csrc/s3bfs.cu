@@ -132,7 +132,7 @@ s3bfs_status build_reordered(s3bfs_ctx *h, cudaStream_t st) {
   CK(h, cudaMemsetAsync(status, 0, (size_t)tiles * 8, st));
   k_scan_u32<<<tiles, SCAN_THREADS, 0, st>>>(deg, ro2, n, status);
   k_relabel_rows<<<h->num_sms * 16, 256, 0, st>>>(h->ro, h->col, n2o, o2n, ro2, n, col2);
-  k_build_vinfo<<<grid, 256, 0, st>>>(ro2, n, h->P.vinfo);
+  k_build_vinfo<<<grid, 256, 0, st>>>(ro2, n2o, n, h->P.vinfo);
   CK(h, cudaGetLastError());
   cudaFreeAsync(status, st);
   cudaFreeAsync(tmp, st);
@@ -368,7 +368,7 @@ s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32
     s3bfs_status rs = build_reordered(h, stream);
     if (rs != S3BFS_OK) return bail(rs);
   } else {
-    k_build_vinfo<<<h->num_sms * 8, 256, 0, stream>>>(row_offsets, n, P.vinfo);
+    k_build_vinfo<<<h->num_sms * 8, 256, 0, stream>>>(row_offsets, nullptr, n, P.vinfo);
     if ((e = cudaGetLastError()) != cudaSuccess) return bail(cuda_fail(h, e, "k_build_vinfo"));
   }
   if ((e = cudaMemsetAsync(P.ctl, 0, sizeof(Ctl), stream)) != cudaSuccess) return bail(cuda_fail(h, e, "memset(ctl)"));

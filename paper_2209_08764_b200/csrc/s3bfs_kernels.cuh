@@ -89,14 +89,15 @@ struct Ctl {
 
 struct Params {
   const int32_t *col;           // internal adjacency (degree-ordered copy, or the caller's)
-  int4 *vinfo;                  // per internal vertex: {row start, degree, -, Owner (Fig1 L3;
-                                //  never initialised, R3)} -- one sector per k_compact probe
-  int2 *lp;                     // per internal vertex: {d, parent (internal id)}, valid where
+  int4 *vinfo;                  // per internal vertex: {row start, degree, caller id, Owner
+                                //  (Fig1 L3; never initialised, R3)} -- one sector per probe
+  int2 *lp;                     // per internal vertex: {d, parent (caller id)}, valid where
                                 //  the visited bit is set
   const int32_t *n2o, *o2n;     // internal -> caller ids and back (NULL: identity)
   int32_t n;
   Ctl *ctl;
-  int32_t *f[2], *frs[2], *fex[2];  // frontier: internal ids, row starts, exclusive degree scan
+  int32_t *f[2], *frs[2], *fex[2];  // frontier: caller ids (parents of the next level's
+                                    // discoveries), internal row starts, degree scan
   int32_t *cand;                // candidate per slot (k_explore), compacted by k_compact
   int2 *cand_rd;                // (row start, degree) of kept candidates, pass 1 -> pass 2
   uint32_t *bm;                 // visited bitmap: bit set => visited (exact at level start)
@@ -346,8 +347,8 @@ __global__ void k_init(Params P, int32_t s, int32_t *level, int32_t *parent) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     Ctl *c = P.ctl;
     const int4 vs = P.vinfo[si];
-    P.lp[si] = make_int2(0, si);
-    P.f[0][0] = si;       // Fig1 L7: CurLevelVertices <- [s]
+    P.lp[si] = make_int2(0, s);
+    P.f[0][0] = s;        // Fig1 L7: CurLevelVertices <- [s]
     P.frs[0][0] = vs.x;
     P.fex[0][0] = 0;      // exclusive degree scan of the frontier (R5)
     P.fex[0][1] = vs.y;
@@ -473,32 +474,35 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
         v[g] = (my_e < bend) ? ldg_stream(col + pos, pol_stream) : -1;
       }
     }
-    // visited test: the bitmap (visited before this level), then the claim tag
-    bool need[KX_GROUPS];
+    // visited test: the bitmap (visited before this level), branch-free (an invalid slot
+    // probes word 0 and is masked); the claim/discovery code runs only if some lane of the
+    // warp met a vertex not visited at level start -- rare on the heavy levels
+    uint32_t needm = 0;
 #pragma unroll
     for (int g = 0; g < KX_GROUPS; ++g) {
-      need[g] = false;
-      if (v[g] >= 0) {
-        const uint32_t w = S3BFS_BM_NC ? ldg_status_u32(bm + (v[g] >> 5), pol_status)
-                                       : ld_status_u32(bm + (v[g] >> 5), pol_status);
-        need[g] = !((w >> (v[g] & 31)) & 1u);
-      }
+      const int vv = max(v[g], 0);
+      const uint32_t w = S3BFS_BM_NC ? ldg_status_u32(bm + (vv >> 5), pol_status)
+                                     : ld_status_u32(bm + (vv >> 5), pol_status);
+      if (v[g] >= 0 && !((w >> (vv & 31)) & 1u)) needm |= 1u << g;
     }
-    int cl[KX_GROUPS];
+    if (__any_sync(0xffffffffu, needm != 0)) {
+      int cl[KX_GROUPS];  // claim tags of the vertices not visited at level start
 #pragma unroll
-    for (int g = 0; g < KX_GROUPS; ++g) cl[g] = need[g] ? ld_cg_u8(claim + v[g]) : tag;
+      for (int g = 0; g < KX_GROUPS; ++g)
+        cl[g] = ((needm >> g) & 1u) ? ld_cg_u8(claim + v[g]) : tag;
 #pragma unroll
-    for (int g = 0; g < KX_GROUPS; ++g) {
-      const bool disc = need[g] && cl[g] != tag;
-      const unsigned m = __ballot_sync(0xffffffffu, disc);
-      if (disc) {
-        const int slot = segbase + wcount + __popc(m & lanemask_lt());
-        st_u8(claim + v[g], tag);
-        st_weak_v2(lp + v[g], new_level, xv[g]);   // d[v] <- l, parent (Fig1 L18)
-        st_weak(owner_of(vinfo, v[g]), slot);      // Owner[v] <- i (benign race)
-        cand[slot] = v[g];                         // Q[i].Enqueue(v)
+      for (int g = 0; g < KX_GROUPS; ++g) {
+        const bool disc = cl[g] != tag;
+        const unsigned m = __ballot_sync(0xffffffffu, disc);
+        if (disc) {
+          const int slot = segbase + wcount + __popc(m & lanemask_lt());
+          st_u8(claim + v[g], tag);
+          st_weak_v2(lp + v[g], new_level, xv[g]);   // d[v] <- l, parent (Fig1 L18)
+          st_weak(owner_of(vinfo, v[g]), slot);      // Owner[v] <- i (benign race)
+          cand[slot] = v[g];                         // Q[i].Enqueue(v)
+        }
+        wcount += __popc(m);
       }
-      wcount += __popc(m);
     }
     e = min(e + KX_GROUPS * 32, bend);
   }
@@ -510,6 +514,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
 // Pass 1 (Fig1 L20-L23): keep cand[k] iff Owner[cand[k]] == k (one 16-byte vertex-record
 // probe gives Owner, row start and degree); publish the kept vertex's visited bit and
 // compact (id, row start, degree) in place -- the degree is Fig1 L13 of the next level.
+// The next frontier holds caller ids (from the same record), the parents k_explore records.
 // A decoupled look-back over CTAs scans the (kept, degree-sum) pairs (Fig1 L24 and L14 of
 // the next level in one pass).  Pass 2 (Fig1 L25-L29): write the next frontier, its row
 // starts and its exclusive degree scan.  The last CTA to finish advances the control block
@@ -539,7 +544,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
       const int k = k0 + g * 32 + lane;
       v[g] = (k < cnt) ? cand[seg + k] : -1;
     }
-    int4 vi[KC_GROUPS];  // {row start, degree, -, Owner}: one sector per candidate
+    int4 vi[KC_GROUPS];  // {row start, degree, caller id, Owner}: one sector per candidate
 #pragma unroll
     for (int g = 0; g < KC_GROUPS; ++g)
       vi[g] = (v[g] >= 0) ? __ldg(vinfo + v[g]) : make_int4(0, 0, 0, -1);
@@ -552,7 +557,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       if (keep) {
         const int q = seg + kept + __popc(m & lanemask_lt());
-        cand[q] = v[g];
+        cand[q] = vi[g].z;
         crd[q] = make_int2(vi[g].x, d);
       }
       kept += __popc(m);
@@ -640,8 +645,8 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
   Ctl *c = P.ctl;
   if (c->tier != TIER_SMALL) return;
   extern __shared__ int32_t smem[];
-  int32_t *sf = smem;                 // CurLevelVertices
-  int32_t *srs = sf + KS_NCAP;        // row starts
+  int32_t *sf = smem;                 // CurLevelVertices (caller ids)
+  int32_t *srs = sf + KS_NCAP;        // internal row starts
   int32_t *sex = srs + KS_NCAP;       // exclusive degree scan, KS_NCAP + 1 entries
   int32_t *cv = sex + KS_NCAP + 4;    // candidate per level-local edge (or -1)
   int32_t *cpv = cv + KS_ECAP;        // its discoverer
@@ -701,7 +706,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
         if (v >= 0) {
           const int4 vi = ld_weak_v4(vinfo + v);  // same-SM writes: L1-coherent
           if (vi.w == e) {
-            kv[i] = v; kr[i] = vi.x; kd[i] = vi.y;
+            kv[i] = vi.z; kr[i] = vi.x; kd[i] = vi.y;
             P.lp[v] = make_int2(L + 1, cpv[e]);         // d[v] <- l, parent (Fig1 L18)
             atomicOr(P.bm + (v >> 5), 1u << (v & 31));  // exact visited bit (not discovery)
           }
@@ -770,8 +775,8 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
 
 // ---- d[0:n-1] in caller ids --------------------------------------------------------------
 // level[o] = d of internal vertex o2n[o] if its visited bit is set, else -1 (unreachable, R1);
-// parent[o] = the parent's caller id (R2).  Reads the internal records in caller order; the
-// caller's arrays are written exactly once, coalesced.
+// parent[o] = its recorded parent (a caller id, R2).  Reads the internal records in caller
+// order; the caller's arrays are written exactly once, coalesced.
 __global__ void k_finalize(Params P) {
   const Ctl *c = P.ctl;
   int32_t *__restrict__ level = c->level_out;
@@ -784,7 +789,7 @@ __global__ void k_finalize(Params P) {
     if ((__ldg(P.bm + (i >> 5)) >> (i & 31)) & 1u) {
       const int2 r = __ldg(P.lp + i);
       lv = r.x;
-      pa = P.n2o ? __ldg(P.n2o + r.y) : r.y;
+      pa = r.y;
     }
     level[o] = lv;
     parent[o] = pa;
@@ -820,11 +825,11 @@ __global__ void k_relabel_rows(const int32_t *ro, const int32_t *col, const int3
     for (int j = lane; j < len; j += 32) col2[d + j] = o2n[col[s + j]];
   }
 }
-// vinfo[i] = {row start, degree, 0, Owner = 0} over a CSR's row offsets
-__global__ void k_build_vinfo(const int32_t *ro, int n, int4 *vinfo) {
+// vinfo[i] = {row start, degree, caller id, Owner = 0} over a CSR's row offsets
+__global__ void k_build_vinfo(const int32_t *ro, const int32_t *n2o, int n, int4 *vinfo) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
-    vinfo[i] = make_int4(ro[i], ro[i + 1] - ro[i], 0, 0);
+    vinfo[i] = make_int4(ro[i], ro[i + 1] - ro[i], n2o ? n2o[i] : (int)i, 0);
 }
 
 // ---- test entry kernels ---------------------------------------------------------------------

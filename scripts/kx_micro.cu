@@ -3,7 +3,8 @@
 #include "../paper_2209_08764_b200/csrc/s3bfs_kernels.cuh"
 using namespace s3bfs;
 extern "C" int kx_micro(const int32_t *col, int n, int n_l, int e_l, int32_t *f, int32_t *frs,
-                        int32_t *fex, uint32_t *bm, uint8_t *claim, int4 *vinfo, int32_t *level,
+                        int32_t *fex, uint32_t *bm, uint8_t *claim, int4 *vinfo, int2 *lp,
+                        int32_t *level,
                         int32_t *parent, int32_t *cand, int32_t *wcnt,
                         unsigned long long *status, int p_max, int grain, int level_no, int reps,
                         float *ms_out, int *cands_out) {
@@ -17,7 +18,7 @@ extern "C" int kx_micro(const int32_t *col, int n, int n_l, int e_l, int32_t *f,
     p_max = sms * (occ > 0 ? occ : 1);
   }
   Params P{};
-  P.col = col; P.vinfo = vinfo; P.n = n; P.ctl = ctl;
+  P.col = col; P.vinfo = vinfo; P.lp = lp; P.n = n; P.ctl = ctl;
   P.f[0] = P.f[1] = f; P.frs[0] = P.frs[1] = frs; P.fex[0] = P.fex[1] = fex;
   P.cand = cand; P.bm = bm; P.claim = claim; P.wcnt = wcnt; P.status = status;
   P.p_max = p_max; P.grain = grain; P.t0 = -1;

@@ -39,6 +39,7 @@ if relabel:  # degree-descending internal ids (experiment: hot vertices get the 
     deg = deg2
     torch.cuda.synchronize()
 L = int(lvl.max().item())
+lpbuf = torch.zeros((n, 2), dtype=torch.int32, device=dev)
 vinfo = torch.zeros((n, 4), dtype=torch.int32, device=dev)
 vinfo[:, 0] = ro[:-1]
 vinfo[:, 1] = deg
@@ -87,11 +88,12 @@ for l, fr, e_l in levels:
             cands = ctypes.c_int()
             vp = ctypes.c_void_p
             lib.kx_micro.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp,
-                                     vp, vp, vp, vp, vp, vp, vp, ctypes.c_int, ctypes.c_int,
+                                     vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int, ctypes.c_int,
                                      ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_float),
                                      ctypes.POINTER(ctypes.c_int)]
             rc = lib.kx_micro(col.data_ptr(), n, f.numel(), e_l, f.data_ptr(), frs.data_ptr(),
                               fex.data_ptr(), bm.data_ptr(), claim.data_ptr(), vinfo.data_ptr(),
+                              lpbuf.data_ptr(),
                               out_l.data_ptr(), out_p.data_ptr(), cand.data_ptr(),
                               wcnt.data_ptr(), status.data_ptr(), 296, 16384, l, 5,
                               ctypes.byref(ms), ctypes.byref(cands))
