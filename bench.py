@@ -125,6 +125,26 @@ def launches_from_stats(st) -> int:
     return 1 + iterations + segs0 + 2 * t1
 
 
+def shard_sources(srcs, rank: int, world: int) -> list:
+    """Rank r's traversal order: the config's sources rotated by r (replicas, weak scaling:
+    every rank runs the same number of independent traversals, no data-path collective)."""
+    return [srcs[(rank + k) % len(srcs)] for k in range(len(srcs))]
+
+
+def job_throughput(my_ms: float, my_edges: float, dev, world: int):
+    """Whole-job GTEPS: edges summed over ranks / device time max-reduced over ranks.
+    Returns (gteps, max_ms, total_edges).  Plain values when world == 1."""
+    import torch
+    t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
+    e = torch.tensor([my_edges], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(e, op=dist.ReduceOp.SUM)
+    max_ms, tot = float(t.item()), float(e.item())
+    return tot / (max_ms / 1e3) / 1e9, max_ms, tot
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -204,7 +224,7 @@ def main():
     # ---- untimed: per-source edge counts (m_c from the traversal's own levels), launches,
     # and bit-exact oracle checks + CPU baseline on a bounded sample of sources ------------
     srcs = g.sources
-    my_srcs = [srcs[(rank + world * k) % len(srcs)] for k in range(len(srcs))]
+    my_srcs = shard_sources(srcs, rank, world)
     per = {}
     for s in sorted(set(my_srcs)):
         pkg.s3bfs_run_ptr(bfs.handle, s, lp, pp, sp)
@@ -265,13 +285,7 @@ def main():
     my_ms = float(sum(step_ms))
     my_edges = sum(per[s]["m_c"] // 2 for s in done_srcs)
     my_launches = sum(per[s]["launches"] for s in done_srcs)
-    t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
-    e = torch.tensor([my_edges], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(e, op=dist.ReduceOp.SUM)
-    max_ms, tot_edges = float(t.item()), float(e.item())
-    value = tot_edges / (max_ms / 1e3) / 1e9
+    value, max_ms, tot_edges = job_throughput(my_ms, my_edges, dev, world)
     per_step_gteps = [per[s]["m_c"] / 2 / (ms / 1e3) / 1e9 for s, ms in zip(done_srcs, step_ms)]
     hmean = len(per_step_gteps) / sum(1.0 / x for x in per_step_gteps)
 
@@ -293,12 +307,7 @@ def main():
         b.synchronize()
         e2e_ms += a.elapsed_time(b)
         e2e_edges += per[s]["m_c"] // 2
-    te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-    ee = torch.tensor([e2e_edges], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        dist.all_reduce(ee, op=dist.ReduceOp.SUM)
-    e2e_value = float(ee.item()) / (float(te.item()) / 1e3) / 1e9
+    e2e_value, _, _ = job_throughput(e2e_ms, e2e_edges, dev, world)
 
     # ---- roofline of k_explore: per-launch CUDA events (host-loop pass, same kernels) -----
     roof = None

@@ -16,13 +16,14 @@ ap.add_argument("--config", default="rmat24")
 ap.add_argument("--source-index", type=int, default=0)
 ap.add_argument("--loop-mode", type=int, default=2)
 ap.add_argument("--runs", type=int, default=1)
+ap.add_argument("--all", action="store_true", help="one run from every source of the config")
 a = ap.parse_args()
 g = graphgen.make_config(a.config)
 ro = torch.from_numpy(g.row_offsets).cuda()
 col = torch.from_numpy(g.col_indices).cuda()
 bfs = pkg.S3BFS(ro, col, pkg.Options(loop_mode=a.loop_mode))
-s = g.sources[a.source_index]
-for _ in range(a.runs):
+srcs = g.sources if a.all else [g.sources[a.source_index]] * a.runs
+for s in srcs:
     level, parent = bfs.run(s)
 torch.cuda.synchronize()
 st = bfs.level_stats()

@@ -1,0 +1,57 @@
+"""The N>1 bench path on CPU: world-size-2 gloo processes run the same sharding and
+max-over-ranks / sum-over-ranks reductions bench.py uses under torchrun (replicas only:
+independent sources, no data-path collective -- DESIGN.md s.9)."""
+import os
+import socket
+import sys
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, out):
+    sys.path.insert(0, ROOT)
+    import bench
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    srcs = list(range(100, 116))
+    mine = bench.shard_sources(srcs, rank, world)
+    # per-rank device time and edges (rank-dependent so the reductions are checked)
+    gteps, max_ms, tot = bench.job_throughput(10.0 + rank, 1e9 * (rank + 1), "cpu", world)
+    out[rank] = (mine, gteps, max_ms, tot)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_sharding_and_reductions():
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_worker, args=(2, port, out), nprocs=2, join=True)
+        res = dict(out)
+    m0, m1 = res[0][0], res[1][0]
+    assert sorted(m0) == sorted(m1) == list(range(100, 116))   # each rank: every source once
+    assert m0[0] != m1[0]                                       # different traversal order
+    for r in (0, 1):
+        _, gteps, max_ms, tot = res[r]
+        assert max_ms == 11.0                                   # max over ranks
+        assert tot == 3e9                                       # sum over ranks
+        assert abs(gteps - 3e9 / 0.011 / 1e9) < 1e-9
+
+
+def test_single_rank_is_plain():
+    sys.path.insert(0, ROOT)
+    import bench
+    g, ms, tot = bench.job_throughput(2.0, 4e9, "cpu", 1)
+    assert ms == 2.0 and tot == 4e9 and abs(g - 2000.0) < 1e-9
+    assert bench.shard_sources([1, 2, 3], 0, 1) == [1, 2, 3]
