@@ -288,7 +288,7 @@ s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32
   if (occ < 1) occ = 1;
   int p_max = h->num_sms * occ;  // every CTA resident: the look-back never waits on a CTA
   if (h->opt.max_ctas > 0 && h->opt.max_ctas < p_max) p_max = h->opt.max_ctas;
-  const int grain = h->opt.edges_per_cta > 0 ? h->opt.edges_per_cta : 16384;
+  const int grain = h->opt.edges_per_cta > 0 ? h->opt.edges_per_cta : 2048;
   int t0 = h->opt.tier0_max_edges == 0 ? KS_ECAP : h->opt.tier0_max_edges;
   if (t0 > KS_ECAP) t0 = KS_ECAP;
   if (h->opt.variant == 1) t0 = -1;

@@ -46,6 +46,12 @@ namespace s3bfs {
 #ifndef S3BFS_KX_FAST
 #define S3BFS_KX_FAST 1   // uniform-row fast path
 #endif
+#ifndef S3BFS_KS_LOCKSTEP
+#define S3BFS_KS_LOCKSTEP 0
+#endif
+#ifndef S3BFS_KS_BATCHED
+#define S3BFS_KS_BATCHED 1
+#endif
 #ifndef S3BFS_BM_NC
 #define S3BFS_BM_NC 1     // bitmap probes through the non-coherent (read-only) path
 #endif
@@ -632,6 +638,78 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
   }
 }
 
+// ---- tier 0, warp path: consecutive tiny levels (n_l <= 32, e_l <= 32) ---------------------------
+// Run by warp 0 of k_small alone, frontier in registers (lane u holds frontier vertex u), no
+// CTA barrier: lane i takes edge i (its vertex by a 5-step shuffle search of the degree
+// scan), loads col, then the visited word and the vertex record together.  Duplicates among
+// the warp's lanes are removed by __match_any_sync -- the same "one copy survives" rule as
+// the Owner check (R4), without the Owner round trip.  Returns when the next level is not
+// tiny (or empty), leaving that frontier in shared memory and its (n, e, level) in st[].
+__device__ void tiny_levels(const Params &P, Ctl *c, int32_t *sf, int32_t *srs, int32_t *sex,
+                            int32_t *st, unsigned long long &t_prev) {
+  const int lane = threadIdx.x & 31;
+  const int32_t *__restrict__ col = P.col;
+  int n_l = st[0], e_l = st[1], L = st[2];
+  const int lim_e = (P.t0 >= 0 && P.t0 < 32) ? P.t0 : 32;
+  int fx = lane < n_l ? sf[lane] : 0;
+  int frs = lane < n_l ? srs[lane] : 0;
+  int fex = lane < n_l ? sex[lane] : 0x7fffffff;
+  for (;;) {
+    int u = 0;
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+      const int cu = __shfl_sync(0xffffffffu, fex, u + s);
+      if (cu <= lane) u += s;
+    }
+    const int px = __shfl_sync(0xffffffffu, fx, u);
+    const int pr = __shfl_sync(0xffffffffu, frs, u);
+    const int pe = __shfl_sync(0xffffffffu, fex, u);
+    const bool has = lane < e_l;
+    const int v = has ? __ldg(col + pr + (lane - pe)) : 0;
+    const uint32_t w = __ldcg(P.bm + (v >> 5));      // published by atomicOr at L2
+    const int4 vi = __ldg(P.vinfo + v);               // issued together with the bitmap word
+    const bool fresh = has && !((w >> (v & 31)) & 1u);
+    const unsigned mm = __match_any_sync(0xffffffffu, fresh ? v : -1 - lane);
+    const bool keep = fresh && lane == __ffs(mm) - 1;
+    const unsigned km = __ballot_sync(0xffffffffu, keep);
+    const int ncand = __popc(__ballot_sync(0xffffffffu, fresh));
+    if (keep) {
+      P.lp[v] = make_int2(L + 1, px);                 // d[v] <- l, parent (Fig1 L18)
+      atomicOr(P.bm + (v >> 5), 1u << (v & 31));      // exact visited bit
+    }
+    const int d = keep ? vi.y : 0;
+    const int inc = warp_incl_scan(d);
+    const int n_next = __popc(km), e_next = __shfl_sync(0xffffffffu, inc, 31);
+    const int src = lane < n_next ? (int)__fns(km, 0, lane + 1) : 0;
+    const int nfx = __shfl_sync(0xffffffffu, vi.z, src);
+    const int nfr = __shfl_sync(0xffffffffu, vi.x, src);
+    const int nfe = __shfl_sync(0xffffffffu, inc - d, src);
+    if (lane == 0) {
+      const unsigned long long t = globaltimer();
+      record_stat(P, c, L, n_l, e_l, TIER_SMALL, 1, ncand, n_next, t_prev, t);
+      t_prev = t;
+    }
+    fx = lane < n_next ? nfx : 0;
+    frs = lane < n_next ? nfr : 0;
+    fex = lane < n_next ? nfe : 0x7fffffff;
+    ++L;
+    n_l = n_next;
+    e_l = e_next;
+    if (n_l == 0 || e_l == 0 || n_l > 32 || e_l > lim_e) break;
+  }
+  if (lane < n_l) {
+    sf[lane] = fx;
+    srs[lane] = frs;
+    sex[lane] = fex;
+  }
+  if (lane == 0) {
+    sex[n_l] = e_l;
+    st[0] = n_l;
+    st[1] = e_l;
+    st[2] = L;
+  }
+}
+
 // ---- tier 0: k_small -------------------------------------------------------------------------
 // One CTA runs consecutive tiny levels (e_l <= T0) with __syncthreads between the steps: the
 // paper's "use only as many cores as there is work" at CTA granularity.  Same
@@ -652,6 +730,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
   int32_t *cpv = cv + KS_ECAP;        // its discoverer
   __shared__ int32_t s_wk[KS_THREADS / 32], s_wd[KS_THREADS / 32], s_wc[KS_THREADS / 32];
   __shared__ int32_t s_tot[3];
+  __shared__ int32_t s_tiny[3];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int32_t *__restrict__ col = P.col;
@@ -669,25 +748,74 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
   __syncthreads();
 
   for (;;) {
-    // (c)+(d): explore, edge e -> vertex u by binary search of the smem degree scan
+    if (n_l <= 32 && e_l <= 32) {  // tiny levels: warp 0 alone, no CTA barrier per level
+      if (tid == 0) { s_tiny[0] = n_l; s_tiny[1] = e_l; s_tiny[2] = L; }
+      __syncwarp();
+      if (warp == 0) tiny_levels(P, c, sf, srs, sex, s_tiny, t_prev);
+      __syncthreads();
+      n_l = s_tiny[0];
+      e_l = s_tiny[1];
+      L = s_tiny[2];
+      if (n_l == 0 || e_l == 0 || P.t0 < 0 || e_l > P.t0 || n_l > KS_NCAP) break;
+      continue;
+    }
+    // (c)+(d): explore, edge e -> vertex u by binary search of the smem degree scan; a
+    // thread's (<= KS_IPT) edges issue their col loads together, then their visited probes
     int ncand = 0;
-    for (int e = tid; e < e_l; e += KS_THREADS) {
-      int lo = 0, hi = n_l;
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (sex[mid] <= e) lo = mid; else hi = mid;
+    int ev[KS_IPT], ux[KS_IPT], lo[KS_IPT], hi[KS_IPT];
+#pragma unroll
+    for (int i = 0; i < KS_IPT; ++i) { lo[i] = 0; hi[i] = n_l; }
+#if S3BFS_KS_LOCKSTEP
+    for (int span = n_l; span > 1; span = (span + 1) >> 1) {  // the KS_IPT searches in lock-step
+#pragma unroll
+      for (int i = 0; i < KS_IPT; ++i) {
+        const int e = tid + i * KS_THREADS;
+        if (hi[i] - lo[i] > 1) {
+          const int mid = (lo[i] + hi[i]) >> 1;
+          if (sex[mid] <= e) lo[i] = mid; else hi[i] = mid;
+        }
       }
-      const int v = __ldg(col + srs[lo] + (e - sex[lo]));
-      int w = -1;
-      // L1-bypassing read: the bits were published by atomicOr (at L2) in earlier levels of
-      // this same kernel, so an L1 line cached before that would be stale
-      if (!((__ldcg(bm + (v >> 5)) >> (v & 31)) & 1u)) {
-        st_weak(owner_of(vinfo, v), e);  // Owner[v] <- e (benign race)
-        w = v;
-        ++ncand;
+    }
+#else
+#pragma unroll
+    for (int i = 0; i < KS_IPT; ++i) {
+      const int e = tid + i * KS_THREADS;
+      if (e < e_l) {
+        while (hi[i] - lo[i] > 1) {
+          const int mid = (lo[i] + hi[i]) >> 1;
+          if (sex[mid] <= e) lo[i] = mid; else hi[i] = mid;
+        }
       }
-      cv[e] = w;
-      cpv[e] = sf[lo];
+    }
+#endif
+#pragma unroll
+    for (int i = 0; i < KS_IPT; ++i) {
+      const int e = tid + i * KS_THREADS;
+      ev[i] = -1;
+      ux[i] = 0;
+      if (e < e_l) {
+        ux[i] = sf[lo[i]];
+        ev[i] = __ldg(col + srs[lo[i]] + (e - sex[lo[i]]));
+      }
+    }
+    uint32_t wv[KS_IPT];
+#pragma unroll
+    for (int i = 0; i < KS_IPT; ++i)  // L1-bypassing: bits are published by atomicOr at L2 in
+      wv[i] = ev[i] >= 0 ? __ldcg(bm + (ev[i] >> 5)) : 0xffffffffu;  // earlier levels (H2)
+#pragma unroll
+    for (int i = 0; i < KS_IPT; ++i) {
+      const int e = tid + i * KS_THREADS;
+      if (e < e_l) {
+        const int v = ev[i];
+        int w = -1;
+        if (!((wv[i] >> (v & 31)) & 1u)) {
+          st_weak(owner_of(vinfo, v), e);  // Owner[v] <- e (benign race)
+          w = v;
+          ++ncand;
+        }
+        cv[e] = w;
+        cpv[e] = ux[i];
+      }
     }
     __syncthreads();
     // (e): owner check + next-level degree, blocked items for the scan
@@ -695,6 +823,29 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
     const int e0 = tid * ipt;
     int kv[KS_IPT], kr[KS_IPT], kd[KS_IPT];
     int cnt = 0, dsum = 0;
+#if S3BFS_KS_BATCHED
+    int4 vis[KS_IPT];  // all record loads first (one round trip for the thread's items)
+#pragma unroll
+    for (int i = 0; i < KS_IPT; ++i) {
+      const int e = e0 + i;
+      const int v = (i < ipt && e < e_l) ? cv[e] : -1;
+      kv[i] = v;
+      vis[i] = v >= 0 ? ld_weak_v4(vinfo + v) : make_int4(0, 0, 0, -1);  // same-SM: coherent
+    }
+#pragma unroll
+    for (int i = 0; i < KS_IPT; ++i) {
+      const int e = e0 + i;
+      const int v = kv[i];
+      kv[i] = -1;
+      kr[i] = 0;
+      kd[i] = 0;
+      if (v >= 0 && vis[i].w == e) {
+        kv[i] = vis[i].z; kr[i] = vis[i].x; kd[i] = vis[i].y;
+        P.lp[v] = make_int2(L + 1, cpv[e]);         // d[v] <- l, parent (Fig1 L18)
+        atomicOr(P.bm + (v >> 5), 1u << (v & 31));  // exact visited bit (not discovery)
+      }
+    }
+#else
 #pragma unroll
     for (int i = 0; i < KS_IPT; ++i) {
       kv[i] = -1;
@@ -713,6 +864,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
         }
       }
     }
+#endif
 #pragma unroll
     for (int i = 0; i < KS_IPT; ++i) {
       cnt += kv[i] >= 0;
