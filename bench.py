@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--loop-mode", type=int, default=0)
     ap.add_argument("--tier0", type=int, default=0)
     ap.add_argument("--grain", type=int, default=0)
+    ap.add_argument("--direction", type=int, default=0,
+                    help="1: direction-optimising traversal (NEXT-3); default: the paper's top-down")
     return ap.parse_args()
 
 
@@ -211,7 +213,7 @@ def main():
     col = torch.from_numpy(g.col_indices).to(dev)
     deg = (ro[1:] - ro[:-1]).to(torch.int64)
     opts = pkg.Options(loop_mode=args.loop_mode, tier0_max_edges=args.tier0,
-                       edges_per_cta=args.grain)
+                       edges_per_cta=args.grain, direction=args.direction)
     bfs = pkg.S3BFS(ro, col, opts)
     info = bfs.info()
     n = g.n
@@ -315,7 +317,7 @@ def main():
     if rank == 0:
         hb = pkg.S3BFS(ro, col, pkg.Options(loop_mode=2, time_kernels=1,
                                             tier0_max_edges=args.tier0,
-                                            edges_per_cta=args.grain))
+                                            edges_per_cta=args.grain, direction=args.direction))
         ex_ms, ex_launch, alg_bytes, cm_ms, sm_ms = 0.0, 0, 0, 0.0, 0.0
         step_ms_hl = 0.0
         for s in srcs:
@@ -380,7 +382,8 @@ def main():
                              if not args.no_flush else "not flushed (col 2 GB > L2)",
                        "loop": "cuda-graph" if args.loop_mode != 2 else "host",
                        "p_max": info["p_max"], "grain": info["edges_per_cta"],
-                       "t0": info["tier0_max_edges"]},
+                       "t0": info["tier0_max_edges"],
+                       "direction": "optimising (NEXT-3)" if args.direction else "top-down (S3BFS)"},
             "gteps_hmean": hmean, "gteps_min": min(per_step_gteps),
             "gteps_max": max(per_step_gteps),
             "roofline": roof, "cpu_baseline": cpu,

@@ -75,12 +75,18 @@ typedef struct {
   int32_t reorder;         /* 0/1: create builds an internal copy of the graph relabelled by
                               descending degree (outputs stay in caller ids); -1: traverse the
                               caller's arrays directly (no copy) */
-  int32_t reserved[6];
+  int32_t direction;       /* NEXT-3: 1 = direction-optimising -- a level runs
+                              bottom-up when e_l * alpha > arcs of unvisited vertices, and returns
+                              top-down when n_l * beta < n (Beamer); 0 = top-down S3BFS only */
+  int32_t do_alpha;        /* 0 -> 14 */
+  int32_t do_beta;         /* 0 -> 24; < 0 -> never switch back */
+  int32_t reserved[3];
 } s3bfs_options;
 
 /* One record per BFS level (the SPEC LevelStats analogue).  n_l = |frontier|
  * (Fig1 L9), e_l = sum of its degrees (Fig1 L15), tier 0 = single CTA, 1 = full kernels,
- * 2 = a last level with e_l = 0 (nothing explored), grid = CTAs used (P_l), candidates =
+ * 2 = a last level with e_l = 0 (nothing explored), 3 = bottom-up (NEXT-3), grid = CTAs used
+ * (P_l), candidates =
  * discoveries incl. benign-race duplicates, kept = n_{l+1} after owner dedup.  Times are
  * %globaltimer ns: level start (= previous level's end, so launch gaps count) and end; for
  * tier 1 also k_explore's start (its CTA 0) and k_compact's start (its CTA 0), whose
@@ -134,8 +140,8 @@ s3bfs_status s3bfs_get_info(s3bfs_handle h, s3bfs_info *out);
 /* CUDA-event kernel times of the last run (options.time_kernels = 1 and loop_mode = 2;
  * otherwise all zero).  Synchronises the run's stream. */
 typedef struct {
-  double explore_ms, compact_ms, small_ms;  /* summed over launches */
-  int32_t explore_launches, compact_launches, small_launches, pad;
+  double explore_ms, compact_ms, small_ms, bottom_up_ms;  /* summed over launches */
+  int32_t explore_launches, compact_launches, small_launches, bottom_up_launches;
 } s3bfs_kernel_times;
 s3bfs_status s3bfs_get_kernel_times(s3bfs_handle h, s3bfs_kernel_times *out);
 

@@ -19,6 +19,7 @@
 #include <string>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 
 #include "s3bfs_kernels.cuh"
 
@@ -34,6 +35,9 @@ struct s3bfs_ctx {
   void *ws = nullptr;
   void *graph2 = nullptr;  // degree-ordered internal CSR + id maps
   size_t graph2_bytes = 0;
+  void *graph3 = nullptr;  // transpose of a non-symmetric graph (NEXT-3 only)
+  size_t graph3_bytes = 0;
+  const int32_t *ro_int = nullptr;  // row offsets of the internal CSR
   size_t ws_bytes = 0;
   int64_t cand_cap = 0;
   size_t ks_smem = 0;
@@ -105,12 +109,14 @@ s3bfs_status build_reordered(s3bfs_ctx *h, cudaStream_t st) {
   auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return o; };
   const size_t o_col2 = take((size_t)nnz * 4 + 16);
   const size_t o_n2o = take((size_t)n * 4), o_o2n = take((size_t)n * 4);
+  const size_t o_ro2 = take((size_t)(n + 1) * 4);
   h->graph2_bytes = off;
   CK(h, cudaMalloc(&h->graph2, off));
   char *g = (char *)h->graph2;
   int32_t *col2 = (int32_t *)(g + o_col2);
   int32_t *n2o = (int32_t *)(g + o_n2o), *o2n = (int32_t *)(g + o_o2n);
-  int32_t *deg = nullptr, *deg_sorted = nullptr, *iota = nullptr, *ro2 = nullptr;
+  int32_t *deg = nullptr, *deg_sorted = nullptr, *iota = nullptr;
+  int32_t *ro2 = (int32_t *)(g + o_ro2);
   void *tmp = nullptr;
   size_t tmp_bytes = 0;
   CK(h, cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, deg, deg_sorted, iota,
@@ -118,7 +124,6 @@ s3bfs_status build_reordered(s3bfs_ctx *h, cudaStream_t st) {
   CK(h, cudaMallocAsync((void **)&deg, (size_t)n * 4, st));
   CK(h, cudaMallocAsync((void **)&deg_sorted, (size_t)n * 4, st));
   CK(h, cudaMallocAsync((void **)&iota, (size_t)n * 4, st));
-  CK(h, cudaMallocAsync((void **)&ro2, (size_t)(n + 1) * 4, st));
   CK(h, cudaMallocAsync(&tmp, tmp_bytes, st));
   const int grid = h->num_sms * 8;
   k_degrees<<<grid, 256, 0, st>>>(h->ro, n, deg, iota);
@@ -133,10 +138,15 @@ s3bfs_status build_reordered(s3bfs_ctx *h, cudaStream_t st) {
   k_scan_u32<<<tiles, SCAN_THREADS, 0, st>>>(deg, ro2, n, status);
   k_relabel_rows<<<h->num_sms * 16, 256, 0, st>>>(h->ro, h->col, n2o, o2n, ro2, n, col2);
   k_build_vinfo<<<grid, 256, 0, st>>>(ro2, n2o, n, h->P.vinfo);
+  int *d_nz = nullptr, h_nz = 0;
+  CK(h, cudaMallocAsync((void **)&d_nz, 4, st));
+  CK(h, cudaMemsetAsync(d_nz, 0, 4, st));
+  k_count_nonzero<<<grid, 256, 0, st>>>(deg, n, d_nz);  // internal degrees, descending
+  CK(h, cudaMemcpyAsync(&h_nz, d_nz, 4, cudaMemcpyDeviceToHost, st));
+  cudaFreeAsync(d_nz, st);
   CK(h, cudaGetLastError());
   cudaFreeAsync(status, st);
   cudaFreeAsync(tmp, st);
-  cudaFreeAsync(ro2, st);
   cudaFreeAsync(iota, st);
   cudaFreeAsync(deg_sorted, st);
   cudaFreeAsync(deg, st);
@@ -144,6 +154,80 @@ s3bfs_status build_reordered(s3bfs_ctx *h, cudaStream_t st) {
   h->P.col = col2;
   h->P.n2o = n2o;
   h->P.o2n = o2n;
+  h->P.n_scan = h_nz;  // internal ids >= h_nz have degree 0: bottom-up never scans them
+  h->ro_int = ro2;
+  return S3BFS_OK;
+}
+
+// Sort every row of a CSR by (internal) id, out of place: with degree-ordered ids the
+// highest-degree neighbours come first, where the bottom-up step finds its frontier parents.
+s3bfs_status sort_rows(s3bfs_ctx *h, const int32_t *ro, const int32_t *in, int32_t *out,
+                       cudaStream_t st) {
+  if (h->nnz == 0) return S3BFS_OK;
+  void *tmp = nullptr;
+  size_t bytes = 0;
+  CK(h, cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, in, out, (int)h->nnz, h->n, ro,
+                                           ro + 1, st));
+  CK(h, cudaMallocAsync(&tmp, bytes, st));
+  CK(h, cub::DeviceSegmentedSort::SortKeys(tmp, bytes, in, out, (int)h->nnz, h->n, ro, ro + 1,
+                                           st));
+  cudaFreeAsync(tmp, st);
+  return S3BFS_OK;
+}
+
+// NEXT-3: the in-adjacency the bottom-up step scans, rows sorted by internal id.  For a
+// symmetric graph (every BASELINE config) it is a row-sorted copy of the internal CSR;
+// otherwise the row-sorted transpose.  (The top-down adjacency stays in input order: sorted
+// rows make k_compact's visited-bit publication contend on shared words -- measured.)
+s3bfs_status build_in_adjacency(s3bfs_ctx *h, cudaStream_t st) {
+  const int n = h->n;
+  const long long nnz = h->nnz;
+  const int32_t *ro = h->ro_int, *col = h->P.col;
+  unsigned long long *d_h = nullptr, hh[2] = {0, 0};
+  CK(h, cudaMallocAsync((void **)&d_h, 16, st));
+  CK(h, cudaMemsetAsync(d_h, 0, 16, st));
+  k_sym_hash<<<h->num_sms * 16, 256, 0, st>>>(ro, col, n, d_h);
+  CK(h, cudaMemcpyAsync(hh, d_h, 16, cudaMemcpyDeviceToHost, st));
+  cudaFreeAsync(d_h, st);
+  CK(h, cudaStreamSynchronize(st));
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return o; };
+  const size_t o_tro = take((size_t)(n + 1) * 4), o_tcol = take((size_t)nnz * 4 + 16);
+  CK(h, cudaMalloc(&h->graph3, off));
+  h->graph3_bytes = off;
+  int32_t *tro = (int32_t *)((char *)h->graph3 + o_tro);
+  int32_t *tcol = (int32_t *)((char *)h->graph3 + o_tcol);
+  if (hh[0] == hh[1]) {
+    s3bfs_status ss = sort_rows(h, ro, col, tcol, st);
+    if (ss != S3BFS_OK) return ss;
+    CK(h, cudaStreamSynchronize(st));
+    h->P.tro = ro;
+    h->P.tcol = tcol;
+    return S3BFS_OK;
+  }
+  int32_t *tunsorted = nullptr;
+  CK(h, cudaMallocAsync((void **)&tunsorted, (size_t)nnz * 4 + 16, st));
+  int32_t *tdeg = nullptr;
+  CK(h, cudaMallocAsync((void **)&tdeg, (size_t)n * 4, st));
+  CK(h, cudaMemsetAsync(tdeg, 0, (size_t)n * 4, st));
+  k_in_degree<<<h->num_sms * 16, 256, 0, st>>>(ro, col, n, tdeg);
+  const int tiles = (int)(((long long)n + SCAN_TILE - 1) / SCAN_TILE);
+  unsigned long long *status = nullptr;
+  CK(h, cudaMallocAsync((void **)&status, (size_t)tiles * 8, st));
+  CK(h, cudaMemsetAsync(status, 0, (size_t)tiles * 8, st));
+  k_scan_u32<<<tiles, SCAN_THREADS, 0, st>>>(tdeg, tro, n, status);
+  CK(h, cudaMemcpyAsync(tdeg, tro, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));  // cursors
+  k_transpose<<<h->num_sms * 16, 256, 0, st>>>(ro, col, n, tdeg, tunsorted);
+  CK(h, cudaGetLastError());
+  s3bfs_status ss = sort_rows(h, tro, tunsorted, tcol, st);
+  if (ss != S3BFS_OK) return ss;
+  cudaFreeAsync(tunsorted, st);
+  cudaFreeAsync(status, st);
+  cudaFreeAsync(tdeg, st);
+  CK(h, cudaStreamSynchronize(st));
+  h->P.tro = tro;
+  h->P.tcol = tcol;
+  h->P.n_scan = n;  // the degree-order prefix is by out-degree; in-degrees differ here
   return S3BFS_OK;
 }
 
@@ -151,13 +235,16 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
   cudaGraph_t g = nullptr;
   CK(h, cudaGraphCreate(&g, 0));
   h->graph = g;
-  cudaGraphConditionalHandle hw, h0, h1;
+  cudaGraphConditionalHandle hw, h0, h1, h2;
   CK(h, cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault));
   CK(h, cudaGraphConditionalHandleCreate(&h0, g, 0, cudaGraphCondAssignDefault));
   CK(h, cudaGraphConditionalHandleCreate(&h1, g, 0, cudaGraphCondAssignDefault));
+  h2 = 0;
+  if (h->P.direction) CK(h, cudaGraphConditionalHandleCreate(&h2, g, 0, cudaGraphCondAssignDefault));
   h->P.h_while = hw;
   h->P.h_t0 = h0;
   h->P.h_t1 = h1;
+  h->P.h_t2 = h2;
   h->P.use_graph = 1;
 
   cudaGraphNodeParams wp = {};
@@ -215,6 +302,23 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
   CK(h, cudaGraphAddKernelNode(&kx, b1, nullptr, 0, &kkx));
   cudaKernelNodeParams kkc = kparams((void *)k_compact, h->P.p_max, KD_THREADS, 0);
   CK(h, cudaGraphAddKernelNode(&kc, b1, &kx, 1, &kkc));
+
+  if (h->P.direction) {  // NEXT-3: IF(bottom-up) { k_fb_clear; k_fb_set; k_bottom_up }
+    cudaGraphNodeParams ip2 = {};
+    ip2.type = cudaGraphNodeTypeConditional;
+    ip2.conditional.handle = h2;
+    ip2.conditional.type = cudaGraphCondTypeIf;
+    ip2.conditional.size = 1;
+    cudaGraphNode_t n2, fc, fs, bu;
+    CK(h, cudaGraphAddNode(&n2, body, &n1, 1, &ip2));
+    cudaGraph_t b2 = ip2.conditional.phGraph_out[0];
+    cudaKernelNodeParams kfc = kparams((void *)k_fb_clear, h->num_sms * 4, 256, 0);
+    CK(h, cudaGraphAddKernelNode(&fc, b2, nullptr, 0, &kfc));
+    cudaKernelNodeParams kfs = kparams((void *)k_fb_set, h->num_sms * 4, 256, 0);
+    CK(h, cudaGraphAddKernelNode(&fs, b2, &fc, 1, &kfs));
+    cudaKernelNodeParams kbu = kparams((void *)k_bottom_up, h->P.p_max, KD_THREADS, 0);
+    CK(h, cudaGraphAddKernelNode(&bu, b2, &fs, 1, &kbu));
+  }
 
   CK(h, cudaGraphInstantiate(&h->exec, g, 0));
   return S3BFS_OK;
@@ -312,6 +416,7 @@ s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32
   const size_t bm_bytes = ((size_t)n + 127) / 128 * 16;  // 16 B padded (vector clears)
   const size_t o_bm = take(bm_bytes);
   const size_t o_claim = take(((size_t)n + 15) / 16 * 16);
+  const size_t o_fb0 = take(bm_bytes), o_fb1 = take(bm_bytes);
   const size_t o_wcnt = take((size_t)p_max * KD_WARPS * 4);
   const size_t o_status = take((size_t)p_max * 8);
   const size_t o_ctl = take(sizeof(Ctl));
@@ -334,6 +439,8 @@ s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32
   P.cand_rd = (int2 *)(base + o_crd);
   P.bm = (uint32_t *)(base + o_bm);
   P.claim = (uint8_t *)(base + o_claim);
+  P.fb[0] = (uint32_t *)(base + o_fb0);
+  P.fb[1] = (uint32_t *)(base + o_fb1);
   P.wcnt = (int32_t *)(base + o_wcnt);
   P.status = (unsigned long long *)(base + o_status);
   P.stats = (s3bfs_level_stat *)(base + o_stats);
@@ -346,6 +453,11 @@ s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32
   P.use_graph = 0;
   P.n2o = nullptr;
   P.o2n = nullptr;
+  P.direction = h->opt.direction == 1 ? 1 : 0;
+  P.do_alpha = h->opt.do_alpha > 0 ? h->opt.do_alpha : 14;
+  P.do_beta = h->opt.do_beta != 0 ? h->opt.do_beta : 24;
+  P.n_scan = n;
+  P.nnz = nnz;
   if (h->opt.validate_csr) {
     int *d_err = nullptr;
     int h_err = 0;
@@ -370,6 +482,11 @@ s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32
   } else {
     k_build_vinfo<<<h->num_sms * 8, 256, 0, stream>>>(row_offsets, nullptr, n, P.vinfo);
     if ((e = cudaGetLastError()) != cudaSuccess) return bail(cuda_fail(h, e, "k_build_vinfo"));
+    h->ro_int = row_offsets;
+  }
+  if (P.direction) {
+    s3bfs_status ts = build_in_adjacency(h, stream);
+    if (ts != S3BFS_OK) return bail(ts);
   }
   if ((e = cudaMemsetAsync(P.ctl, 0, sizeof(Ctl), stream)) != cudaSuccess) return bail(cuda_fail(h, e, "memset(ctl)"));
   if ((e = cudaMemsetAsync(P.status, 0, (size_t)p_max * 8, stream)) != cudaSuccess) return bail(cuda_fail(h, e, "memset(status)"));
@@ -428,6 +545,10 @@ s3bfs_status s3bfs_run(s3bfs_handle h, int32_t source, int32_t *level, int32_t *
         CK(h, cudaEventElapsedTime(&a, h->ev[0], h->ev[1]));
         h->kt.small_ms += a;
         h->kt.small_launches++;
+      } else if (pending == TIER_BU) {
+        CK(h, cudaEventElapsedTime(&a, h->ev[0], h->ev[1]));
+        h->kt.bottom_up_ms += a;
+        h->kt.bottom_up_launches++;
       } else {
         CK(h, cudaEventElapsedTime(&a, h->ev[0], h->ev[1]));
         CK(h, cudaEventElapsedTime(&b, h->ev[1], h->ev[2]));
@@ -447,6 +568,11 @@ s3bfs_status s3bfs_run(s3bfs_handle h, int32_t source, int32_t *level, int32_t *
     if (h->time_kernels) CK(h, cudaEventRecord(h->ev[0], stream));
     if (c.tier == TIER_SMALL) {
       k_small<<<1, KS_THREADS, h->ks_smem, stream>>>(h->P);
+      if (h->time_kernels) CK(h, cudaEventRecord(h->ev[1], stream));
+    } else if (c.tier == TIER_BU) {
+      k_fb_clear<<<h->num_sms * 4, 256, 0, stream>>>(h->P);
+      k_fb_set<<<h->num_sms * 4, 256, 0, stream>>>(h->P);
+      k_bottom_up<<<h->P.p_max, KD_THREADS, 0, stream>>>(h->P);
       if (h->time_kernels) CK(h, cudaEventRecord(h->ev[1], stream));
     } else {
       k_explore<<<c.p_l, KD_THREADS, 0, stream>>>(h->P);
@@ -468,6 +594,7 @@ s3bfs_status s3bfs_destroy(s3bfs_handle h) {
   if (h->graph) cudaGraphDestroy(h->graph);
   if (h->ws) cudaFree(h->ws);
   if (h->graph2) cudaFree(h->graph2);
+  if (h->graph3) cudaFree(h->graph3);
   if (h->h_ctl) cudaFreeHost(h->h_ctl);
   for (auto &ev : h->ev)
     if (ev) cudaEventDestroy(ev);
@@ -507,7 +634,7 @@ s3bfs_status s3bfs_get_info(s3bfs_handle h, s3bfs_info *out) {
   out->kd_tile_edges = KX_GROUPS * 32;
   out->ksmall_threads = KS_THREADS;
   out->ksmall_max_frontier = KS_NCAP;
-  out->workspace_bytes = (int64_t)(h->ws_bytes + h->graph2_bytes);
+  out->workspace_bytes = (int64_t)(h->ws_bytes + h->graph2_bytes + h->graph3_bytes);
   return S3BFS_OK;
 }
 

@@ -69,7 +69,9 @@ constexpr int SCAN_THREADS = 512;
 constexpr int SCAN_ITEMS = 8;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 
-constexpr int TIER_SMALL = 0, TIER_LARGE = 1, TIER_DONE = 2;
+constexpr int TIER_SMALL = 0, TIER_LARGE = 1, TIER_DONE = 2, TIER_BU = 3;
+constexpr int BU_W = 4;   // bottom-up: bitmap words per warp round
+constexpr int BU_P = 2;   // bottom-up: in-neighbours probed per vertex per round
 
 // Device control block: the paper's loop state (Fig1 L8-L11, L15-L16) kept on the device so
 // the level loop needs no host round trip.
@@ -87,7 +89,9 @@ struct Ctl {
   int32_t num_levels;       // stats records written
   int32_t cand_acc;         // stats: candidates of the level (incl. duplicates)
   int32_t source;
-  int32_t pad0, pad1;
+  int32_t bu;               // NEXT-3: the current level runs bottom-up
+  int32_t fb_valid;         // fb[cur] already holds the current frontier (a bottom-up product)
+  long long m_visited;      // sum of the degrees of all visited vertices (Beamer's m_u = m - it)
   int32_t *level_out, *parent_out;
   unsigned long long t_prev;
   unsigned long long t_kx_begin, t_kx_end;  // k_explore CTA 0 start, k_compact CTA 0 start
@@ -108,13 +112,18 @@ struct Params {
   int2 *cand_rd;                // (row start, degree) of kept candidates, pass 1 -> pass 2
   uint32_t *bm;                 // visited bitmap: bit set => visited (exact at level start)
   uint8_t *claim;               // per-vertex tag of the level that discovered it (k_explore)
+  uint32_t *fb[2];              // NEXT-3: frontier bitmaps (bottom-up levels only)
+  const int32_t *tro, *tcol;    // NEXT-3: in-adjacency (internal ids) the bottom-up step scans
   int32_t *wcnt;
   unsigned long long *status;
   s3bfs_level_stat *stats;
   int32_t stats_cap;
   int32_t p_max, grain, t0, variant, collect_stats;
+  int32_t direction, do_alpha, do_beta;  // NEXT-3 switch rule (Beamer): alpha, beta
+  int32_t n_scan;               // bottom-up scans internal ids [0, n_scan): the ones with deg > 0
+  long long nnz;
   int32_t use_graph;
-  unsigned long long h_while, h_t0, h_t1;  // cudaGraphConditionalHandle values
+  unsigned long long h_while, h_t0, h_t1, h_t2;  // cudaGraphConditionalHandle values
 };
 
 // ---- PTX helpers ------------------------------------------------------------------------
@@ -316,6 +325,19 @@ __device__ void decide(const Params &P, Ctl *c, int32_t n_l, int32_t e_l) {
     c->p_l = 0;
     return;
   }
+  if (P.direction) {  // NEXT-3: Beamer's direction-optimising switch
+    const long long m_u = P.nnz - c->m_visited;  // arcs of still-unvisited vertices
+    if (!c->bu) {
+      if ((long long)e_l * P.do_alpha > m_u) c->bu = 1;
+    } else if (P.do_beta > 0 && (long long)n_l * P.do_beta < (long long)P.n) {
+      c->bu = 0;
+    }
+    if (c->bu) {
+      c->tier = TIER_BU;
+      c->p_l = P.p_max;
+      return;
+    }
+  }
   if (P.variant == 0 && P.t0 >= 0 && e_l <= P.t0 && n_l <= KS_NCAP) {
     c->tier = TIER_SMALL;
     c->p_l = 1;
@@ -367,6 +389,9 @@ __global__ void k_init(Params P, int32_t s, int32_t *level, int32_t *parent) {
     c->done_ctr = 0;
     c->cand_acc = 0;
     c->t_prev = globaltimer();
+    c->bu = 0;
+    c->fb_valid = 0;
+    c->m_visited = vs.y;
     decide(P, c, 1, vs.y);
   }
 }
@@ -376,6 +401,8 @@ __global__ void k_dispatch(Params P) {
   const int t = P.ctl->tier;
   cudaGraphSetConditional((cudaGraphConditionalHandle)P.h_t0, t == TIER_SMALL ? 1u : 0u);
   cudaGraphSetConditional((cudaGraphConditionalHandle)P.h_t1, t == TIER_LARGE ? 1u : 0u);
+  if (P.direction)
+    cudaGraphSetConditional((cudaGraphConditionalHandle)P.h_t2, t == TIER_BU ? 1u : 0u);
   if (t == TIER_DONE) cudaGraphSetConditional((cudaGraphConditionalHandle)P.h_while, 0u);
 }
 
@@ -634,6 +661,8 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
     c->t_prev = t;
     c->level = c->level + 1;  // Fig1 L10
     c->cur = nxt;
+    c->m_visited += e_next;
+    c->fb_valid = 0;
     decide(P, c, n_next, e_next);
   }
 }
@@ -646,7 +675,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
 // the Owner check (R4), without the Owner round trip.  Returns when the next level is not
 // tiny (or empty), leaving that frontier in shared memory and its (n, e, level) in st[].
 __device__ void tiny_levels(const Params &P, Ctl *c, int32_t *sf, int32_t *srs, int32_t *sex,
-                            int32_t *st, unsigned long long &t_prev) {
+                            int32_t *st, unsigned long long &t_prev, long long &m_add) {
   const int lane = threadIdx.x & 31;
   const int32_t *__restrict__ col = P.col;
   int n_l = st[0], e_l = st[1], L = st[2];
@@ -688,6 +717,7 @@ __device__ void tiny_levels(const Params &P, Ctl *c, int32_t *sf, int32_t *srs, 
       const unsigned long long t = globaltimer();
       record_stat(P, c, L, n_l, e_l, TIER_SMALL, 1, ncand, n_next, t_prev, t);
       t_prev = t;
+      m_add += e_next;
     }
     fx = lane < n_next ? nfx : 0;
     frs = lane < n_next ? nfr : 0;
@@ -739,6 +769,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
   int n_l = c->n_l, e_l = c->e_l, L = c->level;
   const int cur = c->cur;
   unsigned long long t_prev = c->t_prev;
+  long long m_add = 0;  // degrees of the frontiers created here (thread 0)
   for (int i = tid; i < n_l; i += KS_THREADS) {
     sf[i] = P.f[cur][i];
     srs[i] = P.frs[cur][i];
@@ -751,7 +782,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
     if (n_l <= 32 && e_l <= 32) {  // tiny levels: warp 0 alone, no CTA barrier per level
       if (tid == 0) { s_tiny[0] = n_l; s_tiny[1] = e_l; s_tiny[2] = L; }
       __syncwarp();
-      if (warp == 0) tiny_levels(P, c, sf, srs, sex, s_tiny, t_prev);
+      if (warp == 0) tiny_levels(P, c, sf, srs, sex, s_tiny, t_prev, m_add);
       __syncthreads();
       n_l = s_tiny[0];
       e_l = s_tiny[1];
@@ -902,6 +933,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
       const unsigned long long t = globaltimer();
       record_stat(P, c, L, n_l, e_l, TIER_SMALL, 1, s_tot[2], n_next, t_prev, t);
       t_prev = t;
+      m_add += e_next;
     }
     __syncthreads();
     ++L;
@@ -921,7 +953,179 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
   if (tid == 0) {
     c->level = L;
     c->t_prev = t_prev;
+    c->m_visited += m_add;
+    c->fb_valid = 0;
+    c->bu = 0;
     decide(P, c, n_l, e_l);
+  }
+}
+
+// ---- NEXT-3: direction-optimising bottom-up level (P:131 names it as compatible) --------------
+// Beamer's bottom-up step over the same state: every vertex not yet visited looks for a
+// neighbour in the current frontier (a bitmap), stopping at the first one.  The frontier
+// bitmap is built from the frontier list when the previous level was top-down.
+__global__ void k_fb_clear(Params P) {
+  Ctl *c = P.ctl;
+  if (c->tier != TIER_BU) return;
+  const long long gs = (long long)gridDim.x * blockDim.x;
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (long long i = g; i < P.p_max; i += gs) P.status[i] = 0ull;  // k_bottom_up's look-back
+  if (c->fb_valid) return;
+  const long long nw4 = ((long long)P.n + 127) >> 7;
+  uint4 *fb = reinterpret_cast<uint4 *>(P.fb[c->cur]);
+  for (long long i = g; i < nw4; i += gs) fb[i] = make_uint4(0, 0, 0, 0);
+}
+__global__ void k_fb_set(Params P) {
+  Ctl *c = P.ctl;
+  if (c->tier != TIER_BU || c->fb_valid) return;
+  const int n_l = c->n_l;
+  const int32_t *f = P.f[c->cur];
+  uint32_t *fb = P.fb[c->cur];
+  for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < n_l;
+       u += (long long)gridDim.x * blockDim.x) {
+    const int o = f[u];
+    const int i = P.o2n ? __ldg(P.o2n + o) : o;
+    atomicOr(fb + (i >> 5), 1u << (i & 31));  // frontier membership (not the discovery path)
+  }
+}
+// One warp per visited-bitmap word (32 consecutive internal ids); the warp owns the word, so
+// the visited word and the next frontier's bitmap word are written with plain stores and no
+// vertex can be found twice (no Owner dedup needed).  CTA b takes a contiguous range of
+// words; found vertices are compacted into the next frontier list with the same decoupled
+// look-back (kept, degree-sum) scan as k_compact.
+__global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params P) {
+  Ctl *c = P.ctl;
+  if (c->tier != TIER_BU) return;
+  __shared__ int32_t s_k[KD_WARPS], s_d[KD_WARPS];
+  __shared__ int s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = blockIdx.x, nb = gridDim.x;
+  const int cur = c->cur, nxt = cur ^ 1;
+  const int new_level = c->level + 1;
+  const int4 *__restrict__ vinfo = P.vinfo;
+  const uint32_t *__restrict__ fbc = P.fb[cur];
+  uint32_t *__restrict__ fbn = P.fb[nxt];
+  uint32_t *__restrict__ bm = P.bm;
+  const int nwords = (int)((((long long)P.n + 127) >> 7) << 2);
+  const int nscan = P.n_scan;
+  const int wpc = (nwords + nb - 1) / nb;
+  const int w0 = min(b * wpc, nwords), w1 = min(w0 + wpc, nwords);
+  if (b == 0 && tid == 0) c->t_kx_begin = globaltimer();
+  // pass 1: BU_W words per warp round (BU_W independent probe chains per lane); every round
+  // probes the next BU_P in-neighbours of each unresolved vertex, loads issued together
+  int kept = 0, dsum = 0;
+  for (int wb = w0 + warp * BU_W; wb < w1; wb += KD_WARPS * BU_W) {
+    uint32_t bw[BU_W];
+    int r0[BU_W], r1[BU_W], dg[BU_W], pu[BU_W];
+#pragma unroll
+    for (int i = 0; i < BU_W; ++i) {
+      const int w = wb + i;
+      const int v = (w << 5) + lane;
+      bw[i] = (w < w1) ? bm[w] : 0xffffffffu;
+      const bool act = w < w1 && v < nscan && !((bw[i] >> lane) & 1u);
+      r0[i] = act ? __ldg(P.tro + v) : 0;
+      r1[i] = act ? __ldg(P.tro + v + 1) : 0;
+      dg[i] = act ? __ldg(vinfo + v).y : 0;  // out-degree: the next level's e_l (Fig1 L13)
+      pu[i] = -1;
+    }
+    for (;;) {  // rounds until every vertex found a frontier in-neighbour or ran out of them
+      bool more = false;
+#pragma unroll
+      for (int i = 0; i < BU_W; ++i) more |= r0[i] < r1[i];
+      if (!__any_sync(0xffffffffu, more)) break;
+      int u[BU_W][BU_P];
+#pragma unroll
+      for (int i = 0; i < BU_W; ++i)
+#pragma unroll
+        for (int j = 0; j < BU_P; ++j)
+          u[i][j] = (r0[i] + j < r1[i]) ? __ldg(P.tcol + r0[i] + j) : -1;
+      uint32_t fw[BU_W][BU_P];
+#pragma unroll
+      for (int i = 0; i < BU_W; ++i)
+#pragma unroll
+        for (int j = 0; j < BU_P; ++j)
+          fw[i][j] = (u[i][j] >= 0) ? __ldg(fbc + (u[i][j] >> 5)) : 0u;
+#pragma unroll
+      for (int i = 0; i < BU_W; ++i) {
+#pragma unroll
+        for (int j = BU_P - 1; j >= 0; --j)  // the first hit in row order wins
+          if (u[i][j] >= 0 && ((fw[i][j] >> (u[i][j] & 31)) & 1u)) pu[i] = u[i][j];
+        r0[i] = (pu[i] >= 0) ? r1[i] : r0[i] + BU_P;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < BU_W; ++i) {
+      const int w = wb + i;
+      const int v = (w << 5) + lane;
+      const bool found = pu[i] >= 0;
+      if (found) P.lp[v] = make_int2(new_level, __ldg(vinfo + pu[i]).z);  // d, parent (caller)
+      const unsigned m = __ballot_sync(0xffffffffu, found);
+      if (lane == 0 && w < w1) {
+        if (m) bm[w] = bw[i] | m;  // this warp owns word w
+        fbn[w] = m;
+      }
+      kept += __popc(m);
+      dsum += found ? dg[i] : 0;
+    }
+  }
+  dsum = warp_sum(dsum);
+  if (lane == 0) { s_k[warp] = kept; s_d[warp] = dsum; }
+  __syncthreads();
+  if (warp == 0) {
+    const int kk = lane < KD_WARPS ? s_k[lane] : 0;
+    const int dd = lane < KD_WARPS ? s_d[lane] : 0;
+    const int ik = warp_incl_scan(kk), id = warp_incl_scan(dd);
+    const Pair agg{(uint32_t)__shfl_sync(0xffffffffu, ik, 31),
+                   (uint32_t)__shfl_sync(0xffffffffu, id, 31)};
+    const Pair ex = lookback<true>(P.status, b, agg);
+    if (lane < KD_WARPS) {
+      s_k[lane] = (int)ex.a + ik - kk;
+      s_d[lane] = (int)ex.b + id - dd;
+    }
+    if (b == nb - 1 && lane == 0) {
+      const int n_next = (int)(ex.a + agg.a), e_next = (int)(ex.b + agg.b);
+      c->n_next = n_next;
+      c->e_next = e_next;
+      P.fex[nxt][n_next] = e_next;
+    }
+  }
+  __syncthreads();
+  // pass 2: the warp's found vertices (its own fbn words) into the next frontier list
+  int koff = s_k[warp], doff = s_d[warp];
+  for (int wb = w0 + warp * BU_W; wb < w1; wb += KD_WARPS * BU_W)
+  for (int w = wb; w < min(wb + BU_W, w1); ++w) {
+    const uint32_t m = fbn[w];
+    if (!m) continue;
+    const bool mine = (m >> lane) & 1u;
+    const int4 vi = mine ? __ldg(vinfo + (w << 5) + lane) : make_int4(0, 0, 0, 0);
+    const int d = mine ? vi.y : 0;
+    const int inc = warp_incl_scan(d);
+    const int pos = koff + __popc(m & lanemask_lt());
+    if (mine) {
+      P.f[nxt][pos] = vi.z;
+      P.frs[nxt][pos] = vi.x;
+      P.fex[nxt][pos] = doff + inc - d;
+    }
+    koff += __popc(m);
+    doff += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(&c->done_ctr, 1u) == (unsigned)(nb - 1);
+  __syncthreads();
+  if (s_last && tid == 0) {
+    __threadfence();
+    const int n_next = ld_volatile(&c->n_next), e_next = ld_volatile(&c->e_next);
+    const unsigned long long t = globaltimer();
+    record_stat(P, c, c->level, c->n_l, c->e_l, TIER_BU, nb, n_next, n_next, c->t_prev, t,
+                *(volatile unsigned long long *)&c->t_kx_begin, t);
+    c->done_ctr = 0;
+    c->t_prev = t;
+    c->level = c->level + 1;
+    c->cur = nxt;
+    c->m_visited += e_next;
+    c->fb_valid = 1;
+    decide(P, c, n_next, e_next);
   }
 }
 
@@ -976,6 +1180,56 @@ __global__ void k_relabel_rows(const int32_t *ro, const int32_t *col, const int3
     const int s = ro[o], len = ro[o + 1] - s, d = ro2[i];
     for (int j = lane; j < len; j += 32) col2[d + j] = o2n[col[s + j]];
   }
+}
+// symmetry test of the arc multiset (create time, NEXT-3): sums of a 64-bit hash of (u, v)
+// and of (v, u) over all arcs -- equal iff the multiset is symmetric (with prob. 1 - 2^-64)
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__global__ void k_sym_hash(const int32_t *ro, const int32_t *col, int n,
+                           unsigned long long *out) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long a = 0, b = 0;
+  for (long long u = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n;
+       u += ((long long)gridDim.x * blockDim.x) >> 5) {
+    for (int k = ro[u] + lane; k < ro[u + 1]; k += 32) {
+      const unsigned long long v = (unsigned)col[k];
+      a += mix64(((unsigned long long)u << 32) | v);
+      b += mix64((v << 32) | (unsigned long long)u);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if (lane == 0) { atomicAdd(out, a); atomicAdd(out + 1, b); }
+}
+// transpose (in-adjacency): in-degree count, then scatter (create time, order irrelevant)
+__global__ void k_in_degree(const int32_t *ro, const int32_t *col, int n, int32_t *tdeg) {
+  const int lane = threadIdx.x & 31;
+  for (long long u = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n;
+       u += ((long long)gridDim.x * blockDim.x) >> 5)
+    for (int k = ro[u] + lane; k < ro[u + 1]; k += 32) atomicAdd(tdeg + col[k], 1);
+}
+__global__ void k_transpose(const int32_t *ro, const int32_t *col, int n, int32_t *cursor,
+                            int32_t *tcol) {
+  const int lane = threadIdx.x & 31;
+  for (long long u = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n;
+       u += ((long long)gridDim.x * blockDim.x) >> 5)
+    for (int k = ro[u] + lane; k < ro[u + 1]; k += 32) tcol[atomicAdd(cursor + col[k], 1)] = (int)u;
+}
+// number of vertices with degree > 0 (create time; with the degree order they are a prefix)
+__global__ void k_count_nonzero(const int32_t *deg, int n, int *out) {
+  int c = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    c += deg[i] > 0;
+  c = warp_sum(c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
 // vinfo[i] = {row start, degree, caller id, Owner = 0} over a CSR's row offsets
 __global__ void k_build_vinfo(const int32_t *ro, const int32_t *n2o, int n, int4 *vinfo) {

@@ -40,7 +40,8 @@ class Options(ctypes.Structure):
                 ("validate_csr", ctypes.c_int32), ("variant", ctypes.c_int32),
                 ("max_ctas", ctypes.c_int32), ("debug_poison", ctypes.c_int32),
                 ("time_kernels", ctypes.c_int32), ("reorder", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 6)]
+                ("direction", ctypes.c_int32), ("do_alpha", ctypes.c_int32),
+                ("do_beta", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
 
 
 class LevelStat(ctypes.Structure):
@@ -54,9 +55,9 @@ class LevelStat(ctypes.Structure):
 
 class KernelTimes(ctypes.Structure):
     _fields_ = [("explore_ms", ctypes.c_double), ("compact_ms", ctypes.c_double),
-                ("small_ms", ctypes.c_double), ("explore_launches", ctypes.c_int32),
-                ("compact_launches", ctypes.c_int32), ("small_launches", ctypes.c_int32),
-                ("pad", ctypes.c_int32)]
+                ("small_ms", ctypes.c_double), ("bottom_up_ms", ctypes.c_double),
+                ("explore_launches", ctypes.c_int32), ("compact_launches", ctypes.c_int32),
+                ("small_launches", ctypes.c_int32), ("bottom_up_launches", ctypes.c_int32)]
 
 
 class Info(ctypes.Structure):
@@ -194,7 +195,7 @@ def s3bfs_get_kernel_times(handle) -> dict:
     kt = KernelTimes()
     _check(load().s3bfs_get_kernel_times(handle, ctypes.byref(kt)), "s3bfs_get_kernel_times",
            handle)
-    return {f: getattr(kt, f) for f, _ in KernelTimes._fields_ if f != "pad"}
+    return {f: getattr(kt, f) for f, _ in KernelTimes._fields_}
 
 
 def s3bfs_debug_exclusive_scan(inp, out, stream=None) -> None:

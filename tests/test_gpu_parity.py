@@ -27,6 +27,12 @@ SETTINGS = [
     ("work-insensitive", dict(debug_poison=1, variant=1)),
     ("grain-4096-T0-1", dict(debug_poison=1, tier0_max_edges=1, edges_per_cta=4096)),
     ("no-reorder", dict(debug_poison=1, reorder=-1, tier0_max_edges=64)),
+    # NEXT-3 direction optimisation: bottom-up on every level / switching back and forth
+    ("bu-always", dict(debug_poison=1, tier0_max_edges=-1, direction=1, do_alpha=1 << 30,
+                       do_beta=-1)),
+    ("bu-mixed", dict(debug_poison=1, tier0_max_edges=16, direction=1, do_alpha=64, do_beta=3)),
+    ("bu-no-reorder", dict(debug_poison=1, reorder=-1, tier0_max_edges=-1, direction=1,
+                           do_alpha=1 << 30, do_beta=-1)),
 ]
 
 
@@ -115,7 +121,7 @@ def test_random_multigraphs(seed):
     g = graphgen.from_edges(n, np.stack([src, dst], 1), symmetrize=bool(seed % 2),
                             name=f"rand{seed}")
     ro, col = to_dev(g)
-    for _, kw in SETTINGS[:5] + SETTINGS[-2:]:
+    for _, kw in SETTINGS[:5] + SETTINGS[-5:]:
         bfs = pkg.S3BFS(ro, col, pkg.Options(**kw))
         for s in rng.choice(n, 3, replace=False):
             check_traversal(g, bfs, int(s))
@@ -252,6 +258,11 @@ def test_configs_levels_bit_exact(cfg, max_sources):
     g = graphgen.make_config(cfg)
     ro, col = to_dev(g)
     bfs = pkg.S3BFS(ro, col)            # default options = the bench configuration
+    for s in g.sources[:max_sources]:
+        check_traversal(g, bfs, s)
+    bfs.close()
+    # NEXT-3: direction-optimising traversal, default switch rule (alpha 14, beta 24)
+    bfs = pkg.S3BFS(ro, col, pkg.Options(direction=1))
     for s in g.sources[:max_sources]:
         check_traversal(g, bfs, s)
     bfs.close()
