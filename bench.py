@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--loop-mode", type=int, default=0)
     ap.add_argument("--tier0", type=int, default=0)
     ap.add_argument("--grain", type=int, default=0)
+    ap.add_argument("--no-next3", action="store_true",
+                    help="skip the extra direction-optimising (NEXT-3) measurement")
     ap.add_argument("--direction", type=int, default=0,
                     help="1: direction-optimising traversal (NEXT-3); default: the paper's top-down")
     return ap.parse_args()
@@ -236,6 +238,7 @@ def main():
                   "stats": st}
     verified = {"sources": 0, "levels_bit_exact": True, "parents_valid": True}
     cpu_times, cpu_edges = [], []
+    oracle_levels = {}
     if rank == 0 and args.oracle_sources > 0:
         import oracle
         for s in srcs[: args.oracle_sources]:
@@ -245,6 +248,7 @@ def main():
             t0 = time.perf_counter()
             ref, _ = oracle.bfs(g.row_offsets, g.col_indices, s)
             cpu_times.append(time.perf_counter() - t0)
+            oracle_levels[s] = ref
             _, _, m_c, _ = oracle.level_profile(g.row_offsets, ref)
             cpu_edges.append(m_c // 2)
             ok = bool(np.array_equal(lv, ref))
@@ -310,6 +314,37 @@ def main():
         e2e_ms += a.elapsed_time(b)
         e2e_edges += per[s]["m_c"] // 2
     e2e_value, _, _ = job_throughput(e2e_ms, e2e_edges, dev, world)
+
+    # ---- NEXT-3: the same steps with the direction-optimising option (not the headline) ----
+    next3 = None
+    if not args.direction and not args.no_next3:
+        hd = pkg.S3BFS(ro, col, pkg.Options(direction=1, loop_mode=args.loop_mode))
+        d_ok = True
+        for s, ref in oracle_levels.items():  # bit-exact against the oracle too
+            pkg.s3bfs_run_ptr(hd.handle, s, lp, pp, sp)
+            torch.cuda.synchronize()
+            d_ok &= bool(np.array_equal(level.cpu().numpy(), ref))
+        for k in range(args.warmup):
+            pkg.s3bfs_run_ptr(hd.handle, my_srcs[k % len(my_srcs)], lp, pp, sp)
+        torch.cuda.synchronize()
+        d_ms, d_edges = 0.0, 0
+        for k in range(args.steps):
+            s = my_srcs[k % len(my_srcs)]
+            if not args.no_flush:
+                flush_buf.fill_(k & 255)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            pkg.s3bfs_run_ptr(hd.handle, s, lp, pp, sp)
+            b.record(stream)
+            b.synchronize()
+            d_ms += a.elapsed_time(b)
+            d_edges += per[s]["m_c"] // 2
+        d_value, d_max_ms, _ = job_throughput(d_ms, d_edges, dev, world)
+        hd.close()
+        next3 = {"what": "direction-optimising traversal (SURVEY NEXT-3, option direction=1; "
+                         "Beamer switch alpha=14 beta=24), same sources/steps/flushes",
+                 "value": d_value, "unit": "GTEPS", "ms_per_step": d_max_ms / args.steps,
+                 "levels_bit_exact_vs_oracle": d_ok, "sources_checked": len(oracle_levels)}
 
     # ---- roofline of k_explore: per-launch CUDA events (host-loop pass, same kernels) -----
     roof = None
@@ -392,6 +427,7 @@ def main():
                     "what": "s3bfs_run through the C ABI (source by value) + level/parent "
                             "copied to pinned host memory, CUDA events around both"},
             "clocks": clk.summary(), "gpu_launches": my_launches, "verified": verified,
+            "next3_direction_optimising": next3,
         }
         print(json.dumps(line), flush=True)
         if args.detail_out:
