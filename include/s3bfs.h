@@ -109,6 +109,12 @@ s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32
                           const int32_t *col_indices, const s3bfs_options *opts,
                           s3bfs_stream_t stream);
 
+/* NEXT-2 (multi-source throughput): a new handle over src's prepared graph (the internal
+ * degree-ordered copy and in-adjacency are shared, reference-counted; the workspace is the
+ * clone's own), so K handles can run K traversals concurrently on K streams.  Same options
+ * as src.  src may be destroyed before its clones.  May synchronise `stream`. */
+s3bfs_status s3bfs_clone(s3bfs_handle src, s3bfs_handle *out, s3bfs_stream_t stream);
+
 /* Parallel-BFS(s, P): enqueue one traversal from `source` on `stream`.
  * level, parent: device, n int32 each, caller-owned, FULLY overwritten.
  * Errors: INVALID_ARGUMENT for source outside [0, n) or null/non-device outputs. */

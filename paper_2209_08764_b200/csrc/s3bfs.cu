@@ -13,6 +13,7 @@
 // P_l and every per-level decision stay on the device (SURVEY.md s.8(a) row f, H6).
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -25,6 +26,18 @@
 
 using namespace s3bfs;
 
+// Device memory of the prepared graph (degree-ordered CSR, id maps, in-adjacency), shared by a
+// handle and its clones (NEXT-2: concurrent traversals); freed with the last of them.
+struct GraphStore {
+  void *g2 = nullptr, *g3 = nullptr;
+  size_t b2 = 0, b3 = 0;
+  std::atomic<int> refs{1};
+  ~GraphStore() {
+    if (g2) cudaFree(g2);
+    if (g3) cudaFree(g3);
+  }
+};
+
 struct s3bfs_ctx {
   int dev = 0, num_sms = 0;
   int32_t n = 0;
@@ -33,10 +46,7 @@ struct s3bfs_ctx {
   s3bfs_options opt{};
   Params P{};
   void *ws = nullptr;
-  void *graph2 = nullptr;  // degree-ordered internal CSR + id maps
-  size_t graph2_bytes = 0;
-  void *graph3 = nullptr;  // transpose of a non-symmetric graph (NEXT-3 only)
-  size_t graph3_bytes = 0;
+  GraphStore *gs = nullptr;         // shared prepared graph (see GraphStore)
   const int32_t *ro_int = nullptr;  // row offsets of the internal CSR
   size_t ws_bytes = 0;
   int64_t cand_cap = 0;
@@ -110,9 +120,9 @@ s3bfs_status build_reordered(s3bfs_ctx *h, cudaStream_t st) {
   const size_t o_col2 = take((size_t)nnz * 4 + 16);
   const size_t o_n2o = take((size_t)n * 4), o_o2n = take((size_t)n * 4);
   const size_t o_ro2 = take((size_t)(n + 1) * 4);
-  h->graph2_bytes = off;
-  CK(h, cudaMalloc(&h->graph2, off));
-  char *g = (char *)h->graph2;
+  h->gs->b2 = off;
+  CK(h, cudaMalloc(&h->gs->g2, off));
+  char *g = (char *)h->gs->g2;
   int32_t *col2 = (int32_t *)(g + o_col2);
   int32_t *n2o = (int32_t *)(g + o_n2o), *o2n = (int32_t *)(g + o_o2n);
   int32_t *deg = nullptr, *deg_sorted = nullptr, *iota = nullptr;
@@ -193,10 +203,10 @@ s3bfs_status build_in_adjacency(s3bfs_ctx *h, cudaStream_t st) {
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return o; };
   const size_t o_tro = take((size_t)(n + 1) * 4), o_tcol = take((size_t)nnz * 4 + 16);
-  CK(h, cudaMalloc(&h->graph3, off));
-  h->graph3_bytes = off;
-  int32_t *tro = (int32_t *)((char *)h->graph3 + o_tro);
-  int32_t *tcol = (int32_t *)((char *)h->graph3 + o_tcol);
+  CK(h, cudaMalloc(&h->gs->g3, off));
+  h->gs->b3 = off;
+  int32_t *tro = (int32_t *)((char *)h->gs->g3 + o_tro);
+  int32_t *tcol = (int32_t *)((char *)h->gs->g3 + o_tcol);
   if (hh[0] == hh[1]) {
     s3bfs_status ss = sort_rows(h, ro, col, tcol, st);
     if (ss != S3BFS_OK) return ss;
@@ -346,9 +356,13 @@ s3bfs_status s3bfs_last_error(s3bfs_handle h, const char **msg) {
   return S3BFS_OK;
 }
 
-s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_t *row_offsets,
-                          const int32_t *col_indices, const s3bfs_options *opts,
-                          s3bfs_stream_t stream_) {
+}  // extern "C"
+
+namespace {
+// create (share == NULL) or clone (share = the handle whose prepared graph is reused)
+s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_t *row_offsets,
+                         const int32_t *col_indices, const s3bfs_options *opts,
+                         s3bfs_stream_t stream_, const s3bfs_ctx *share) {
   if (!out) return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "out is NULL");
   *out = nullptr;
   if (n <= 0) return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "n must be >= 1");
@@ -371,6 +385,13 @@ s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32
   h->ro = row_offsets;
   h->col = col_indices;
   if (opts) h->opt = *opts;
+  if (share) {
+    h->gs = share->gs;
+    h->gs->refs++;
+  } else {
+    h->gs = new (std::nothrow) GraphStore;
+    if (!h->gs) return bail(fail(h, S3BFS_ERR_OUT_OF_MEMORY, "host allocation failed"));
+  }
   cudaError_t e;
   if ((e = cudaGetDevice(&h->dev)) != cudaSuccess) return bail(cuda_fail(h, e, "cudaGetDevice"));
   cudaDeviceProp prop;
@@ -458,7 +479,19 @@ s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32
   P.do_beta = h->opt.do_beta != 0 ? h->opt.do_beta : 24;
   P.n_scan = n;
   P.nnz = nnz;
-  if (h->opt.validate_csr) {
+  if (share) {  // a clone: the prepared graph is the source handle's; vertex records copied
+    P.col = share->P.col;
+    P.n2o = share->P.n2o;
+    P.o2n = share->P.o2n;
+    P.n_scan = share->P.n_scan;
+    P.tro = share->P.tro;
+    P.tcol = share->P.tcol;
+    h->ro_int = share->ro_int;
+    if ((e = cudaMemcpyAsync(P.vinfo, share->P.vinfo, (size_t)n * 16, cudaMemcpyDeviceToDevice,
+                             stream)) != cudaSuccess)
+      return bail(cuda_fail(h, e, "copy vertex records"));
+  }
+  if (!share && h->opt.validate_csr) {
     int *d_err = nullptr;
     int h_err = 0;
     if ((e = cudaMallocAsync((void **)&d_err, 4, stream)) != cudaSuccess) return bail(cuda_fail(h, e, "cudaMallocAsync"));
@@ -476,7 +509,8 @@ s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32
       return bail(fail(h, S3BFS_ERR_INVALID_GRAPH, m));
     }
   }
-  if (h->opt.reorder >= 0) {
+  if (share) {
+  } else if (h->opt.reorder >= 0) {
     s3bfs_status rs = build_reordered(h, stream);
     if (rs != S3BFS_OK) return bail(rs);
   } else {
@@ -484,7 +518,7 @@ s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32
     if ((e = cudaGetLastError()) != cudaSuccess) return bail(cuda_fail(h, e, "k_build_vinfo"));
     h->ro_int = row_offsets;
   }
-  if (P.direction) {
+  if (P.direction && !share) {
     s3bfs_status ts = build_in_adjacency(h, stream);
     if (ts != S3BFS_OK) return bail(ts);
   }
@@ -514,6 +548,20 @@ s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32
   if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) return bail(cuda_fail(h, e, "create sync"));
   *out = h;
   return S3BFS_OK;
+}
+}  // namespace
+
+extern "C" {
+
+s3bfs_status s3bfs_create(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_t *row_offsets,
+                          const int32_t *col_indices, const s3bfs_options *opts,
+                          s3bfs_stream_t stream) {
+  return create_impl(out, n, nnz, row_offsets, col_indices, opts, stream, nullptr);
+}
+
+s3bfs_status s3bfs_clone(s3bfs_handle src, s3bfs_handle *out, s3bfs_stream_t stream) {
+  if (!src) return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "source handle is NULL");
+  return create_impl(out, src->n, src->nnz, src->ro, src->col, &src->opt, stream, src);
 }
 
 s3bfs_status s3bfs_run(s3bfs_handle h, int32_t source, int32_t *level, int32_t *parent,
@@ -593,8 +641,7 @@ s3bfs_status s3bfs_destroy(s3bfs_handle h) {
   if (h->exec) cudaGraphExecDestroy(h->exec);
   if (h->graph) cudaGraphDestroy(h->graph);
   if (h->ws) cudaFree(h->ws);
-  if (h->graph2) cudaFree(h->graph2);
-  if (h->graph3) cudaFree(h->graph3);
+  if (h->gs && --h->gs->refs == 0) delete h->gs;
   if (h->h_ctl) cudaFreeHost(h->h_ctl);
   for (auto &ev : h->ev)
     if (ev) cudaEventDestroy(ev);
@@ -634,7 +681,7 @@ s3bfs_status s3bfs_get_info(s3bfs_handle h, s3bfs_info *out) {
   out->kd_tile_edges = KX_GROUPS * 32;
   out->ksmall_threads = KS_THREADS;
   out->ksmall_max_frontier = KS_NCAP;
-  out->workspace_bytes = (int64_t)(h->ws_bytes + h->graph2_bytes + h->graph3_bytes);
+  out->workspace_bytes = (int64_t)(h->ws_bytes + (h->gs ? h->gs->b2 + h->gs->b3 : 0));
   return S3BFS_OK;
 }
 

@@ -86,6 +86,8 @@ struct Ctl {
   int32_t wcap;       // edges (= candidate capacity) per warp
   int32_t n_next, e_next;   // written by the last k_compact CTA in tile order
   uint32_t done_ctr;        // last-CTA election in k_compact (not the discovery path)
+  uint32_t tile_ctr;        // look-back tile ids in start order (forward progress under any
+                            // CTA dispatch order, e.g. concurrent traversals; not discovery)
   int32_t num_levels;       // stats records written
   int32_t cand_acc;         // stats: candidates of the level (incl. duplicates)
   int32_t source;
@@ -387,6 +389,7 @@ __global__ void k_init(Params P, int32_t s, int32_t *level, int32_t *parent) {
     c->parent_out = parent;
     c->num_levels = 0;
     c->done_ctr = 0;
+    c->tile_ctr = 0;
     c->cand_acc = 0;
     c->t_prev = globaltimer();
     c->bu = 0;
@@ -555,13 +558,18 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
 __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P) {
   Ctl *c = P.ctl;
   if (c->tier != TIER_LARGE) return;
-  const int b = blockIdx.x;
   const int p_l = c->p_l;
-  if (b >= p_l) return;
   __shared__ int32_t s_k[KD_WARPS], s_d[KD_WARPS];
-  __shared__ int s_last;
+  __shared__ int s_last, s_tile;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // Surplus CTAs (blockIdx >= P_l) do no work but are still counted by the last-CTA
+  // election below: the control block is rewritten only after EVERY CTA of this launch has
+  // read it (a late-starting surplus CTA would otherwise see the next level's state).
   const int nxt = c->cur ^ 1;
+  if ((int)blockIdx.x < p_l) {
+  if (tid == 0) s_tile = (int)atomicAdd(&c->tile_ctr, 1u);  // look-back order = start order
+  __syncthreads();
+  const int b = s_tile;  // this CTA handles tile b: the segments of k_explore's CTA b
   const int4 *__restrict__ vinfo = P.vinfo;
   int32_t *__restrict__ cand = P.cand;
   int2 *__restrict__ crd = P.cand_rd;
@@ -644,10 +652,11 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
     }
     doff += __shfl_sync(0xffffffffu, inc, 31);
   }
-  // last-CTA election (one atomic per CTA; not on the discovery path, R17)
+  }  // active CTA
+  // last-CTA election over the whole grid (one atomic per CTA; not the discovery path, R17)
   __threadfence();
   __syncthreads();
-  if (tid == 0) s_last = atomicAdd(&c->done_ctr, 1u) == (unsigned)(p_l - 1);
+  if (tid == 0) s_last = atomicAdd(&c->done_ctr, 1u) == gridDim.x - 1;
   __syncthreads();
   if (s_last && tid == 0) {
     __threadfence();
@@ -658,6 +667,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
                 *(volatile unsigned long long *)&c->t_kx_end);
     c->cand_acc = 0;
     c->done_ctr = 0;
+    c->tile_ctr = 0;
     c->t_prev = t;
     c->level = c->level + 1;  // Fig1 L10
     c->cur = nxt;
@@ -997,9 +1007,11 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params 
   Ctl *c = P.ctl;
   if (c->tier != TIER_BU) return;
   __shared__ int32_t s_k[KD_WARPS], s_d[KD_WARPS];
-  __shared__ int s_last;
+  __shared__ int s_last, s_tile;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int b = blockIdx.x, nb = gridDim.x;
+  if (tid == 0) s_tile = (int)atomicAdd(&c->tile_ctr, 1u);  // look-back order = start order
+  __syncthreads();
+  const int b = s_tile, nb = gridDim.x;
   const int cur = c->cur, nxt = cur ^ 1;
   const int new_level = c->level + 1;
   const int4 *__restrict__ vinfo = P.vinfo;
@@ -1120,6 +1132,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params 
     record_stat(P, c, c->level, c->n_l, c->e_l, TIER_BU, nb, n_next, n_next, c->t_prev, t,
                 *(volatile unsigned long long *)&c->t_kx_begin, t);
     c->done_ctr = 0;
+    c->tile_ctr = 0;
     c->t_prev = t;
     c->level = c->level + 1;
     c->cur = nxt;

@@ -21,7 +21,7 @@ S3BFS_OK = 0
 STATUS_NAMES = {0: "ok", 1: "invalid argument", 2: "unsupported", 3: "out of memory",
                 4: "CUDA error", 5: "invalid CSR graph"}
 
-EXPORTED = ("s3bfs_create", "s3bfs_run", "s3bfs_destroy", "s3bfs_status_string",
+EXPORTED = ("s3bfs_create", "s3bfs_clone", "s3bfs_run", "s3bfs_destroy", "s3bfs_status_string",
             "s3bfs_last_error", "s3bfs_get_level_stats", "s3bfs_get_info", "s3bfs_get_kernel_times",
             "s3bfs_debug_exclusive_scan", "s3bfs_debug_find_start_points")
 
@@ -85,6 +85,7 @@ def load(build_if_missing: bool = True):
     vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
     lib.s3bfs_create.argtypes = [ctypes.POINTER(vp), i32, i64, vp, vp, ctypes.POINTER(Options), vp]
     lib.s3bfs_run.argtypes = [vp, i32, vp, vp, vp]
+    lib.s3bfs_clone.argtypes = [vp, ctypes.POINTER(vp), vp]
     lib.s3bfs_destroy.argtypes = [vp]
     lib.s3bfs_status_string.argtypes = [ctypes.c_int]
     lib.s3bfs_status_string.restype = ctypes.c_char_p
@@ -144,6 +145,13 @@ def s3bfs_create(row_offsets, col_indices, options: Options | None = None, strea
     rc = load().s3bfs_create(ctypes.byref(h), n, nnz, _ptr(row_offsets), col_p, opts,
                              _stream(stream))
     _check(rc, "s3bfs_create")
+    return h
+
+
+def s3bfs_clone(handle, stream=None):
+    """NEXT-2: a handle sharing `handle`'s prepared graph, with its own workspace."""
+    h = ctypes.c_void_p()
+    _check(load().s3bfs_clone(handle, ctypes.byref(h), _stream(stream)), "s3bfs_clone", handle)
     return h
 
 
@@ -232,6 +240,13 @@ class S3BFS:
             parent = torch.empty(self.n, dtype=torch.int32, device=dev)
         s3bfs_run(self.handle, source, level, parent, stream)
         return level, parent
+
+    def clone(self, stream=None) -> "S3BFS":
+        """NEXT-2: another traversal context over the same prepared graph."""
+        c = S3BFS.__new__(S3BFS)
+        c.row_offsets, c.col_indices, c.n = self.row_offsets, self.col_indices, self.n
+        c.handle = s3bfs_clone(self.handle, stream)
+        return c
 
     def level_stats(self) -> np.ndarray:
         return s3bfs_get_level_stats(self.handle)

@@ -266,3 +266,34 @@ def test_configs_levels_bit_exact(cfg, max_sources):
     for s in g.sources[:max_sources]:
         check_traversal(g, bfs, s)
     bfs.close()
+
+
+# ---- NEXT-2: clones over one prepared graph, concurrent traversals on separate streams -------
+@pytest.mark.parametrize("cfg_kw", [("rmat", dict(debug_poison=1)),
+                                    ("rmat", dict(debug_poison=1, direction=1)),
+                                    ("grid", dict(debug_poison=1))])
+def test_clones_run_concurrently(cfg_kw):
+    kind, kw = cfg_kw
+    g = graphgen.rmat(14, 16, seed=3) if kind == "rmat" else graphgen.grid(64, 64)
+    g.name = kind
+    ro, col = to_dev(g)
+    base = pkg.S3BFS(ro, col, pkg.Options(**kw))
+    clones = [base] + [base.clone() for _ in range(7)]
+    srcs = graphgen.pick_sources(g, 8, seed=11)
+    streams = [torch.cuda.Stream() for _ in clones]
+    outs = []
+    for h, st, s in zip(clones, streams, srcs):
+        lv = torch.empty(g.n, dtype=torch.int32, device="cuda")
+        pa = torch.empty(g.n, dtype=torch.int32, device="cuda")
+        pkg.s3bfs_run(h.handle, s, lv, pa, st)
+        outs.append((s, lv, pa))
+    torch.cuda.synchronize()
+    base.close()                      # the prepared graph outlives the source handle
+    for (s, lv, pa), h in zip(outs, clones):
+        ref, _ = oracle.bfs(g.row_offsets, g.col_indices, s)
+        assert np.array_equal(lv.cpu().numpy(), ref)
+        assert oracle.check_bfs(g.row_offsets, g.col_indices, s, lv.cpu().numpy(),
+                                pa.cpu().numpy())[0] == 0
+    for h in clones[1:]:              # clones still usable after the source is gone
+        check_traversal(g, h, srcs[0], stats=False)
+        h.close()
