@@ -151,6 +151,10 @@ typedef struct {
 } s3bfs_kernel_times;
 s3bfs_status s3bfs_get_kernel_times(s3bfs_handle h, s3bfs_kernel_times *out);
 
+/* Test-only: %globaltimer stamps of the last run's first level (ns): out[0] k_init start,
+ * out[1] first k_dispatch, out[2] k_small start (0 when not reached).  Synchronises. */
+s3bfs_status s3bfs_debug_timeline(s3bfs_handle h, uint64_t out[4]);
+
 /* ---- test-only entry points (same kernels the traversal uses) ------------------------ */
 
 /* (b) alone: single-pass decoupled-look-back exclusive scan (Fig1 L14; DESIGN R5).

@@ -3,11 +3,15 @@
 // Owns the workspace, resolves the (f) tunables (P_max from the occupancy of the level
 // kernels on this device, the grain, T0), and builds the captured level loop:
 //
-//   s3bfs_run:  k_init (Fig1 L1-L8)  ->  graph { WHILE(n_l > 0) {              Fig1 L9
-//                                          k_dispatch;                        (f)
-//                                          IF(tier 0) { k_small }             (f) tier 0
-//                                          IF(tier 1) { k_explore; k_compact }  (c)(d) / (e)(a)(b)
-//                                      } }
+//   s3bfs_run:  graph { k_init (Fig1 L1-L8);
+//                       WHILE(n_l > 0) {                                   Fig1 L9
+//                         IF(tier 0)  { k_small }                          (f) tier 0
+//                         IF(tier 1)  { k_explore; k_compact }             (c)(d) / (e)(a)(b)
+//                         IF(bottom-up) { k_fb_clear; k_fb_set; k_bottom_up }   NEXT-3
+//                       }
+//                       k_finalize }
+//   The kernel that decides a level's successor sets the conditional handles (no dispatch
+//   kernel); k_init's per-run arguments are patched into the executable graph per run.
 //
 // The host crosses the host/device boundary once per traversal (enqueue); the level loop,
 // P_l and every per-level decision stay on the device (SURVEY.md s.8(a) row f, H6).
@@ -54,6 +58,7 @@ struct s3bfs_ctx {
   int loop_graph = 1;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
+  cudaGraphNode_t init_node = nullptr;
   cudaStream_t last_stream = nullptr;
   bool ran = false;
   Ctl *h_ctl = nullptr;  // pinned, host-loop mode
@@ -262,11 +267,22 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
   wp.conditional.handle = hw;
   wp.conditional.type = cudaGraphCondTypeWhile;
   wp.conditional.size = 1;
+  void *args[] = {&h->P};
+  {  // first node: k_init (its source / output pointers are patched per run)
+    int32_t s0 = 0;
+    int32_t *l0 = nullptr, *p0 = nullptr;
+    void *iargs[] = {&h->P, &s0, &l0, &p0};
+    cudaKernelNodeParams ki = {};
+    ki.func = (void *)k_init;
+    ki.gridDim = dim3(init_grid(h));
+    ki.blockDim = dim3(256);
+    ki.kernelParams = iargs;
+    CK(h, cudaGraphAddKernelNode(&h->init_node, g, nullptr, 0, &ki));
+  }
   cudaGraphNode_t wnode;
-  CK(h, cudaGraphAddNode(&wnode, g, nullptr, 0, &wp));
+  CK(h, cudaGraphAddNode(&wnode, g, &h->init_node, 1, &wp));
   cudaGraph_t body = wp.conditional.phGraph_out[0];
 
-  void *args[] = {&h->P};
   {  // after the loop: d[0:n-1] and parent in caller ids
     cudaKernelNodeParams kf = {};
     kf.func = (void *)k_finalize;
@@ -285,16 +301,13 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
     k.kernelParams = args;
     return k;
   };
-  cudaGraphNode_t nd, n0, n1;
-  cudaKernelNodeParams kd = kparams((void *)k_dispatch, 1, 1, 0);
-  CK(h, cudaGraphAddKernelNode(&nd, body, nullptr, 0, &kd));
-
+  cudaGraphNode_t n0, n1;
   cudaGraphNodeParams ip0 = {};
   ip0.type = cudaGraphNodeTypeConditional;
   ip0.conditional.handle = h0;
   ip0.conditional.type = cudaGraphCondTypeIf;
   ip0.conditional.size = 1;
-  CK(h, cudaGraphAddNode(&n0, body, &nd, 1, &ip0));
+  CK(h, cudaGraphAddNode(&n0, body, nullptr, 0, &ip0));
   cudaGraph_t b0 = ip0.conditional.phGraph_out[0];
   cudaGraphNode_t ks;
   cudaKernelNodeParams kks = kparams((void *)k_small, 1, KS_THREADS, h->ks_smem);
@@ -518,6 +531,7 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
     if ((e = cudaGetLastError()) != cudaSuccess) return bail(cuda_fail(h, e, "k_build_vinfo"));
     h->ro_int = row_offsets;
   }
+  P.col_vec = (((uintptr_t)P.col) & 15) == 0 ? 1 : 0;
   if (P.direction && !share) {
     s3bfs_status ts = build_in_adjacency(h, stream);
     if (ts != S3BFS_OK) return bail(ts);
@@ -573,14 +587,21 @@ s3bfs_status s3bfs_run(s3bfs_handle h, int32_t source, int32_t *level, int32_t *
   if (!is_device_ptr(level) || !is_device_ptr(parent))
     return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "level/parent must be device memory");
   cudaStream_t stream = (cudaStream_t)stream_;
-  k_init<<<init_grid(h), 256, 0, stream>>>(h->P, source, level, parent);
-  CK(h, cudaGetLastError());
   h->last_stream = stream;
   h->ran = true;
   if (h->loop_graph) {
+    void *iargs[] = {&h->P, &source, &level, &parent};
+    cudaKernelNodeParams ki = {};
+    ki.func = (void *)k_init;
+    ki.gridDim = dim3(init_grid(h));
+    ki.blockDim = dim3(256);
+    ki.kernelParams = iargs;
+    CK(h, cudaGraphExecKernelNodeSetParams(h->exec, h->init_node, &ki));
     CK(h, cudaGraphLaunch(h->exec, stream));
     return S3BFS_OK;
   }
+  k_init<<<init_grid(h), 256, 0, stream>>>(h->P, source, level, parent);
+  CK(h, cudaGetLastError());
   // host-driven loop: one control-block read per level (debug / timing mode)
   h->kt = s3bfs_kernel_times{};
   int pending = -1;  // tier of the launch whose events are not yet read
@@ -668,6 +689,15 @@ s3bfs_status s3bfs_get_kernel_times(s3bfs_handle h, s3bfs_kernel_times *out) {
   if (!h || !out) return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "bad arguments");
   if (h->ran) CK(h, cudaStreamSynchronize(h->last_stream));
   *out = h->kt;
+  return S3BFS_OK;
+}
+
+s3bfs_status s3bfs_debug_timeline(s3bfs_handle h, uint64_t out[4]) {
+  if (!h || !out) return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (h->ran) CK(h, cudaStreamSynchronize(h->last_stream));
+  Ctl c;
+  CK(h, cudaMemcpy(&c, h->P.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < 4; ++i) out[i] = c.t_dbg[i];
   return S3BFS_OK;
 }
 

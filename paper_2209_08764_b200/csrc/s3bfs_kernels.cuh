@@ -21,7 +21,6 @@
 //                           pairs across CTAs, write f_next / row starts / degree scan.
 //   k_small    tier 0 (f)   one CTA runs whole levels (a)-(e) in shared memory while the level
 //                           stays tiny (P:22 -- "never use more cores than necessary").
-//   k_dispatch (f)          graph mode: selects the tier of the next WHILE iteration.
 //   k_finalize              d[0:n-1] and parent in caller ids ("Returns d[0:n-1]").
 //   k_scan_u32 (b) alone    test entry: the same look-back scan over a plain int32 array.
 //   k_find_start (c) alone  test entry: the same warp search, one warp per worker.
@@ -51,6 +50,15 @@ namespace s3bfs {
 #endif
 #ifndef S3BFS_KS_BATCHED
 #define S3BFS_KS_BATCHED 1
+#endif
+#ifndef S3BFS_KX_RANK
+#define S3BFS_KX_RANK 1   // rank (REDUX + POPC) edge->row mapping for multi-row batches
+#endif
+#ifndef S3BFS_KX_PIPE2
+#define S3BFS_KX_PIPE2 0  // software-pipelined batches (experiment switch)
+#endif
+#ifndef S3BFS_KX_VEC
+#define S3BFS_KX_VEC 1    // 16-byte col loads in the uniform-row fast path
 #endif
 #ifndef S3BFS_BM_NC
 #define S3BFS_BM_NC 1     // bitmap probes through the non-coherent (read-only) path
@@ -97,6 +105,7 @@ struct Ctl {
   int32_t *level_out, *parent_out;
   unsigned long long t_prev;
   unsigned long long t_kx_begin, t_kx_end;  // k_explore CTA 0 start, k_compact CTA 0 start
+  unsigned long long t_dbg[4];  // first-level timeline: init start, dispatch, k_small start/end
 };
 
 struct Params {
@@ -124,6 +133,7 @@ struct Params {
   int32_t direction, do_alpha, do_beta;  // NEXT-3 switch rule (Beamer): alpha, beta
   int32_t n_scan;               // bottom-up scans internal ids [0, n_scan): the ones with deg > 0
   long long nnz;
+  int32_t col_vec;              // col is 16-byte aligned: vectorised loads allowed
   int32_t use_graph;
   unsigned long long h_while, h_t0, h_t1, h_t2;  // cudaGraphConditionalHandle values
 };
@@ -151,6 +161,12 @@ __device__ __forceinline__ unsigned long long policy_evict_last() {
 __device__ __forceinline__ int ldg_stream(const int32_t *p, unsigned long long pol) {
   int v;
   asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int4 ldg_stream4(const int32_t *p, unsigned long long pol) {
+  int4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
   return v;
 }
 // the visited bitmap inside k_explore: read-only there (written by earlier kernels only); the
@@ -315,7 +331,24 @@ __device__ void record_stat(const Params &P, Ctl *c, int32_t level, int32_t n_l,
   c->num_levels = k + 1;
 }
 
+// Graph mode: the thread that decides the next level's tier also steers the captured loop --
+// WHILE (more levels) and the three IF nodes (tier 0 / top-down / bottom-up) that follow one
+// another inside a WHILE iteration.  No separate dispatch kernel.
+__device__ void steer(const Params &P, int tier) {
+  if (!P.use_graph) return;
+  cudaGraphSetConditional((cudaGraphConditionalHandle)P.h_t0, tier == TIER_SMALL ? 1u : 0u);
+  cudaGraphSetConditional((cudaGraphConditionalHandle)P.h_t1, tier == TIER_LARGE ? 1u : 0u);
+  if (P.direction)
+    cudaGraphSetConditional((cudaGraphConditionalHandle)P.h_t2, tier == TIER_BU ? 1u : 0u);
+  cudaGraphSetConditional((cudaGraphConditionalHandle)P.h_while, tier != TIER_DONE ? 1u : 0u);
+}
+
+__device__ void decide_tier(const Params &P, Ctl *c, int32_t n_l, int32_t e_l);
 __device__ void decide(const Params &P, Ctl *c, int32_t n_l, int32_t e_l) {
+  decide_tier(P, c, n_l, e_l);
+  steer(P, c->tier);
+}
+__device__ void decide_tier(const Params &P, Ctl *c, int32_t n_l, int32_t e_l) {
   c->n_l = n_l;
   c->e_l = e_l;
   if (n_l == 0 || e_l == 0) {  // C10: nothing to explore, the loop ends (Fig1 L9)
@@ -392,21 +425,13 @@ __global__ void k_init(Params P, int32_t s, int32_t *level, int32_t *parent) {
     c->tile_ctr = 0;
     c->cand_acc = 0;
     c->t_prev = globaltimer();
+    c->t_dbg[0] = c->t_prev;
+    c->t_dbg[1] = 0;
     c->bu = 0;
     c->fb_valid = 0;
     c->m_visited = vs.y;
     decide(P, c, 1, vs.y);
   }
-}
-
-// Graph mode: one thread selects what the next WHILE iteration runs (f).
-__global__ void k_dispatch(Params P) {
-  const int t = P.ctl->tier;
-  cudaGraphSetConditional((cudaGraphConditionalHandle)P.h_t0, t == TIER_SMALL ? 1u : 0u);
-  cudaGraphSetConditional((cudaGraphConditionalHandle)P.h_t1, t == TIER_LARGE ? 1u : 0u);
-  if (P.direction)
-    cudaGraphSetConditional((cudaGraphConditionalHandle)P.h_t2, t == TIER_BU ? 1u : 0u);
-  if (t == TIER_DONE) cudaGraphSetConditional((cudaGraphConditionalHandle)P.h_while, 0u);
 }
 
 // ---- (c)+(d): k_explore ----------------------------------------------------------------------
@@ -459,25 +484,30 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   const unsigned long long pol_status = policy_evict_last();
   int wcount = 0;
   int u0 = 0, wex = 0, wx = 0, wb = 0, lim = 0;
+  bool wzero = false;  // the window holds an empty row (two equal row starts)
   auto load_window = [&](int base) {
     const int u = base + lane;
     wex = (u < n_l) ? __ldg(fex + u) : 0x7fffffff;
     wx = (u < n_l) ? __ldg(fx + u) : 0;
     wb = (u < n_l) ? __ldg(frs + u) - wex : 0;
     lim = __ldg(fex + min(base + 32, n_l));
+    const int down = __shfl_down_sync(0xffffffffu, wex, 1);  // all lanes shuffle
+    const int nxt_start = (lane < 31) ? down : lim;
+    wzero = __any_sync(0xffffffffu, u < n_l && nxt_start == wex);
   };
   if (e_begin < e_end) {
     u0 = warp_search(fex, n_l, e_begin);  // Find-StartExpPoint (c)
     load_window(u0);
   }
-  int e = e_begin;
-  while (e < e_end) {
-    while (lim <= e) {  // window exhausted (also skips runs of zero-degree vertices, C9)
+#if S3BFS_KX_PIPE2
+  // software-pipelined: batch k+1's col loads are in flight while batch k is probed; two
+  // register sets (A/B) alternate so no pending load is ever copied
+  auto map_load = [&](int e, int (&v)[KX_GROUPS], int (&xv)[KX_GROUPS]) -> int {
+    while (lim <= e) {
       u0 += 32;
       load_window(u0);
     }
     const int bend = min(e_end, lim);
-    int v[KX_GROUPS], xv[KX_GROUPS];
     int j0 = 0;  // window slot of the batch's first edge (warp-uniform)
 #pragma unroll
     for (int s = 16; s >= 1; s >>= 1) {
@@ -485,15 +515,54 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
       if (cj <= e) j0 += s;
     }
     const int row_end = (j0 < 31) ? __shfl_sync(0xffffffffu, wex, min(j0 + 1, 31)) : lim;
+    int e_next = min(e + KX_GROUPS * 32, bend);
     if (S3BFS_KX_FAST && row_end >= min(e + KX_GROUPS * 32, bend)) {
       // the whole batch lies in one frontier row (most R-MAT arcs): uniform x and base
       const int x = __shfl_sync(0xffffffffu, wx, j0);
       const int base = __shfl_sync(0xffffffffu, wb, j0);
+      const int start = base + e;  // col index of the batch's first edge
+      const int a0 = start & ~3;   // 16-byte aligned
+#pragma unroll
+      for (int g = 0; g < KX_GROUPS; ++g) xv[g] = x;
+      if (S3BFS_KX_VEC && P.col_vec && (long long)a0 + KX_GROUPS * 32 <= P.nnz) {
+        // vectorised streaming: lane i loads 16 B at a0 + 4*(i + 32k), i.e. each warp
+        // instruction fetches 512 contiguous bytes of the row; edges outside
+        // [start, row/slice end) are masked.  Next batch starts 16-byte aligned.
+        const int lim_idx = base + bend;
+#pragma unroll
+        for (int k = 0; k < KX_GROUPS / 4; ++k) {
+          const int i0 = a0 + 4 * (lane + 32 * k);
+          int4 q = make_int4(-1, -1, -1, -1);
+          if (i0 < lim_idx) q = ldg_stream4(col + i0, pol_stream);
+          v[4 * k + 0] = (i0 + 0 >= start && i0 + 0 < lim_idx) ? q.x : -1;
+          v[4 * k + 1] = (i0 + 1 >= start && i0 + 1 < lim_idx) ? q.y : -1;
+          v[4 * k + 2] = (i0 + 2 >= start && i0 + 2 < lim_idx) ? q.z : -1;
+          v[4 * k + 3] = (i0 + 3 >= start && i0 + 3 < lim_idx) ? q.w : -1;
+        }
+        e_next = min(bend, a0 + KX_GROUPS * 32 - base);
+      } else {
+#pragma unroll
+        for (int g = 0; g < KX_GROUPS; ++g) {
+          const int my_e = e + g * 32 + lane;
+          v[g] = (my_e < bend) ? ldg_stream(col + base + my_e, pol_stream) : -1;
+        }
+      }
+    } else if (S3BFS_KX_RANK && !wzero) {
+      // several rows in the batch: rank mapping.  Window lane j's row starts at edge wex_j;
+      // for group g (edges eg .. eg+31) the row starts strictly inside the group form a
+      // 32-bit mask (one REDUX), and lane i's row is the group's first row plus the number
+      // of row starts at or below edge eg+i (exact while no row of the window is empty)
+      int r = j0;  // row of the group's first edge
 #pragma unroll
       for (int g = 0; g < KX_GROUPS; ++g) {
-        const int my_e = e + g * 32 + lane;
-        xv[g] = x;
-        v[g] = (my_e < bend) ? ldg_stream(col + base + my_e, pol_stream) : -1;
+        const int eg = e + g * 32;
+        const int rel = wex - eg;  // this window lane's row start relative to the group
+        const unsigned m = __reduce_or_sync(0xffffffffu, (rel >= 1 && rel < 32) ? (1u << rel) : 0u);
+        const int j = r + __popc(m & ((2u << lane) - 2u));
+        xv[g] = __shfl_sync(0xffffffffu, wx, j);
+        const int pos = __shfl_sync(0xffffffffu, wb, j) + eg + lane;
+        v[g] = (eg + lane < bend) ? ldg_stream(col + pos, pol_stream) : -1;
+        r += __popc(m) + (__any_sync(0xffffffffu, rel == 32) ? 1 : 0);
       }
     } else {
 #pragma unroll
@@ -540,8 +609,115 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
         wcount += __popc(m);
       }
     }
-    e = min(e + KX_GROUPS * 32, bend);
+  };
+  int vA[KX_GROUPS], xA[KX_GROUPS], vB[KX_GROUPS], xB[KX_GROUPS];
+  int e = e_begin;
+  int eA = e < e_end ? map_load(e, vA, xA) : e_end;
+  while (e < e_end) {
+    int eB = eA < e_end ? map_load(eA, vB, xB) : e_end;
+    process(vA, xA);
+    e = eA;
+    if (e >= e_end) break;
+    eA = eB < e_end ? map_load(eB, vA, xA) : e_end;
+    process(vB, xB);
+    e = eB;
   }
+#else
+  int e = e_begin;
+  while (e < e_end) {
+    while (lim <= e) {  // window exhausted (also skips runs of zero-degree vertices, C9)
+      u0 += 32;
+      load_window(u0);
+    }
+    const int bend = min(e_end, lim);
+    int v[KX_GROUPS], xv[KX_GROUPS];
+    int j0 = 0;  // window slot of the batch's first edge (warp-uniform)
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+      const int cj = __shfl_sync(0xffffffffu, wex, j0 + s);
+      if (cj <= e) j0 += s;
+    }
+    const int row_end = (j0 < 31) ? __shfl_sync(0xffffffffu, wex, min(j0 + 1, 31)) : lim;
+    int e_next = min(e + KX_GROUPS * 32, bend);
+    if (S3BFS_KX_FAST && row_end >= min(e + KX_GROUPS * 32, bend)) {
+      // the whole batch lies in one frontier row (most R-MAT arcs): uniform x and base
+      const int x = __shfl_sync(0xffffffffu, wx, j0);
+      const int base = __shfl_sync(0xffffffffu, wb, j0);
+      const int start = base + e;  // col index of the batch's first edge
+      const int a0 = start & ~3;   // 16-byte aligned
+#pragma unroll
+      for (int g = 0; g < KX_GROUPS; ++g) xv[g] = x;
+      if (S3BFS_KX_VEC && P.col_vec && (long long)a0 + KX_GROUPS * 32 <= P.nnz) {
+        // vectorised streaming: lane i loads 16 B at a0 + 4*(i + 32k), i.e. each warp
+        // instruction fetches 512 contiguous bytes of the row; edges outside
+        // [start, row/slice end) are masked.  Next batch starts 16-byte aligned.
+        const int lim_idx = base + bend;
+#pragma unroll
+        for (int k = 0; k < KX_GROUPS / 4; ++k) {
+          const int i0 = a0 + 4 * (lane + 32 * k);
+          int4 q = make_int4(-1, -1, -1, -1);
+          if (i0 < lim_idx) q = ldg_stream4(col + i0, pol_stream);
+          v[4 * k + 0] = (i0 + 0 >= start && i0 + 0 < lim_idx) ? q.x : -1;
+          v[4 * k + 1] = (i0 + 1 >= start && i0 + 1 < lim_idx) ? q.y : -1;
+          v[4 * k + 2] = (i0 + 2 >= start && i0 + 2 < lim_idx) ? q.z : -1;
+          v[4 * k + 3] = (i0 + 3 >= start && i0 + 3 < lim_idx) ? q.w : -1;
+        }
+        e_next = min(bend, a0 + KX_GROUPS * 32 - base);
+      } else {
+#pragma unroll
+        for (int g = 0; g < KX_GROUPS; ++g) {
+          const int my_e = e + g * 32 + lane;
+          v[g] = (my_e < bend) ? ldg_stream(col + base + my_e, pol_stream) : -1;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int g = 0; g < KX_GROUPS; ++g) {
+        const int my_e = e + g * 32 + lane;
+        int j = j0;  // largest window slot with excl <= my_e (>= j0)
+#pragma unroll
+        for (int s = 16; s >= 1; s >>= 1) {
+          const int cj = __shfl_sync(0xffffffffu, wex, min(j + s, 31));
+          if (j + s <= 31 && cj <= my_e) j += s;
+        }
+        xv[g] = __shfl_sync(0xffffffffu, wx, j);
+        const int pos = __shfl_sync(0xffffffffu, wb, j) + my_e;
+        v[g] = (my_e < bend) ? ldg_stream(col + pos, pol_stream) : -1;
+      }
+    }
+    // visited test: the bitmap (visited before this level), branch-free (an invalid slot
+    // probes word 0 and is masked); the claim/discovery code runs only if some lane of the
+    // warp met a vertex not visited at level start -- rare on the heavy levels
+    uint32_t needm = 0;
+#pragma unroll
+    for (int g = 0; g < KX_GROUPS; ++g) {
+      const int vv = max(v[g], 0);
+      const uint32_t w = S3BFS_BM_NC ? ldg_status_u32(bm + (vv >> 5), pol_status)
+                                     : ld_status_u32(bm + (vv >> 5), pol_status);
+      if (v[g] >= 0 && !((w >> (vv & 31)) & 1u)) needm |= 1u << g;
+    }
+    if (__any_sync(0xffffffffu, needm != 0)) {
+      int cl[KX_GROUPS];  // claim tags of the vertices not visited at level start
+#pragma unroll
+      for (int g = 0; g < KX_GROUPS; ++g)
+        cl[g] = ((needm >> g) & 1u) ? ld_cg_u8(claim + v[g]) : tag;
+#pragma unroll
+      for (int g = 0; g < KX_GROUPS; ++g) {
+        const bool disc = cl[g] != tag;
+        const unsigned m = __ballot_sync(0xffffffffu, disc);
+        if (disc) {
+          const int slot = segbase + wcount + __popc(m & lanemask_lt());
+          st_u8(claim + v[g], tag);
+          st_weak_v2(lp + v[g], new_level, xv[g]);   // d[v] <- l, parent (Fig1 L18)
+          st_weak(owner_of(vinfo, v[g]), slot);      // Owner[v] <- i (benign race)
+          cand[slot] = v[g];                         // Q[i].Enqueue(v)
+        }
+        wcount += __popc(m);
+      }
+    }
+    e = e_next;
+  }
+#endif
   if (lane == 0) P.wcnt[b * KD_WARPS + warp] = wcount;
 }
 
@@ -779,6 +955,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
   int n_l = c->n_l, e_l = c->e_l, L = c->level;
   const int cur = c->cur;
   unsigned long long t_prev = c->t_prev;
+  if (tid == 0 && L == 0) c->t_dbg[2] = globaltimer();
   long long m_add = 0;  // degrees of the frontiers created here (thread 0)
   for (int i = tid; i < n_l; i += KS_THREADS) {
     sf[i] = P.f[cur][i];

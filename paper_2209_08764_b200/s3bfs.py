@@ -23,7 +23,7 @@ STATUS_NAMES = {0: "ok", 1: "invalid argument", 2: "unsupported", 3: "out of mem
 
 EXPORTED = ("s3bfs_create", "s3bfs_clone", "s3bfs_run", "s3bfs_destroy", "s3bfs_status_string",
             "s3bfs_last_error", "s3bfs_get_level_stats", "s3bfs_get_info", "s3bfs_get_kernel_times",
-            "s3bfs_debug_exclusive_scan", "s3bfs_debug_find_start_points")
+            "s3bfs_debug_exclusive_scan", "s3bfs_debug_find_start_points", "s3bfs_debug_timeline")
 
 
 class S3BFSError(RuntimeError):
@@ -95,6 +95,7 @@ def load(build_if_missing: bool = True):
     lib.s3bfs_get_kernel_times.argtypes = [vp, ctypes.POINTER(KernelTimes)]
     lib.s3bfs_debug_exclusive_scan.argtypes = [vp, vp, i32, vp]
     lib.s3bfs_debug_find_start_points.argtypes = [vp, i32, i32, i32, vp, vp, vp]
+    lib.s3bfs_debug_timeline.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64)]
     for name in EXPORTED:
         if name != "s3bfs_status_string":
             getattr(lib, name).restype = ctypes.c_int
@@ -220,6 +221,12 @@ def s3bfs_debug_find_start_points(excl, chunk: int, p_l: int, out_u, out_off,
     _check(load().s3bfs_debug_find_start_points(_ptr(excl), n_l, int(chunk), int(p_l),
                                                 _ptr(out_u), _ptr(out_off), _stream(stream)),
            "s3bfs_debug_find_start_points")
+
+
+def s3bfs_debug_timeline(handle) -> list:
+    out = (ctypes.c_uint64 * 4)()
+    _check(load().s3bfs_debug_timeline(handle, out), "s3bfs_debug_timeline", handle)
+    return list(out)
 
 
 class S3BFS:

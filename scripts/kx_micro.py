@@ -38,6 +38,7 @@ if relabel:  # degree-descending internal ids (experiment: hot vertices get the 
     lvl = lvl[n2o]
     deg = deg2
     torch.cuda.synchronize()
+col = torch.cat([col, torch.zeros(1024, dtype=torch.int32, device=dev)])  # vector over-read pad
 L = int(lvl.max().item())
 lpbuf = torch.zeros((n, 2), dtype=torch.int32, device=dev)
 vinfo = torch.zeros((n, 4), dtype=torch.int32, device=dev)
@@ -73,7 +74,8 @@ for l, fr, e_l in levels:
         raw.kx_raw.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p,
                                ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                ctypes.POINTER(ctypes.c_float)]
-        for which, name in ((0, "stream-all-col"), (1, "rows-warp"), (2, "rows-warp+bm")):
+        for which, name in ((0, "stream-all-col"), (1, "rows-warp"), (2, "rows-warp+bm"),
+                            (3, "rows-chunked"), (4, "rows-chunked+bm")):
             if which == 0 and order == "sorted":
                 continue
             ms = ctypes.c_float()
