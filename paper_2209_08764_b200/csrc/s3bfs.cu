@@ -449,7 +449,9 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   const size_t o_crd = take((size_t)h->cand_cap * 8);
   const size_t bm_bytes = ((size_t)n + 127) / 128 * 16;  // 16 B padded (vector clears)
   const size_t o_bm = take(bm_bytes);
-  const size_t o_claim = take(((size_t)n + 15) / 16 * 16);
+  size_t claim_n = 16;  // claim slots: a power of two >= n (claim_slot's hash is mod 2^k)
+  while (claim_n < (size_t)n) claim_n <<= 1;
+  const size_t o_claim = take(claim_n);
   const size_t o_fb0 = take(bm_bytes), o_fb1 = take(bm_bytes);
   const size_t o_wcnt = take((size_t)p_max * KD_WARPS * 4);
   const size_t o_status = take((size_t)p_max * 8);
@@ -473,6 +475,7 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   P.cand_rd = (int2 *)(base + o_crd);
   P.bm = (uint32_t *)(base + o_bm);
   P.claim = (uint8_t *)(base + o_claim);
+  P.claim_mask = (uint32_t)(claim_n - 1);
   P.fb[0] = (uint32_t *)(base + o_fb0);
   P.fb[1] = (uint32_t *)(base + o_fb1);
   P.wcnt = (int32_t *)(base + o_wcnt);

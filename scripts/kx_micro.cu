@@ -21,6 +21,9 @@ extern "C" int kx_micro(const int32_t *col, int n, int n_l, int e_l, int32_t *f,
   P.col = col; P.vinfo = vinfo; P.lp = lp; P.n = n; P.ctl = ctl;
   P.f[0] = P.f[1] = f; P.frs[0] = P.frs[1] = frs; P.fex[0] = P.fex[1] = fex;
   P.cand = cand; P.bm = bm; P.claim = claim; P.wcnt = wcnt; P.status = status;
+  size_t claim_n = 16;  // as s3bfs_create: a power of two >= n (kx_micro.py allocates it)
+  while (claim_n < (size_t)n) claim_n <<= 1;
+  P.claim_mask = (uint32_t)(claim_n - 1);
   P.p_max = p_max; P.grain = grain; P.t0 = -1;
   P.nnz = 0x7fffffff;  // harness: col has 4 KB of padding (see kx_micro.py)
   P.col_vec = (((uintptr_t)col) & 15) == 0;
@@ -38,7 +41,7 @@ extern "C" int kx_micro(const int32_t *col, int n, int n_l, int e_l, int32_t *f,
   int cands = 0;
   for (int r = 0; r <= reps; ++r) {
     cudaMemcpy(ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice);
-    cudaMemset(claim, 0, ((size_t)n + 15) / 16 * 16);
+    cudaMemset(claim, 0, claim_n);
     cudaDeviceSynchronize();
     cudaEventRecord(a);
     k_explore<<<h.p_l, KD_THREADS, 0>>>(P);

@@ -47,7 +47,7 @@ vinfo[:, 1] = deg
 cand = torch.empty(g.nnz + 1_000_000, dtype=torch.int32, device=dev)
 wcnt = torch.zeros(4096 * 64, dtype=torch.int32, device=dev)
 status = torch.zeros(4096, dtype=torch.int64, device=dev)
-claim = torch.zeros((n + 15) // 16 * 16, dtype=torch.uint8, device=dev)
+claim = torch.zeros(max(16, 1 << (n - 1).bit_length()), dtype=torch.uint8, device=dev)  # pow2 slots
 out_l = torch.empty(n, dtype=torch.int32, device=dev)
 out_p = torch.empty(n, dtype=torch.int32, device=dev)
 levels = []

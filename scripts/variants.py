@@ -61,7 +61,7 @@ for tag, path in variants:
             lib.s3bfs_get_level_stats(h, buf, 256, ctypes.byref(num))
             lv = [(r.level, r.e_l, r.tier, (r.t_explore_end_ns - r.t_explore_begin_ns) / 1e3,
                    (r.t_end_ns - r.t_explore_end_ns) / 1e3 if r.tier == 1 else 0.0,
-                   r.candidates) for r in buf[: min(num.value, 256)]]
+                   r.candidates, r.kept) for r in buf[: min(num.value, 256)]]
             per.append({"src": s, "ms": ms, "gteps": m_c / 2 / ms / 1e6,
                         "heavy": [x for x in lv if x[1] > 1_000_000]})
             tot_ms += ms
@@ -72,6 +72,6 @@ for tag, path in variants:
         print(f"{key:32s} GTEPS {tot_e / tot_ms / 1e6:7.2f}  ms/src " +
               " ".join(f"{p['ms']:.3f}" for p in per), flush=True)
         for p in per[:2]:
-            print("    src", p["src"], " ".join(f"[e={x[1]/1e6:.1f}M kx={x[3]:.0f} kc={x[4]:.0f} c={x[5]/1e6:.2f}M]"
+            print("    src", p["src"], " ".join(f"[e={x[1]/1e6:.1f}M kx={x[3]:.0f} kc={x[4]:.0f} c={x[5]/1e6:.2f}M k={x[6]/1e6:.2f}M]"
                                                for x in p["heavy"]), flush=True)
 json.dump(results, open(os.environ.get("VARIANT_OUT", "gpurun_out/variants.json"), "w"))
