@@ -63,6 +63,9 @@ namespace s3bfs {
 #ifndef S3BFS_CLAIM_SCATTER
 #define S3BFS_CLAIM_SCATTER 1  // claim tag of v at a multiplicative-hash slot (see claim_slot)
 #endif
+#ifndef S3BFS_BM_AGG
+#define S3BFS_BM_AGG 1  // k_compact: one atomicOr per run of same-word kept candidates
+#endif
 #ifndef S3BFS_BM_NC
 #define S3BFS_BM_NC 1     // bitmap probes through the non-coherent (read-only) path
 #endif
@@ -735,6 +738,29 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   if (lane == 0) P.wcnt[b * KD_WARPS + warp] = wcount;
 }
 
+// Publish the visited bits of a warp's kept candidates: lanes holding the same bitmap word in
+// a run of consecutive lanes OR their bits together (segmented shuffle scan) and the run's
+// last lane issues one atomicOr -- same-word atomics from one instruction would serialise in
+// the L2 atomic unit.  Same-word lanes in different runs still issue separate (correct) ORs.
+__device__ __forceinline__ void bm_publish(uint32_t *bm, bool keep, int v, int lane) {
+#if S3BFS_BM_AGG
+  const int wd = keep ? (v >> 5) : -1;
+  uint32_t acc = keep ? 1u << (v & 31) : 0u;
+  const int prev = __shfl_up_sync(0xffffffffu, wd, 1);
+  const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || prev != wd);
+  const int run0 = 31 - __clz(heads & ((2u << lane) - 1u));  // first lane of my run
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    const uint32_t o = __shfl_up_sync(0xffffffffu, acc, s);
+    if (lane - s >= run0) acc |= o;
+  }
+  const bool last = lane == 31 || ((heads >> (lane + 1)) & 1u);
+  if (keep && last) atomicOr(bm + wd, acc);
+#else
+  if (keep) atomicOr(bm + (v >> 5), 1u << (v & 31));
+#endif
+}
+
 // ---- (e)+(a)+(b): k_compact -------------------------------------------------------------------
 // CTA b handles the candidate segments its k_explore twin wrote (one per warp).
 // Pass 1 (Fig1 L20-L23): keep cand[k] iff Owner[cand[k]] == k (one 16-byte vertex-record
@@ -784,7 +810,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
       const int k = k0 + g * 32 + lane;
       const bool keep = v[g] >= 0 && vi[g].w == seg + k;  // Fig1 L22: "if Owner[v] = i"
       const int d = keep ? vi[g].y : 0;
-      if (keep) atomicOr(P.bm + (v[g] >> 5), 1u << (v[g] & 31));  // exact visited bit (R17)
+      bm_publish(P.bm, keep, v[g], lane);  // exact visited bit (R17)
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       if (keep) {
         const int q = seg + kept + __popc(m & lanemask_lt());
