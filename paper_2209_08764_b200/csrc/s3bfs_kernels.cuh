@@ -54,9 +54,6 @@ namespace s3bfs {
 #ifndef S3BFS_KX_RANK
 #define S3BFS_KX_RANK 1   // rank (REDUX + POPC) edge->row mapping for multi-row batches
 #endif
-#ifndef S3BFS_KX_PIPE2
-#define S3BFS_KX_PIPE2 0  // software-pipelined batches (experiment switch)
-#endif
 #ifndef S3BFS_KX_VEC
 #define S3BFS_KX_VEC 1    // 16-byte col loads in the uniform-row fast path
 #endif
@@ -516,11 +513,10 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
     u0 = warp_search(fex, n_l, e_begin);  // Find-StartExpPoint (c)
     load_window(u0);
   }
-#if S3BFS_KX_PIPE2
-  // software-pipelined: batch k+1's col loads are in flight while batch k is probed; two
-  // register sets (A/B) alternate so no pending load is ever copied
+  // Map the batch of edges [e, e_next) onto lanes and load their targets: v[g] = col entry of
+  // edge e + 32g + lane (-1 outside the batch), xv[g] = its frontier vertex (caller id).
   auto map_load = [&](int e, int (&v)[KX_GROUPS], int (&xv)[KX_GROUPS]) -> int {
-    while (lim <= e) {
+    while (lim <= e) {  // window exhausted (also skips runs of zero-degree vertices, C9)
       u0 += 32;
       load_window(u0);
     }
@@ -533,7 +529,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
     }
     const int row_end = (j0 < 31) ? __shfl_sync(0xffffffffu, wex, min(j0 + 1, 31)) : lim;
     int e_next = min(e + KX_GROUPS * 32, bend);
-    if (S3BFS_KX_FAST && row_end >= min(e + KX_GROUPS * 32, bend)) {
+    if (S3BFS_KX_FAST && row_end >= e_next) {
       // the whole batch lies in one frontier row (most R-MAT arcs): uniform x and base
       const int x = __shfl_sync(0xffffffffu, wx, j0);
       const int base = __shfl_sync(0xffffffffu, wb, j0);
@@ -569,13 +565,14 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
       // for group g (edges eg .. eg+31) the row starts strictly inside the group form a
       // 32-bit mask (one REDUX), and lane i's row is the group's first row plus the number
       // of row starts at or below edge eg+i (exact while no row of the window is empty)
+      const unsigned le = (2u << lane) - 2u;  // bits 1 .. lane
       int r = j0;  // row of the group's first edge
 #pragma unroll
       for (int g = 0; g < KX_GROUPS; ++g) {
         const int eg = e + g * 32;
         const int rel = wex - eg;  // this window lane's row start relative to the group
-        const unsigned m = __reduce_or_sync(0xffffffffu, (rel >= 1 && rel < 32) ? (1u << rel) : 0u);
-        const int j = r + __popc(m & ((2u << lane) - 2u));
+        const unsigned m = __reduce_or_sync(0xffffffffu, ((unsigned)(rel - 1) < 31u) ? (1u << rel) : 0u);
+        const int j = r + __popc(m & le);
         xv[g] = __shfl_sync(0xffffffffu, wx, j);
         const int pos = __shfl_sync(0xffffffffu, wb, j) + eg + lane;
         v[g] = (eg + lane < bend) ? ldg_stream(col + pos, pol_stream) : -1;
@@ -596,115 +593,14 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
         v[g] = (my_e < bend) ? ldg_stream(col + pos, pol_stream) : -1;
       }
     }
-    // visited test: the bitmap (visited before this level), branch-free (an invalid slot
-    // probes word 0 and is masked); the claim/discovery code runs only if some lane of the
-    // warp met a vertex not visited at level start -- rare on the heavy levels
-    uint32_t needm = 0;
-#pragma unroll
-    for (int g = 0; g < KX_GROUPS; ++g) {
-      const int vv = max(v[g], 0);
-      const uint32_t w = S3BFS_BM_NC ? ldg_status_u32(bm + (vv >> 5), pol_status)
-                                     : ld_status_u32(bm + (vv >> 5), pol_status);
-      if (v[g] >= 0 && !((w >> (vv & 31)) & 1u)) needm |= 1u << g;
-    }
-    if (__any_sync(0xffffffffu, needm != 0)) {
-      int cl[KX_GROUPS];  // claim tags of the vertices not visited at level start
-#pragma unroll
-      for (int g = 0; g < KX_GROUPS; ++g)
-        cl[g] = ((needm >> g) & 1u) ? ld_cg_u8(claim + claim_slot(P, v[g])) : tag;
-#pragma unroll
-      for (int g = 0; g < KX_GROUPS; ++g) {
-        const bool disc = cl[g] != tag;
-        const unsigned m = __ballot_sync(0xffffffffu, disc);
-        if (disc) {
-          const int slot = segbase + wcount + __popc(m & lanemask_lt());
-          st_u8(claim + claim_slot(P, v[g]), tag);
-          st_weak_v2(lp + v[g], new_level, xv[g]);   // d[v] <- l, parent (Fig1 L18)
-          st_weak(owner_of(vinfo, v[g]), slot);      // Owner[v] <- i (benign race)
-          cand[slot] = v[g];                         // Q[i].Enqueue(v)
-        }
-        wcount += __popc(m);
-      }
-    }
+    return e_next;
   };
-  int vA[KX_GROUPS], xA[KX_GROUPS], vB[KX_GROUPS], xB[KX_GROUPS];
-  int e = e_begin;
-  int eA = e < e_end ? map_load(e, vA, xA) : e_end;
-  while (e < e_end) {
-    int eB = eA < e_end ? map_load(eA, vB, xB) : e_end;
-    process(vA, xA);
-    e = eA;
-    if (e >= e_end) break;
-    eA = eB < e_end ? map_load(eB, vA, xA) : e_end;
-    process(vB, xB);
-    e = eB;
-  }
-#else
   int e = e_begin;
   while (e < e_end) {
-    while (lim <= e) {  // window exhausted (also skips runs of zero-degree vertices, C9)
-      u0 += 32;
-      load_window(u0);
-    }
-    const int bend = min(e_end, lim);
     int v[KX_GROUPS], xv[KX_GROUPS];
-    int j0 = 0;  // window slot of the batch's first edge (warp-uniform)
-#pragma unroll
-    for (int s = 16; s >= 1; s >>= 1) {
-      const int cj = __shfl_sync(0xffffffffu, wex, j0 + s);
-      if (cj <= e) j0 += s;
-    }
-    const int row_end = (j0 < 31) ? __shfl_sync(0xffffffffu, wex, min(j0 + 1, 31)) : lim;
-    int e_next = min(e + KX_GROUPS * 32, bend);
-    if (S3BFS_KX_FAST && row_end >= min(e + KX_GROUPS * 32, bend)) {
-      // the whole batch lies in one frontier row (most R-MAT arcs): uniform x and base
-      const int x = __shfl_sync(0xffffffffu, wx, j0);
-      const int base = __shfl_sync(0xffffffffu, wb, j0);
-      const int start = base + e;  // col index of the batch's first edge
-      const int a0 = start & ~3;   // 16-byte aligned
-#pragma unroll
-      for (int g = 0; g < KX_GROUPS; ++g) xv[g] = x;
-      if (S3BFS_KX_VEC && P.col_vec && (long long)a0 + KX_GROUPS * 32 <= P.nnz) {
-        // vectorised streaming: lane i loads 16 B at a0 + 4*(i + 32k), i.e. each warp
-        // instruction fetches 512 contiguous bytes of the row; edges outside
-        // [start, row/slice end) are masked.  Next batch starts 16-byte aligned.
-        const int lim_idx = base + bend;
-#pragma unroll
-        for (int k = 0; k < KX_GROUPS / 4; ++k) {
-          const int i0 = a0 + 4 * (lane + 32 * k);
-          int4 q = make_int4(-1, -1, -1, -1);
-          if (i0 < lim_idx) q = ldg_stream4(col + i0, pol_stream);
-          v[4 * k + 0] = (i0 + 0 >= start && i0 + 0 < lim_idx) ? q.x : -1;
-          v[4 * k + 1] = (i0 + 1 >= start && i0 + 1 < lim_idx) ? q.y : -1;
-          v[4 * k + 2] = (i0 + 2 >= start && i0 + 2 < lim_idx) ? q.z : -1;
-          v[4 * k + 3] = (i0 + 3 >= start && i0 + 3 < lim_idx) ? q.w : -1;
-        }
-        e_next = min(bend, a0 + KX_GROUPS * 32 - base);
-      } else {
-#pragma unroll
-        for (int g = 0; g < KX_GROUPS; ++g) {
-          const int my_e = e + g * 32 + lane;
-          v[g] = (my_e < bend) ? ldg_stream(col + base + my_e, pol_stream) : -1;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int g = 0; g < KX_GROUPS; ++g) {
-        const int my_e = e + g * 32 + lane;
-        int j = j0;  // largest window slot with excl <= my_e (>= j0)
-#pragma unroll
-        for (int s = 16; s >= 1; s >>= 1) {
-          const int cj = __shfl_sync(0xffffffffu, wex, min(j + s, 31));
-          if (j + s <= 31 && cj <= my_e) j += s;
-        }
-        xv[g] = __shfl_sync(0xffffffffu, wx, j);
-        const int pos = __shfl_sync(0xffffffffu, wb, j) + my_e;
-        v[g] = (my_e < bend) ? ldg_stream(col + pos, pol_stream) : -1;
-      }
-    }
+    e = map_load(e, v, xv);
     // visited test: the bitmap (visited before this level), branch-free (an invalid slot
-    // probes word 0 and is masked); the claim/discovery code runs only if some lane of the
-    // warp met a vertex not visited at level start -- rare on the heavy levels
+    // probes word 0 and is masked)
     uint32_t needm = 0;
 #pragma unroll
     for (int g = 0; g < KX_GROUPS; ++g) {
@@ -713,13 +609,18 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
                                      : ld_status_u32(bm + (vv >> 5), pol_status);
       if (v[g] >= 0 && !((w >> (vv & 31)) & 1u)) needm |= 1u << g;
     }
-    if (__any_sync(0xffffffffu, needm != 0)) {
+    // claim/discovery only for the groups where some lane met a vertex not visited at level
+    // start (warp-uniform skip: on the heavy levels most batches have one or two such groups)
+    const unsigned wneed = __reduce_or_sync(0xffffffffu, needm);
+    if (wneed) {
       int cl[KX_GROUPS];  // claim tags of the vertices not visited at level start
 #pragma unroll
       for (int g = 0; g < KX_GROUPS; ++g)
-        cl[g] = ((needm >> g) & 1u) ? ld_cg_u8(claim + claim_slot(P, v[g])) : tag;
+        if ((wneed >> g) & 1u)
+          cl[g] = ((needm >> g) & 1u) ? ld_cg_u8(claim + claim_slot(P, v[g])) : tag;
 #pragma unroll
       for (int g = 0; g < KX_GROUPS; ++g) {
+        if (!((wneed >> g) & 1u)) continue;
         const bool disc = cl[g] != tag;
         const unsigned m = __ballot_sync(0xffffffffu, disc);
         if (disc) {
@@ -732,9 +633,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
         wcount += __popc(m);
       }
     }
-    e = e_next;
   }
-#endif
   if (lane == 0) P.wcnt[b * KD_WARPS + warp] = wcount;
 }
 

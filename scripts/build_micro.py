@@ -5,7 +5,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 V = {
-    "base": [], "norank": ["S3BFS_KX_RANK=0"], "pipe2": ["S3BFS_KX_PIPE2=1"], "pipe2g4": ["S3BFS_KX_PIPE2=1", "S3BFS_KX_GROUPS=4"],
+    "base": [], "norank": ["S3BFS_KX_RANK=0"],
     "novec": ["S3BFS_KX_VEC=0"], "vec16": ["S3BFS_KX_GROUPS=16"],
     "nofast": ["S3BFS_KX_FAST=0"], "bmca": ["S3BFS_BM_NC=0"],
     "g4": ["S3BFS_KX_GROUPS=4"],
