@@ -100,7 +100,7 @@ typedef struct {
 /* Create a traversal context over a CSR graph already resident in device memory.
  * row_offsets: device, n+1 int32, BORROWED (caller keeps it alive and unmodified until
  * destroy).  col_indices: device, nnz int32, borrowed (may be NULL iff nnz == 0).
- * Requires 1 <= n, 0 <= nnz <= INT32_MAX - workspace slack.  The handle owns its
+ * Requires 1 <= n <= INT32_MAX - 256, 0 <= nnz <= INT32_MAX - workspace slack.  The handle owns its
  * workspace (per-vertex records, two frontier buffers, candidate buffer, visited bitmap, claim
  * tags, control block, stats) and, unless opts->reorder < 0, a degree-ordered internal copy
  * of the graph (4 nnz + 8 n more bytes), built here on `stream`.

@@ -379,6 +379,8 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   if (!out) return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "out is NULL");
   *out = nullptr;
   if (n <= 0) return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "n must be >= 1");
+  if (n > INT32_MAX - 256)  // internal ids incl. the bitmap sentinel (Params::v_sent) fit int32
+    return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "n out of [1, INT32_MAX - 256]");
   if (nnz < 0 || nnz > INT32_MAX) return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "nnz out of [0, INT32_MAX]");
   if (!row_offsets || (nnz > 0 && !col_indices))
     return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "null graph pointer");
@@ -448,7 +450,7 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   const size_t o_cand = take((size_t)h->cand_cap * 4);
   const size_t o_crd = take((size_t)h->cand_cap * 8);
   const size_t bm_bytes = ((size_t)n + 127) / 128 * 16;  // 16 B padded (vector clears)
-  const size_t o_bm = take(bm_bytes);
+  const size_t o_bm = take(bm_bytes + 16);  // + the sentinel block (Params::v_sent)
   size_t claim_n = 16;  // claim slots: a power of two >= n (claim_slot's hash is mod 2^k)
   while (claim_n < (size_t)n) claim_n <<= 1;
   const size_t o_claim = take(claim_n);
@@ -474,6 +476,7 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   P.cand = (int32_t *)(base + o_cand);
   P.cand_rd = (int2 *)(base + o_crd);
   P.bm = (uint32_t *)(base + o_bm);
+  P.v_sent = (int32_t)(bm_bytes * 8);
   P.claim = (uint8_t *)(base + o_claim);
   P.claim_mask = (uint32_t)(claim_n - 1);
   P.fb[0] = (uint32_t *)(base + o_fb0);

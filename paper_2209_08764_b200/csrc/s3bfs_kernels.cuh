@@ -63,6 +63,9 @@ namespace s3bfs {
 #ifndef S3BFS_BM_AGG
 #define S3BFS_BM_AGG 1  // k_compact: one atomicOr per run of same-word kept candidates
 #endif
+#ifndef S3BFS_COL_HINT
+#define S3BFS_COL_HINT 1  // col loads carry the L2 evict-first policy
+#endif
 #ifndef S3BFS_BM_NC
 #define S3BFS_BM_NC 1     // bitmap probes through the non-coherent (read-only) path
 #endif
@@ -124,7 +127,10 @@ struct Params {
                                     // discoveries), internal row starts, degree scan
   int32_t *cand;                // candidate per slot (k_explore), compacted by k_compact
   int2 *cand_rd;                // (row start, degree) of kept candidates, pass 1 -> pass 2
-  uint32_t *bm;                 // visited bitmap: bit set => visited (exact at level start)
+  uint32_t *bm;                 // visited bitmap: bit set => visited (exact at level start),
+                                //  plus one always-set 16 B sentinel block after the padded end
+  int32_t v_sent;               // sentinel vertex id (first bit of that block): k_explore's
+                                //  masked lanes probe it and need no validity test
   uint8_t *claim;               // per-vertex tag of the level that discovered it (k_explore),
                                 //  at slot claim_slot(v) (scattered, see there)
   uint32_t claim_mask;          // claim array size - 1 (a power of two >= n)
@@ -165,20 +171,28 @@ __device__ __forceinline__ unsigned long long policy_evict_last() {
 // one warp share a boundary line), L2 evict-first
 __device__ __forceinline__ int ldg_stream(const int32_t *p, unsigned long long pol) {
   int v;
-  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+#if S3BFS_COL_HINT
+  asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+#else
+  v = __ldg(p);
+#endif
   return v;
 }
 __device__ __forceinline__ int4 ldg_stream4(const int32_t *p, unsigned long long pol) {
   int4 v;
-  asm volatile("ld.global.nc.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+#if S3BFS_COL_HINT
+  asm("ld.global.nc.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+#else
+  v = __ldg(reinterpret_cast<const int4 *>(p));
+#endif
   return v;
 }
 // the visited bitmap inside k_explore: read-only there (written by earlier kernels only); the
 // hot vertices' words stay L1-resident thanks to the degree order
 __device__ __forceinline__ uint32_t ldg_status_u32(const uint32_t *p, unsigned long long pol) {
   uint32_t v;
-  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
   return v;
 }
 __device__ __forceinline__ uint32_t ld_status_u32(const uint32_t *p, unsigned long long pol) {
@@ -413,8 +427,8 @@ __global__ void k_init(Params P, int32_t s, int32_t *level, int32_t *parent) {
   const long long gstride = (long long)gridDim.x * blockDim.x;
   const int si = P.o2n ? __ldg(P.o2n + s) : s;  // the source's internal id
   const long long nw4 = ((long long)n + 127) >> 7;  // bitmap as uint4 (16 B padded)
-  for (long long i = gtid; i < nw4; i += gstride) {
-    uint4 w = make_uint4(0, 0, 0, 0);
+  for (long long i = gtid; i <= nw4; i += gstride) {  // block nw4: the all-ones sentinel
+    uint4 w = i == nw4 ? make_uint4(~0u, ~0u, ~0u, ~0u) : make_uint4(0, 0, 0, 0);
     if (i == (si >> 7)) (&w.x)[(si >> 5) & 3] = 1u << (si & 31);
     reinterpret_cast<uint4 *>(P.bm)[i] = w;
   }
@@ -484,6 +498,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   int32_t *__restrict__ cand = P.cand;
   const uint32_t *__restrict__ bm = P.bm;
   uint8_t *__restrict__ claim = P.claim;
+  const int vs = P.v_sent;  // masked lanes' target: its visited bit is always set
 
   if (tid == 0) {
     P.status[b] = 0ull;  // reset k_compact's look-back word for this level
@@ -547,17 +562,17 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
           const int i0 = a0 + 4 * (lane + 32 * k);
           int4 q = make_int4(-1, -1, -1, -1);
           if (i0 < lim_idx) q = ldg_stream4(col + i0, pol_stream);
-          v[4 * k + 0] = (i0 + 0 >= start && i0 + 0 < lim_idx) ? q.x : -1;
-          v[4 * k + 1] = (i0 + 1 >= start && i0 + 1 < lim_idx) ? q.y : -1;
-          v[4 * k + 2] = (i0 + 2 >= start && i0 + 2 < lim_idx) ? q.z : -1;
-          v[4 * k + 3] = (i0 + 3 >= start && i0 + 3 < lim_idx) ? q.w : -1;
+          v[4 * k + 0] = (i0 + 0 >= start && i0 + 0 < lim_idx) ? q.x : vs;
+          v[4 * k + 1] = (i0 + 1 >= start && i0 + 1 < lim_idx) ? q.y : vs;
+          v[4 * k + 2] = (i0 + 2 >= start && i0 + 2 < lim_idx) ? q.z : vs;
+          v[4 * k + 3] = (i0 + 3 >= start && i0 + 3 < lim_idx) ? q.w : vs;
         }
         e_next = min(bend, a0 + KX_GROUPS * 32 - base);
       } else {
 #pragma unroll
         for (int g = 0; g < KX_GROUPS; ++g) {
           const int my_e = e + g * 32 + lane;
-          v[g] = (my_e < bend) ? ldg_stream(col + base + my_e, pol_stream) : -1;
+          v[g] = (my_e < bend) ? ldg_stream(col + base + my_e, pol_stream) : vs;
         }
       }
     } else if (S3BFS_KX_RANK && !wzero) {
@@ -565,18 +580,21 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
       // for group g (edges eg .. eg+31) the row starts strictly inside the group form a
       // 32-bit mask (one REDUX), and lane i's row is the group's first row plus the number
       // of row starts at or below edge eg+i (exact while no row of the window is empty)
-      const unsigned le = (2u << lane) - 2u;  // bits 1 .. lane
-      int r = j0;  // row of the group's first edge
+      // (row starts in [eg, eg+31] -> mask bit rel; r = row of edge eg-1, so lane i's row is
+      // r + popc(mask & bits 0..i); the batch's first edge lies in row j0)
+      const unsigned le = 0xffffffffu >> (31 - lane);  // bits 0 .. lane
+      int r = j0;
 #pragma unroll
       for (int g = 0; g < KX_GROUPS; ++g) {
         const int eg = e + g * 32;
         const int rel = wex - eg;  // this window lane's row start relative to the group
-        const unsigned m = __reduce_or_sync(0xffffffffu, ((unsigned)(rel - 1) < 31u) ? (1u << rel) : 0u);
+        const unsigned m = __reduce_or_sync(0xffffffffu, ((unsigned)rel < 32u) ? (1u << rel) : 0u);
+        if (g == 0) r -= (int)(m & 1u);  // a row starting exactly at e is row j0 itself
         const int j = r + __popc(m & le);
         xv[g] = __shfl_sync(0xffffffffu, wx, j);
         const int pos = __shfl_sync(0xffffffffu, wb, j) + eg + lane;
-        v[g] = (eg + lane < bend) ? ldg_stream(col + pos, pol_stream) : -1;
-        r += __popc(m) + (__any_sync(0xffffffffu, rel == 32) ? 1 : 0);
+        v[g] = (eg + lane < bend) ? ldg_stream(col + pos, pol_stream) : vs;
+        r += __popc(m);
       }
     } else {
 #pragma unroll
@@ -590,7 +608,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
         }
         xv[g] = __shfl_sync(0xffffffffu, wx, j);
         const int pos = __shfl_sync(0xffffffffu, wb, j) + my_e;
-        v[g] = (my_e < bend) ? ldg_stream(col + pos, pol_stream) : -1;
+        v[g] = (my_e < bend) ? ldg_stream(col + pos, pol_stream) : vs;
       }
     }
     return e_next;
@@ -599,15 +617,14 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   while (e < e_end) {
     int v[KX_GROUPS], xv[KX_GROUPS];
     e = map_load(e, v, xv);
-    // visited test: the bitmap (visited before this level), branch-free (an invalid slot
-    // probes word 0 and is masked)
+    // visited test: the bitmap (visited before this level), branch-free (a masked slot
+    // probes the always-set sentinel bit)
     uint32_t needm = 0;
 #pragma unroll
     for (int g = 0; g < KX_GROUPS; ++g) {
-      const int vv = max(v[g], 0);
-      const uint32_t w = S3BFS_BM_NC ? ldg_status_u32(bm + (vv >> 5), pol_status)
-                                     : ld_status_u32(bm + (vv >> 5), pol_status);
-      if (v[g] >= 0 && !((w >> (vv & 31)) & 1u)) needm |= 1u << g;
+      const uint32_t w = S3BFS_BM_NC ? ldg_status_u32(bm + (v[g] >> 5), pol_status)
+                                     : ld_status_u32(bm + (v[g] >> 5), pol_status);
+      needm |= ((~w >> (v[g] & 31)) & 1u) << g;
     }
     // claim/discovery only for the groups where some lane met a vertex not visited at level
     // start (warp-uniform skip: on the heavy levels most batches have one or two such groups)

@@ -20,7 +20,7 @@ extern "C" int kx_micro(const int32_t *col, int n, int n_l, int e_l, int32_t *f,
   Params P{};
   P.col = col; P.vinfo = vinfo; P.lp = lp; P.n = n; P.ctl = ctl;
   P.f[0] = P.f[1] = f; P.frs[0] = P.frs[1] = frs; P.fex[0] = P.fex[1] = fex;
-  P.cand = cand; P.bm = bm; P.claim = claim; P.wcnt = wcnt; P.status = status;
+  P.cand = cand; P.bm = bm; P.v_sent = (int)(((size_t)n + 127) / 128 * 128); P.claim = claim; P.wcnt = wcnt; P.status = status;
   size_t claim_n = 16;  // as s3bfs_create: a power of two >= n (kx_micro.py allocates it)
   while (claim_n < (size_t)n) claim_n <<= 1;
   P.claim_mask = (uint32_t)(claim_n - 1);

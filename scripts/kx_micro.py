@@ -63,6 +63,7 @@ for l, fr, e_l in levels:
     bits[:n] = visited.to(torch.int64)
     w = (bits.view(-1, 32) << torch.arange(32, device=dev, dtype=torch.int64)).sum(1)
     bm = w.to(torch.int64).to(torch.int32)  # two's complement view of the u32 words
+    bm = torch.cat([bm, torch.full((4,), -1, dtype=torch.int32, device=dev)])  # sentinel block
     for order in ("discovery", "sorted"):
         f = fr if order == "sorted" else fr[torch.randperm(fr.numel(), device=dev)]
         f = f.contiguous()
