@@ -542,6 +542,16 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
     s3bfs_status ts = build_in_adjacency(h, stream);
     if (ts != S3BFS_OK) return bail(ts);
   }
+  {  // L2 policy descriptors (uniform kernel parameters of k_explore)
+    unsigned long long *d_pol = nullptr, h_pol[2] = {0, 0};
+    if ((e = cudaMallocAsync((void **)&d_pol, 16, stream)) != cudaSuccess) return bail(cuda_fail(h, e, "cudaMallocAsync"));
+    k_policies<<<1, 1, 0, stream>>>(d_pol);
+    cudaMemcpyAsync(h_pol, d_pol, 16, cudaMemcpyDeviceToHost, stream);
+    cudaFreeAsync(d_pol, stream);
+    if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) return bail(cuda_fail(h, e, "k_policies"));
+    P.pol_first = h_pol[0];
+    P.pol_last = h_pol[1];
+  }
   if ((e = cudaMemsetAsync(P.ctl, 0, sizeof(Ctl), stream)) != cudaSuccess) return bail(cuda_fail(h, e, "memset(ctl)"));
   if ((e = cudaMemsetAsync(P.status, 0, (size_t)p_max * 8, stream)) != cudaSuccess) return bail(cuda_fail(h, e, "memset(status)"));
   if (h->opt.debug_poison) {

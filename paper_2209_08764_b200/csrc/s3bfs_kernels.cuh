@@ -129,6 +129,9 @@ struct Params {
   int2 *cand_rd;                // (row start, degree) of kept candidates, pass 1 -> pass 2
   uint32_t *bm;                 // visited bitmap: bit set => visited (exact at level start),
                                 //  plus one always-set 16 B sentinel block after the padded end
+  unsigned long long pol_first, pol_last;  // L2 createpolicy descriptors (evict-first for the
+                                //  col stream, evict-last for the bitmap), made once at create:
+                                //  as kernel parameters they are uniform (no per-load R2UR)
   int32_t v_sent;               // sentinel vertex id (first bit of that block): k_explore's
                                 //  masked lanes probe it and need no validity test
   uint8_t *claim;               // per-vertex tag of the level that discovered it (k_explore),
@@ -187,6 +190,12 @@ __device__ __forceinline__ int4 ldg_stream4(const int32_t *p, unsigned long long
   v = __ldg(reinterpret_cast<const int4 *>(p));
 #endif
   return v;
+}
+// rotate right by (k mod 32): bit 0 of the result is bit (k mod 32) of w (one SHF.WRAP)
+__device__ __forceinline__ uint32_t rotr32(uint32_t w, int k) {
+  uint32_t r;
+  asm("shf.r.wrap.b32 %0, %1, %1, %2;" : "=r"(r) : "r"(w), "r"(k));
+  return r;
 }
 // the visited bitmap inside k_explore: read-only there (written by earlier kernels only); the
 // hot vertices' words stay L1-resident thanks to the degree order
@@ -462,6 +471,12 @@ __global__ void k_init(Params P, int32_t s, int32_t *level, int32_t *parent) {
   }
 }
 
+// create time: the two L2 cache-policy descriptors k_explore passes with its loads
+__global__ void k_policies(unsigned long long *out) {
+  out[0] = policy_evict_first();
+  out[1] = policy_evict_last();
+}
+
 // ---- (c)+(d): k_explore ----------------------------------------------------------------------
 // CTA b < P_l owns global edges [b*chunk, min((b+1)*chunk, e_l)) of the level, split evenly
 // over its warps: each warp is one of the paper's workers with an (almost) equal share of the
@@ -509,8 +524,8 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   const int e_begin = min(E0 + warp * wcap, E1);
   const int e_end = min(e_begin + wcap, E1);
   const int segbase = (b * KD_WARPS + warp) * wcap;
-  const unsigned long long pol_stream = policy_evict_first();
-  const unsigned long long pol_status = policy_evict_last();
+  const unsigned long long pol_stream = P.pol_first;
+  const unsigned long long pol_status = P.pol_last;
   int wcount = 0;
   int u0 = 0, wex = 0, wx = 0, wb = 0, lim = 0;
   bool wzero = false;  // the window holds an empty row (two equal row starts)
@@ -536,12 +551,9 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
       load_window(u0);
     }
     const int bend = min(e_end, lim);
-    int j0 = 0;  // window slot of the batch's first edge (warp-uniform)
-#pragma unroll
-    for (int s = 16; s >= 1; s >>= 1) {
-      const int cj = __shfl_sync(0xffffffffu, wex, j0 + s);
-      if (cj <= e) j0 += s;
-    }
+    // window slot of the batch's first edge (warp-uniform): the window's row starts are
+    // non-decreasing and wex_0 <= e, so it is the count of row starts <= e, minus one
+    const int j0 = __popc(__ballot_sync(0xffffffffu, wex <= e)) - 1;
     const int row_end = (j0 < 31) ? __shfl_sync(0xffffffffu, wex, min(j0 + 1, 31)) : lim;
     int e_next = min(e + KX_GROUPS * 32, bend);
     if (S3BFS_KX_FAST && row_end >= e_next) {
@@ -557,22 +569,34 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
         // instruction fetches 512 contiguous bytes of the row; edges outside
         // [start, row/slice end) are masked.  Next batch starts 16-byte aligned.
         const int lim_idx = base + bend;
+        if (a0 == start && a0 + KX_GROUPS * 32 <= lim_idx) {
+          // interior batch (aligned, whole): no masking
 #pragma unroll
-        for (int k = 0; k < KX_GROUPS / 4; ++k) {
-          const int i0 = a0 + 4 * (lane + 32 * k);
-          int4 q = make_int4(-1, -1, -1, -1);
-          if (i0 < lim_idx) q = ldg_stream4(col + i0, pol_stream);
-          v[4 * k + 0] = (i0 + 0 >= start && i0 + 0 < lim_idx) ? q.x : vs;
-          v[4 * k + 1] = (i0 + 1 >= start && i0 + 1 < lim_idx) ? q.y : vs;
-          v[4 * k + 2] = (i0 + 2 >= start && i0 + 2 < lim_idx) ? q.z : vs;
-          v[4 * k + 3] = (i0 + 3 >= start && i0 + 3 < lim_idx) ? q.w : vs;
+          for (int k = 0; k < KX_GROUPS / 4; ++k) {
+            const int4 q = ldg_stream4(col + a0 + 4 * (lane + 32 * k), pol_stream);
+            v[4 * k + 0] = q.x;
+            v[4 * k + 1] = q.y;
+            v[4 * k + 2] = q.z;
+            v[4 * k + 3] = q.w;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < KX_GROUPS / 4; ++k) {
+            const int i0 = a0 + 4 * (lane + 32 * k);
+            const int4 q = ldg_stream4(col + i0, pol_stream);  // in bounds: a0 + 256 <= nnz
+            v[4 * k + 0] = (i0 + 0 >= start && i0 + 0 < lim_idx) ? q.x : vs;
+            v[4 * k + 1] = (i0 + 1 >= start && i0 + 1 < lim_idx) ? q.y : vs;
+            v[4 * k + 2] = (i0 + 2 >= start && i0 + 2 < lim_idx) ? q.z : vs;
+            v[4 * k + 3] = (i0 + 3 >= start && i0 + 3 < lim_idx) ? q.w : vs;
+          }
         }
         e_next = min(bend, a0 + KX_GROUPS * 32 - base);
       } else {
 #pragma unroll
-        for (int g = 0; g < KX_GROUPS; ++g) {
+        for (int g = 0; g < KX_GROUPS; ++g) {  // masked lanes re-load the batch's first edge
           const int my_e = e + g * 32 + lane;
-          v[g] = (my_e < bend) ? ldg_stream(col + base + my_e, pol_stream) : vs;
+          const int t = ldg_stream(col + base + (my_e < bend ? my_e : e), pol_stream);
+          v[g] = (my_e < bend) ? t : vs;
         }
       }
     } else if (S3BFS_KX_RANK && !wzero) {
@@ -583,6 +607,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
       // (row starts in [eg, eg+31] -> mask bit rel; r = row of edge eg-1, so lane i's row is
       // r + popc(mask & bits 0..i); the batch's first edge lies in row j0)
       const unsigned le = 0xffffffffu >> (31 - lane);  // bits 0 .. lane
+      const int pfirst = __shfl_sync(0xffffffffu, wb, j0) + e;  // col index of edge e (valid)
       int r = j0;
 #pragma unroll
       for (int g = 0; g < KX_GROUPS; ++g) {
@@ -593,7 +618,9 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
         const int j = r + __popc(m & le);
         xv[g] = __shfl_sync(0xffffffffu, wx, j);
         const int pos = __shfl_sync(0xffffffffu, wb, j) + eg + lane;
-        v[g] = (eg + lane < bend) ? ldg_stream(col + pos, pol_stream) : vs;
+        const bool ok = eg + lane < bend;
+        const int t = ldg_stream(col + (ok ? pos : pfirst), pol_stream);  // unconditional
+        v[g] = ok ? t : vs;
         r += __popc(m);
       }
     } else {
@@ -608,7 +635,9 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
         }
         xv[g] = __shfl_sync(0xffffffffu, wx, j);
         const int pos = __shfl_sync(0xffffffffu, wb, j) + my_e;
-        v[g] = (my_e < bend) ? ldg_stream(col + pos, pol_stream) : vs;
+        const int pf = __shfl_sync(0xffffffffu, wb, j0) + e;
+        const int t = ldg_stream(col + (my_e < bend ? pos : pf), pol_stream);
+        v[g] = (my_e < bend) ? t : vs;
       }
     }
     return e_next;
@@ -624,7 +653,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
     for (int g = 0; g < KX_GROUPS; ++g) {
       const uint32_t w = S3BFS_BM_NC ? ldg_status_u32(bm + (v[g] >> 5), pol_status)
                                      : ld_status_u32(bm + (v[g] >> 5), pol_status);
-      needm |= ((~w >> (v[g] & 31)) & 1u) << g;
+      needm |= (~rotr32(w, v[g]) & 1u) << g;  // bit (v mod 32) of w, inverted
     }
     // claim/discovery only for the groups where some lane met a vertex not visited at level
     // start (warp-uniform skip: on the heavy levels most batches have one or two such groups)

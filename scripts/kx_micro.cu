@@ -24,6 +24,15 @@ extern "C" int kx_micro(const int32_t *col, int n, int n_l, int e_l, int32_t *f,
   size_t claim_n = 16;  // as s3bfs_create: a power of two >= n (kx_micro.py allocates it)
   while (claim_n < (size_t)n) claim_n <<= 1;
   P.claim_mask = (uint32_t)(claim_n - 1);
+  {
+    unsigned long long *d_pol = nullptr, h_pol[2];
+    cudaMalloc(&d_pol, 16);
+    k_policies<<<1, 1>>>(d_pol);
+    cudaMemcpy(h_pol, d_pol, 16, cudaMemcpyDeviceToHost);
+    cudaFree(d_pol);
+    P.pol_first = h_pol[0];
+    P.pol_last = h_pol[1];
+  }
   P.p_max = p_max; P.grain = grain; P.t0 = -1;
   P.nnz = 0x7fffffff;  // harness: col has 4 KB of padding (see kx_micro.py)
   P.col_vec = (((uintptr_t)col) & 15) == 0;
