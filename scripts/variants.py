@@ -1,7 +1,8 @@
 """Experiment driver (not a benchmark): time design variants of libs3bfs.so on one graph.
 usage: python scripts/variants.py CONFIG NSRC tag=path.so [tag=path.so ...]
 Each variant x option set: 1 warm-up + 3 timed traversals per source (CUDA events, graph mode);
-prints the median per source and the per-level explore/compact split of the last run."""
+prints the median per source and the per-level explore/compact split of the last run.
+ROUNDS=R repeats the interleaved pass (variants alternate per source) R times."""
 import ctypes
 import json
 import os
@@ -27,6 +28,8 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 st = torch.cuda.current_stream()
 vp = ctypes.c_void_p
 results = {}
+ROUNDS = int(os.environ.get("ROUNDS", "1"))
+handles = []  # (key, lib, handle): every variant is created up front, then runs interleave
 for tag, path in variants:
     lib = ctypes.CDLL(os.path.abspath(path))
     lib.s3bfs_create.argtypes = [ctypes.POINTER(vp), ctypes.c_int32, ctypes.c_int64, vp, vp,
@@ -41,37 +44,42 @@ for tag, path in variants:
         rc = lib.s3bfs_create(ctypes.byref(h), g.n, g.nnz, ro.data_ptr(), col.data_ptr(),
                               ctypes.byref(o), st.cuda_stream)
         assert rc == 0, rc
-        tot_ms, tot_e = 0.0, 0
-        per = []
-        for s in g.sources[:nsrc]:
-            times = []
-            for rep in range(4):
+        handles.append((f"{tag}/{oname}", lib, h))
+srcs = list(g.sources[:nsrc])
+times = {k: {s: [] for s in srcs} for k, _, _ in handles}
+levels = {k: {} for k, _, _ in handles}
+edges = {}
+for rnd in range(ROUNDS):
+    for s in srcs:
+        for key, lib, h in handles:  # interleaved: clock drift hits every variant alike
+            for rep in range(4 if rnd == 0 else 3):
                 flush.fill_(rep)
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(st)
                 assert lib.s3bfs_run(h, s, level.data_ptr(), parent.data_ptr(), st.cuda_stream) == 0
                 b.record(st)
                 b.synchronize()
-                if rep:
-                    times.append(a.elapsed_time(b))
-            ms = float(np.median(times))
-            m_c = int(deg[level >= 0].sum().item())
+                if rep or rnd:
+                    times[key][s].append(a.elapsed_time(b))
+            if s not in edges:
+                edges[s] = int(deg[level >= 0].sum().item()) // 2
             buf = (LevelStat * 256)()
             num = ctypes.c_int32()
             lib.s3bfs_get_level_stats(h, buf, 256, ctypes.byref(num))
-            lv = [(r.level, r.e_l, r.tier, (r.t_explore_end_ns - r.t_explore_begin_ns) / 1e3,
-                   (r.t_end_ns - r.t_explore_end_ns) / 1e3 if r.tier == 1 else 0.0,
-                   r.candidates, r.kept) for r in buf[: min(num.value, 256)]]
-            per.append({"src": s, "ms": ms, "gteps": m_c / 2 / ms / 1e6,
-                        "heavy": [x for x in lv if x[1] > 1_000_000]})
-            tot_ms += ms
-            tot_e += m_c // 2
-        lib.s3bfs_destroy(h)
-        key = f"{tag}/{oname}"
-        results[key] = {"gteps": tot_e / tot_ms / 1e6, "per": per}
-        print(f"{key:32s} GTEPS {tot_e / tot_ms / 1e6:7.2f}  ms/src " +
-              " ".join(f"{p['ms']:.3f}" for p in per), flush=True)
-        for p in per[:2]:
-            print("    src", p["src"], " ".join(f"[e={x[1]/1e6:.1f}M kx={x[3]:.0f} kc={x[4]:.0f} c={x[5]/1e6:.2f}M k={x[6]/1e6:.2f}M]"
-                                               for x in p["heavy"]), flush=True)
+            levels[key][s] = [(r.level, r.e_l, r.tier, (r.t_explore_end_ns - r.t_explore_begin_ns) / 1e3,
+                               (r.t_end_ns - r.t_explore_end_ns) / 1e3 if r.tier == 1 else 0.0,
+                               r.candidates, r.kept) for r in buf[: min(num.value, 256)]]
+for key, lib, h in handles:
+    lib.s3bfs_destroy(h)
+    per = [{"src": s, "ms": float(np.median(times[key][s])), "gteps": edges[s] / float(np.median(times[key][s])) / 1e6,
+            "heavy": [x for x in levels[key][s] if x[1] > 1_000_000]} for s in srcs]
+    tot_ms = sum(p["ms"] for p in per)
+    tot_e = sum(edges[s] for s in srcs)
+    results[key] = {"gteps": tot_e / tot_ms / 1e6, "per": per}
+    print(f"{key:32s} GTEPS {tot_e / tot_ms / 1e6:7.2f}  ms/src " +
+          " ".join(f"{p['ms']:.3f}" for p in per), flush=True)
+    worst = max(per, key=lambda p: p["ms"])
+    for p in per[:2] + ([worst] if worst not in per[:2] else []):
+        print("    src", p["src"], " ".join(f"[e={x[1]/1e6:.1f}M kx={x[3]:.0f} kc={x[4]:.0f} c={x[5]/1e6:.2f}M k={x[6]/1e6:.2f}M]"
+                                           for x in p["heavy"]), flush=True)
 json.dump(results, open(os.environ.get("VARIANT_OUT", "gpurun_out/variants.json"), "w"))
