@@ -80,7 +80,13 @@ typedef struct {
                               top-down when n_l * beta < n (Beamer); 0 = top-down S3BFS only */
   int32_t do_alpha;        /* 0 -> 14 */
   int32_t do_beta;         /* 0 -> 24; < 0 -> never switch back */
-  int32_t reserved[3];
+  int32_t dist_size;       /* NEXT-4: 0/1 single GPU; G > 1: this handle is rank dist_rank of
+                              G ranks that each hold the whole graph and explore 1/G of every
+                              level's edges (replicated-graph split); driven by
+                              the s3bfs_dist_* calls below, not s3bfs_run.  Needs loop_mode 2
+                              semantics (set implicitly), tier 0 off (implicit), direction 0 */
+  int32_t dist_rank;       /* NEXT-4: 0 <= dist_rank < dist_size */
+  int32_t reserved[1];
 } s3bfs_options;
 
 /* One record per BFS level (the SPEC LevelStats analogue).  n_l = |frontier|
@@ -154,6 +160,43 @@ s3bfs_status s3bfs_get_kernel_times(s3bfs_handle h, s3bfs_kernel_times *out);
 /* Test-only: %globaltimer stamps of the last run's first level (ns): out[0] k_init start,
  * out[1] first k_dispatch, out[2] k_small start (0 when not reached).  Synchronises. */
 s3bfs_status s3bfs_debug_timeline(s3bfs_handle h, uint64_t out[4]);
+
+/* ---- NEXT-4: one traversal over G ranks (replicated graph) -------------------
+ * Every rank holds the same frontier; rank r explores the level's global edges
+ * [r*e_l/G, (r+1)*e_l/G) with the single-GPU kernels (c)(d), deduplicates its discoveries by
+ * Owner (e), and leaves its kept vertices as records {internal id, parent (caller id), row
+ * start, degree}.  The caller all-gathers the records (the exchange step, e.g. NCCL over
+ * NVLink; plumbing outside the library) and hands them to s3bfs_dist_merge, which keeps every
+ * vertex once (from the lowest rank that kept it) and builds the identical next frontier on
+ * every rank.  Per traversal:
+ *   s3bfs_dist_begin; loop { s3bfs_dist_expand -> done? ; all-gather ; s3bfs_dist_merge };
+ *   s3bfs_dist_end.
+ * All calls need a handle created with dist_size > 1 (else UNSUPPORTED). */
+
+/* Start a traversal from `source` (same on every rank); level/parent as in s3bfs_run
+ * (written by s3bfs_dist_end).  Enqueued on `stream`. */
+s3bfs_status s3bfs_dist_begin(s3bfs_handle h, int32_t source, int32_t *level, int32_t *parent,
+                              s3bfs_stream_t stream);
+
+/* Expand this rank's slice of the current level.  Synchronises `stream`.  *done = 1 when the
+ * traversal has no further level (then *n_local = 0 and nothing ran); otherwise *n_local =
+ * this rank's record count, readable through s3bfs_dist_records. */
+s3bfs_status s3bfs_dist_expand(s3bfs_handle h, s3bfs_stream_t stream, int32_t *n_local,
+                               int32_t *done);
+
+/* Copy this rank's first `count` records (count <= the last *n_local) into dst: device,
+ * int32 x 4 per record, caller-owned (e.g. the padded send buffer of the all-gather).
+ * Enqueued on `stream`. */
+s3bfs_status s3bfs_dist_records(s3bfs_handle h, void *dst, int32_t count, s3bfs_stream_t stream);
+
+/* Merge the all-gathered records: all = device int32 x 4 [G * stride], rank r's n_r records at
+ * [r * stride, r * stride + n_r); counts = HOST int32[G] (n_r <= stride).  Advances the level.
+ * Enqueued on `stream` (counts are copied before return). */
+s3bfs_status s3bfs_dist_merge(s3bfs_handle h, const void *all, const int32_t *counts,
+                              int32_t stride, s3bfs_stream_t stream);
+
+/* Write level/parent (caller ids) for the traversal begun by s3bfs_dist_begin. */
+s3bfs_status s3bfs_dist_end(s3bfs_handle h, s3bfs_stream_t stream);
 
 /* ---- test-only entry points (same kernels the traversal uses) ------------------------ */
 

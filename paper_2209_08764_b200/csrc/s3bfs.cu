@@ -65,6 +65,7 @@ struct s3bfs_ctx {
   bool time_kernels = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   s3bfs_kernel_times kt{};
+  int32_t *d_counts = nullptr;  // NEXT-4: per-rank record counts (device copy)
   std::string err;
 };
 
@@ -433,6 +434,16 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   if (t0 > KS_ECAP) t0 = KS_ECAP;
   if (h->opt.variant == 1) t0 = -1;
   h->loop_graph = h->opt.loop_mode == 2 ? 0 : 1;
+  const int dist_size = h->opt.dist_size > 1 ? h->opt.dist_size : 1;
+  const int dist_rank = dist_size > 1 ? h->opt.dist_rank : 0;
+  if (dist_size > 1) {  // NEXT-4: host-driven per-level protocol, every level on tier 1
+    if (dist_rank < 0 || dist_rank >= dist_size)
+      return bail(fail(h, S3BFS_ERR_INVALID_ARGUMENT, "dist_rank not in [0, dist_size)"));
+    if (h->opt.direction == 1)
+      return bail(fail(h, S3BFS_ERR_UNSUPPORTED, "dist_size > 1 with direction = 1"));
+    h->loop_graph = 0;
+    t0 = -1;
+  }
   const int collect = h->opt.collect_stats >= 0 ? 1 : 0;
 
   // ---- workspace (one allocation) ----
@@ -459,6 +470,12 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   const size_t o_status = take((size_t)p_max * 8);
   const size_t o_ctl = take(sizeof(Ctl));
   const size_t o_stats = take((size_t)stats_cap * sizeof(s3bfs_level_stat));
+  // NEXT-4 (dist_size > 1 only): records, per-vertex lowest keeping rank, merge look-back
+  const long long m_tiles = dist_size > 1 ? ((long long)dist_size * n + MG_TILE - 1) / MG_TILE + 1 : 0;
+  const size_t o_rec = take(dist_size > 1 ? (size_t)n * 16 : 0);
+  const size_t o_minrank = take(dist_size > 1 ? (size_t)n * 4 : 0);
+  const size_t o_mstatus = take((size_t)m_tiles * 8);
+  const size_t o_dcounts = take((size_t)dist_size * 4);
   h->ws_bytes = off;
   if ((e = cudaMalloc(&h->ws, h->ws_bytes)) != cudaSuccess) return bail(cuda_fail(h, e, "cudaMalloc(workspace)"));
   char *base = (char *)h->ws;
@@ -498,6 +515,14 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   P.do_beta = h->opt.do_beta != 0 ? h->opt.do_beta : 24;
   P.n_scan = n;
   P.nnz = nnz;
+  P.dist_size = dist_size;
+  P.dist_rank = dist_rank;
+  P.rec = dist_size > 1 ? (int4 *)(base + o_rec) : nullptr;
+  P.minrank = dist_size > 1 ? (int32_t *)(base + o_minrank) : nullptr;
+  P.m_status = dist_size > 1 ? (unsigned long long *)(base + o_mstatus) : nullptr;
+  h->d_counts = (int32_t *)(base + o_dcounts);
+  if (dist_size > 1 && (e = cudaMemsetAsync(P.minrank, 0x7f, (size_t)n * 4, stream)) != cudaSuccess)
+    return bail(cuda_fail(h, e, "memset(minrank)"));
   if (share) {  // a clone: the prepared graph is the source handle's; vertex records copied
     P.col = share->P.col;
     P.n2o = share->P.n2o;
@@ -602,6 +627,8 @@ s3bfs_status s3bfs_run(s3bfs_handle h, int32_t source, int32_t *level, int32_t *
   if (!level || !parent) return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "level/parent is NULL");
   if (!is_device_ptr(level) || !is_device_ptr(parent))
     return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "level/parent must be device memory");
+  if (h->P.dist_size > 1)
+    return fail(h, S3BFS_ERR_UNSUPPORTED, "a dist_size > 1 handle is driven by s3bfs_dist_*");
   cudaStream_t stream = (cudaStream_t)stream_;
   h->last_stream = stream;
   h->ran = true;
@@ -668,6 +695,87 @@ s3bfs_status s3bfs_run(s3bfs_handle h, int32_t source, int32_t *level, int32_t *
     CK(h, cudaGetLastError());
     if (h->time_kernels) pending = c.tier;
   }
+  return S3BFS_OK;
+}
+
+// ---- NEXT-4: the per-level protocol over G ranks (include/s3bfs.h) ----------------------------
+s3bfs_status s3bfs_dist_begin(s3bfs_handle h, int32_t source, int32_t *level, int32_t *parent,
+                              s3bfs_stream_t stream_) {
+  if (!h) return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "handle is NULL");
+  if (h->P.dist_size <= 1) return fail(h, S3BFS_ERR_UNSUPPORTED, "handle has dist_size <= 1");
+  if (source < 0 || source >= h->n)
+    return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "source " + std::to_string(source) + " not in [0, n)");
+  if (!level || !parent || !is_device_ptr(level) || !is_device_ptr(parent))
+    return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "level/parent must be device memory");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  h->last_stream = stream;
+  h->ran = true;
+  k_init<<<init_grid(h), 256, 0, stream>>>(h->P, source, level, parent);
+  CK(h, cudaGetLastError());
+  return S3BFS_OK;
+}
+
+s3bfs_status s3bfs_dist_expand(s3bfs_handle h, s3bfs_stream_t stream_, int32_t *n_local,
+                               int32_t *done) {
+  if (!h || !n_local || !done) return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "null argument");
+  if (h->P.dist_size <= 1) return fail(h, S3BFS_ERR_UNSUPPORTED, "handle has dist_size <= 1");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (!h->h_ctl) CK(h, cudaMallocHost((void **)&h->h_ctl, sizeof(Ctl)));
+  CK(h, cudaMemcpyAsync(h->h_ctl, h->P.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, stream));
+  CK(h, cudaStreamSynchronize(stream));
+  const Ctl c = *h->h_ctl;
+  *n_local = 0;
+  *done = c.tier == TIER_DONE ? 1 : 0;
+  if (*done) return S3BFS_OK;
+  k_explore<<<c.p_l, KD_THREADS, 0, stream>>>(h->P);
+  k_compact<<<c.p_l, KD_THREADS, 0, stream>>>(h->P);
+  CK(h, cudaGetLastError());
+  CK(h, cudaMemcpyAsync(h->h_ctl, h->P.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, stream));
+  CK(h, cudaStreamSynchronize(stream));
+  *n_local = h->h_ctl->n_next;
+  return S3BFS_OK;
+}
+
+s3bfs_status s3bfs_dist_records(s3bfs_handle h, void *dst, int32_t count, s3bfs_stream_t stream) {
+  if (!h) return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "handle is NULL");
+  if (h->P.dist_size <= 1) return fail(h, S3BFS_ERR_UNSUPPORTED, "handle has dist_size <= 1");
+  if (count < 0 || count > h->n) return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "count out of [0, n]");
+  if (count == 0) return S3BFS_OK;
+  if (!dst || !is_device_ptr(dst)) return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "dst must be device memory");
+  CK(h, cudaMemcpyAsync(dst, h->P.rec, (size_t)count * 16, cudaMemcpyDeviceToDevice,
+                        (cudaStream_t)stream));
+  return S3BFS_OK;
+}
+
+s3bfs_status s3bfs_dist_merge(s3bfs_handle h, const void *all, const int32_t *counts,
+                              int32_t stride, s3bfs_stream_t stream_) {
+  if (!h || !counts || stride < 0) return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "bad argument");
+  const int G = h->P.dist_size;
+  if (G <= 1) return fail(h, S3BFS_ERR_UNSUPPORTED, "handle has dist_size <= 1");
+  for (int r = 0; r < G; ++r)
+    if (counts[r] < 0 || counts[r] > stride || counts[r] > h->n)
+      return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "record count out of [0, stride]");
+  if (stride > 0 && (!all || !is_device_ptr(all)))
+    return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "records must be device memory");
+  if ((long long)G * stride > (long long)G * h->n)
+    return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "stride > n");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  CK(h, cudaMemcpyAsync(h->d_counts, counts, (size_t)G * 4, cudaMemcpyHostToDevice, stream));
+  long long tiles = ((long long)G * stride + MG_TILE - 1) / MG_TILE;
+  if (tiles < 1) tiles = 1;
+  const int4 *a = (const int4 *)all;
+  k_merge_min<<<h->num_sms * 8, 256, 0, stream>>>(h->P, a, h->d_counts, stride, (int32_t)tiles);
+  k_merge_keep<<<(unsigned)tiles, KD_THREADS, 0, stream>>>(h->P, a, h->d_counts, stride, (int32_t)tiles);
+  CK(h, cudaGetLastError());
+  CK(h, cudaStreamSynchronize(stream));  // counts is the caller's host buffer
+  return S3BFS_OK;
+}
+
+s3bfs_status s3bfs_dist_end(s3bfs_handle h, s3bfs_stream_t stream_) {
+  if (!h) return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "handle is NULL");
+  if (h->P.dist_size <= 1) return fail(h, S3BFS_ERR_UNSUPPORTED, "handle has dist_size <= 1");
+  k_finalize<<<finalize_grid(h), 256, 0, (cudaStream_t)stream_>>>(h->P);
+  CK(h, cudaGetLastError());
   return S3BFS_OK;
 }
 

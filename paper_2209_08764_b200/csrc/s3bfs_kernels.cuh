@@ -98,6 +98,8 @@ struct Ctl {
   int32_t p_l;        // P_l = CTAs of this level (Fig1 L16)
   int32_t chunk;      // edges per CTA (ceil(e_l / P_l))
   int32_t wcap;       // edges (= candidate capacity) per warp
+  int32_t e_lo, e_hi; // this rank's slice of the level's global edge range (NEXT-4; else 0, e_l)
+  uint32_t m_tile_ctr, m_done_ctr;  // NEXT-4 merge: look-back tile ids / last-CTA election
   int32_t n_next, e_next;   // written by the last k_compact CTA in tile order
   uint32_t done_ctr;        // last-CTA election in k_compact (not the discovery path)
   uint32_t tile_ctr;        // look-back tile ids in start order (forward progress under any
@@ -146,6 +148,11 @@ struct Params {
   int32_t p_max, grain, t0, variant, collect_stats;
   int32_t direction, do_alpha, do_beta;  // NEXT-3 switch rule (Beamer): alpha, beta
   int32_t n_scan;               // bottom-up scans internal ids [0, n_scan): the ones with deg > 0
+  int32_t dist_size, dist_rank; // NEXT-4 (replicated graph, level edges split over ranks); 1, 0
+  int4 *rec;                    // NEXT-4: this rank's kept vertices {internal id, parent, row
+                                //  start, degree}, exchanged by all-gather
+  int32_t *minrank;             // NEXT-4: per internal vertex, lowest rank keeping it (INT_MAX)
+  unsigned long long *m_status; // NEXT-4: merge look-back words
   long long nnz;
   int32_t col_vec;              // col is 16-byte aligned: vectorised loads allowed
   int32_t use_graph;
@@ -415,11 +422,18 @@ __device__ void decide_tier(const Params &P, Ctl *c, int32_t n_l, int32_t e_l) {
     c->p_l = 1;
     return;
   }
+  // NEXT-4: with dist_size ranks, this rank explores edges [e_lo, e_hi) of the level
+  const long long e_lo = (long long)e_l * P.dist_rank / P.dist_size;
+  const long long e_hi = (long long)e_l * (P.dist_rank + 1) / P.dist_size;
+  const long long es = e_hi - e_lo;
   long long pt = P.variant ? (long long)P.p_max
-                           : min((long long)P.p_max, ((long long)e_l + P.grain - 1) / P.grain);
+                           : min((long long)P.p_max, (es + P.grain - 1) / P.grain);
   if (pt < 1) pt = 1;
-  const long long chunk = ((long long)e_l + pt - 1) / pt;
-  const long long p_l = ((long long)e_l + chunk - 1) / chunk;
+  const long long chunk = es > 0 ? (es + pt - 1) / pt : 1;
+  long long p_l = (es + chunk - 1) / chunk;
+  if (p_l < 1) p_l = 1;  // an empty slice still runs one (idle) CTA: k_compact reports 0
+  c->e_lo = (int32_t)e_lo;
+  c->e_hi = (int32_t)e_hi;
   c->tier = TIER_LARGE;
   c->p_l = (int32_t)p_l;
   c->chunk = (int32_t)chunk;
@@ -501,7 +515,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   const int p_l = c->p_l;
   if (b >= p_l) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int n_l = c->n_l, e_l = c->e_l, chunk = c->chunk, cur = c->cur, wcap = c->wcap;
+  const int n_l = c->n_l, chunk = c->chunk, cur = c->cur, wcap = c->wcap;
   const int new_level = c->level + 1;     // Fig1 L10: discoveries get l+1 (R11)
   const int tag = 1 + (c->level % 255);   // never 0, the per-run initial value
   const int32_t *__restrict__ fx = P.f[cur];
@@ -519,8 +533,8 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
     P.status[b] = 0ull;  // reset k_compact's look-back word for this level
     if (b == 0) c->t_kx_begin = globaltimer();
   }
-  const int E0 = b * chunk;
-  const int E1 = min(E0 + chunk, e_l);
+  const int E0 = c->e_lo + b * chunk;
+  const int E1 = min(E0 + chunk, c->e_hi);
   const int e_begin = min(E0 + warp * wcap, E1);
   const int e_end = min(e_begin + wcap, E1);
   const int segbase = (b * KD_WARPS + warp) * wcap;
@@ -736,6 +750,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
   int2 *__restrict__ crd = P.cand_rd;
   const int seg = (b * KD_WARPS + warp) * c->wcap;
   const int cnt = P.wcnt[b * KD_WARPS + warp];
+  const bool dist = P.dist_size > 1;
   if (b == 0 && tid == 0) c->t_kx_end = globaltimer();
 
   int kept = 0, dsum = 0;
@@ -759,7 +774,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       if (keep) {
         const int q = seg + kept + __popc(m & lanemask_lt());
-        cand[q] = vi[g].z;
+        cand[q] = dist ? v[g] : vi[g].z;  // NEXT-4 keeps the internal id for the record
         crd[q] = make_int2(vi[g].x, d);
       }
       kept += __popc(m);
@@ -788,7 +803,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
       const int n_next = (int)(ex.a + agg.a), e_next = (int)(ex.b + agg.b);
       c->n_next = n_next;
       c->e_next = e_next;
-      P.fex[nxt][n_next] = e_next;
+      if (!dist) P.fex[nxt][n_next] = e_next;
     }
   }
   __syncthreads();
@@ -807,9 +822,13 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
     }
     const int inc = warp_incl_scan(d);
     if (k < kept) {
-      fn[koff + k] = v;
-      frsn[koff + k] = r0;
-      fexn[koff + k] = doff + inc - d;
+      if (dist) {  // NEXT-4: this rank's kept vertex, for the cross-rank merge
+        P.rec[koff + k] = make_int4(v, P.lp[v].y, r0, d);
+      } else {
+        fn[koff + k] = v;
+        frsn[koff + k] = r0;
+        fexn[koff + k] = doff + inc - d;
+      }
     }
     doff += __shfl_sync(0xffffffffu, inc, 31);
   }
@@ -819,7 +838,12 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
   __syncthreads();
   if (tid == 0) s_last = atomicAdd(&c->done_ctr, 1u) == gridDim.x - 1;
   __syncthreads();
-  if (s_last && tid == 0) {
+  if (s_last && tid == 0 && P.dist_size > 1) {
+    // NEXT-4: the local kept count stays in n_next; the merge advances the level
+    c->done_ctr = 0;
+    c->tile_ctr = 0;
+    c->cand_acc = 0;
+  } else if (s_last && tid == 0) {
     __threadfence();
     const int n_next = ld_volatile(&c->n_next), e_next = ld_volatile(&c->e_next);
     const unsigned long long t = globaltimer();
@@ -834,6 +858,118 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
     c->cur = nxt;
     c->m_visited += e_next;
     c->fb_valid = 0;
+    decide(P, c, n_next, e_next);
+  }
+}
+
+// ---- NEXT-4: cross-rank merge (replicated graph, the level's edges split over ranks) ----------
+// Every rank holds the same frontier and explored 1/G of its edges; k_compact left the rank's
+// kept vertices in rec[].  After an all-gather, all[r * stride + i] (i < counts[r]) holds rank
+// r's records.  A vertex kept by several ranks survives from the lowest rank (atomicMin off the
+// discovery path, then an equality test), so every rank builds the identical next frontier.
+constexpr int MG_TILE = KD_THREADS * 4;  // merge entries per CTA
+__global__ void k_merge_min(Params P, const int4 *__restrict__ all, const int32_t *__restrict__ counts,
+                            int32_t stride, int32_t tiles) {
+  const long long total = (long long)P.dist_size * stride;
+  const long long gs = (long long)gridDim.x * blockDim.x;
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < total; j += gs) {
+    const int r = (int)(j / stride), i = (int)(j - (long long)r * stride);
+    if (i < __ldg(counts + r)) atomicMin(P.minrank + __ldg(&all[j].x), r);
+  }
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < tiles; t += gs)
+    P.m_status[t] = 0ull;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    P.ctl->m_tile_ctr = 0;
+    P.ctl->m_done_ctr = 0;
+  }
+}
+
+__global__ void __launch_bounds__(KD_THREADS) k_merge_keep(Params P, const int4 *__restrict__ all,
+                                                           const int32_t *__restrict__ counts,
+                                                           int32_t stride, int32_t tiles) {
+  Ctl *c = P.ctl;
+  __shared__ int32_t s_k[KD_WARPS], s_d[KD_WARPS];
+  __shared__ int s_last, s_tile;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nxt = c->cur ^ 1, new_level = c->level + 1;
+  if (tid == 0) s_tile = (int)atomicAdd(&c->m_tile_ctr, 1u);  // look-back order = start order
+  __syncthreads();
+  const int b = s_tile;
+  const long long total = (long long)P.dist_size * stride;
+  // each warp: 4 groups of 32 consecutive entries of this tile
+  int4 rv[4];
+  bool keep[4];
+  int kept = 0, dsum = 0;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const long long j = (long long)b * MG_TILE + (warp * 4 + g) * 32 + lane;
+    keep[g] = false;
+    rv[g] = make_int4(0, 0, 0, 0);
+    if (j < total) {
+      const int r = (int)(j / stride), i = (int)(j - (long long)r * stride);
+      if (i < __ldg(counts + r)) {
+        rv[g] = all[j];
+        keep[g] = P.minrank[rv[g].x] == r;
+      }
+    }
+    if (keep[g]) {
+      P.minrank[rv[g].x] = 0x7fffffff;  // the unique keeper resets it for the next level
+      P.lp[rv[g].x] = make_int2(new_level, rv[g].y);
+    }
+    bm_publish(P.bm, keep[g], rv[g].x, lane);  // ranks that did not keep v learn its bit here
+    kept += __popc(__ballot_sync(0xffffffffu, keep[g]));
+    dsum += keep[g] ? rv[g].w : 0;
+  }
+  dsum = warp_sum(dsum);
+  if (lane == 0) { s_k[warp] = kept; s_d[warp] = dsum; }
+  __syncthreads();
+  if (warp == 0) {
+    const int kk = lane < KD_WARPS ? s_k[lane] : 0;
+    const int dd = lane < KD_WARPS ? s_d[lane] : 0;
+    const int ik = warp_incl_scan(kk), id = warp_incl_scan(dd);
+    const Pair agg{(uint32_t)__shfl_sync(0xffffffffu, ik, 31),
+                   (uint32_t)__shfl_sync(0xffffffffu, id, 31)};
+    const Pair ex = lookback<true>(P.m_status, b, agg);
+    if (lane < KD_WARPS) {
+      s_k[lane] = (int)ex.a + ik - kk;
+      s_d[lane] = (int)ex.b + id - dd;
+    }
+    if (b == tiles - 1 && lane == 0) {
+      const int n_next = (int)(ex.a + agg.a), e_next = (int)(ex.b + agg.b);
+      c->n_next = n_next;
+      c->e_next = e_next;
+      P.fex[nxt][n_next] = e_next;
+    }
+  }
+  __syncthreads();
+  int koff = s_k[warp], doff = s_d[warp];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {  // next frontier in (tile, warp, group, lane) order
+    const unsigned m = __ballot_sync(0xffffffffu, keep[g]);
+    const int d = keep[g] ? rv[g].w : 0;
+    const int inc = warp_incl_scan(d);
+    if (keep[g]) {
+      const int pos = koff + __popc(m & lanemask_lt());
+      P.f[nxt][pos] = P.n2o ? __ldg(P.n2o + rv[g].x) : rv[g].x;  // caller id
+      P.frs[nxt][pos] = rv[g].z;
+      P.fex[nxt][pos] = doff + inc - d;
+    }
+    koff += __popc(m);
+    doff += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(&c->m_done_ctr, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (s_last && tid == 0) {  // every CTA has read the control block: advance the level
+    __threadfence();
+    const int n_next = ld_volatile(&c->n_next), e_next = ld_volatile(&c->e_next);
+    const unsigned long long t = globaltimer();
+    record_stat(P, c, c->level, c->n_l, c->e_l, TIER_LARGE, c->p_l, 0, n_next, c->t_prev, t);
+    c->t_prev = t;
+    c->level = new_level;
+    c->cur = nxt;
+    c->m_visited += e_next;
     decide(P, c, n_next, e_next);
   }
 }

@@ -23,7 +23,9 @@ STATUS_NAMES = {0: "ok", 1: "invalid argument", 2: "unsupported", 3: "out of mem
 
 EXPORTED = ("s3bfs_create", "s3bfs_clone", "s3bfs_run", "s3bfs_destroy", "s3bfs_status_string",
             "s3bfs_last_error", "s3bfs_get_level_stats", "s3bfs_get_info", "s3bfs_get_kernel_times",
-            "s3bfs_debug_exclusive_scan", "s3bfs_debug_find_start_points", "s3bfs_debug_timeline")
+            "s3bfs_debug_exclusive_scan", "s3bfs_debug_find_start_points", "s3bfs_debug_timeline",
+            "s3bfs_dist_begin", "s3bfs_dist_expand", "s3bfs_dist_records", "s3bfs_dist_merge",
+            "s3bfs_dist_end")
 
 
 class S3BFSError(RuntimeError):
@@ -41,7 +43,8 @@ class Options(ctypes.Structure):
                 ("max_ctas", ctypes.c_int32), ("debug_poison", ctypes.c_int32),
                 ("time_kernels", ctypes.c_int32), ("reorder", ctypes.c_int32),
                 ("direction", ctypes.c_int32), ("do_alpha", ctypes.c_int32),
-                ("do_beta", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
+                ("do_beta", ctypes.c_int32), ("dist_size", ctypes.c_int32),
+                ("dist_rank", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
 
 
 class LevelStat(ctypes.Structure):
@@ -96,6 +99,11 @@ def load(build_if_missing: bool = True):
     lib.s3bfs_debug_exclusive_scan.argtypes = [vp, vp, i32, vp]
     lib.s3bfs_debug_find_start_points.argtypes = [vp, i32, i32, i32, vp, vp, vp]
     lib.s3bfs_debug_timeline.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64)]
+    lib.s3bfs_dist_begin.argtypes = [vp, i32, vp, vp, vp]
+    lib.s3bfs_dist_expand.argtypes = [vp, vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]
+    lib.s3bfs_dist_records.argtypes = [vp, vp, i32, vp]
+    lib.s3bfs_dist_merge.argtypes = [vp, vp, ctypes.POINTER(i32), i32, vp]
+    lib.s3bfs_dist_end.argtypes = [vp, vp]
     for name in EXPORTED:
         if name != "s3bfs_status_string":
             getattr(lib, name).restype = ctypes.c_int
@@ -227,6 +235,37 @@ def s3bfs_debug_timeline(handle) -> list:
     out = (ctypes.c_uint64 * 4)()
     _check(load().s3bfs_debug_timeline(handle, out), "s3bfs_debug_timeline", handle)
     return list(out)
+
+
+# ---- NEXT-4: the per-level protocol of a traversal over G ranks (include/s3bfs.h) ----------
+def s3bfs_dist_begin(handle, source: int, level, parent, stream=None) -> None:
+    _check(load().s3bfs_dist_begin(handle, int(source), _ptr(level), _ptr(parent), _stream(stream)),
+           "s3bfs_dist_begin", handle)
+
+
+def s3bfs_dist_expand(handle, stream=None) -> tuple[int, bool]:
+    """Expand this rank's slice of the level: (record count, traversal done)."""
+    n_local, done = ctypes.c_int32(), ctypes.c_int32()
+    _check(load().s3bfs_dist_expand(handle, _stream(stream), ctypes.byref(n_local), ctypes.byref(done)),
+           "s3bfs_dist_expand", handle)
+    return n_local.value, bool(done.value)
+
+
+def s3bfs_dist_records(handle, dst, count: int, stream=None) -> None:
+    """Copy the first `count` records into dst (int32 CUDA tensor [>= count, 4])."""
+    _check(load().s3bfs_dist_records(handle, _ptr(dst) if count else 0, int(count), _stream(stream)),
+           "s3bfs_dist_records", handle)
+
+
+def s3bfs_dist_merge(handle, all_records, counts, stride: int, stream=None) -> None:
+    """Merge the all-gathered records (int32 CUDA tensor [G * stride, 4]); counts: G ints."""
+    c = (ctypes.c_int32 * len(counts))(*[int(x) for x in counts])
+    _check(load().s3bfs_dist_merge(handle, _ptr(all_records) if stride else 0, c, int(stride),
+                                   _stream(stream)), "s3bfs_dist_merge", handle)
+
+
+def s3bfs_dist_end(handle, stream=None) -> None:
+    _check(load().s3bfs_dist_end(handle, _stream(stream)), "s3bfs_dist_end", handle)
 
 
 class S3BFS:
