@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--loop-mode", type=int, default=0)
     ap.add_argument("--tier0", type=int, default=0)
     ap.add_argument("--grain", type=int, default=0)
+    ap.add_argument("--next4", action="store_true",
+                    help="multi-GPU nodes: also time ONE traversal split over all ranks (NEXT-4, "
+                         "NCCL all-gathers per level; strong scaling), reported beside the line")
     ap.add_argument("--no-next3", action="store_true",
                     help="skip the extra direction-optimising (NEXT-3) measurement")
     ap.add_argument("--direction", type=int, default=0,
@@ -345,6 +348,41 @@ def main():
                  "value": d_value, "unit": "GTEPS", "ms_per_step": d_max_ms / args.steps,
                  "levels_bit_exact_vs_oracle": d_ok, "sources_checked": len(oracle_levels)}
 
+    # ---- NEXT-4 (opt-in, world > 1): one traversal split over all ranks, strong scaling ----
+    next4 = None
+    if args.next4 and world > 1:
+        import paper_2209_08764_b200.dist as pdist
+        dr = pdist.DistRank(ro, col, rank, world)
+        n4_steps = min(args.steps, 16)
+        n4_ok = True
+        for s in srcs[: args.oracle_sources]:  # every rank traverses (collectives); rank 0 checks
+            (lv4, _), = pdist.traverse([dr], s, group=dist.group.WORLD)
+            torch.cuda.synchronize()
+            if s in oracle_levels:
+                n4_ok &= bool(np.array_equal(lv4.cpu().numpy(), oracle_levels[s]))
+        for k in range(args.warmup):
+            pdist.traverse([dr], srcs[k % len(srcs)], group=dist.group.WORLD)
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        n4_edges = 0
+        for k in range(n4_steps):  # every rank runs the SAME source (one traversal)
+            (lv4, _), = pdist.traverse([dr], srcs[k % len(srcs)], group=dist.group.WORLD)
+            n4_edges += int(deg[lv4 >= 0].sum().item()) // 2
+        b.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dr.close()
+        next4 = {"what": "SURVEY NEXT-4: one traversal over all ranks (replicated graph, each "
+                         "level's edges split over ranks, NCCL all-gather of kept vertices per "
+                         "level, cross-rank merge kernels); same sources, no L2 flush",
+                 "value": n4_edges / (float(t.item()) / 1e3) / 1e9, "unit": "GTEPS",
+                 "ranks": world, "scaling": "strong",
+                 "ms_per_traversal": float(t.item()) / n4_steps,
+                 "levels_bit_exact_vs_oracle": n4_ok}
+
     # ---- roofline of k_explore: per-launch CUDA events (host-loop pass, same kernels) -----
     roof = None
     detail = {}
@@ -428,6 +466,8 @@ def main():
             "clocks": clk.summary(), "gpu_launches": my_launches, "verified": verified,
             "next3_direction_optimising": next3,
         }
+        if next4 is not None:
+            line["next4_one_traversal_over_ranks"] = next4
         print(json.dumps(line), flush=True)
         if args.detail_out:
             detail["per_source"] = {int(s): {"m_c": p["m_c"], "levels": p["levels"],
