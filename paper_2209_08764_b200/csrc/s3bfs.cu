@@ -5,9 +5,9 @@
 //
 //   s3bfs_run:  graph { k_init (Fig1 L1-L8);
 //                       WHILE(n_l > 0) {                                   Fig1 L9
-//                         IF(tier 0)  { k_small }                          (f) tier 0
-//                         IF(tier 1)  { k_explore; k_compact }             (c)(d) / (e)(a)(b)
-//                         IF(bottom-up) { k_fb_clear; k_fb_set; k_bottom_up }   NEXT-3
+//                         SWITCH(tier): 0 { k_small }                      (f) tier 0
+//                                       1 { k_explore; k_compact }         (c)(d) / (e)(a)(b)
+//                                       2 { k_fb_clear; k_fb_set; k_bottom_up }   NEXT-3
 //                       }
 //                       k_finalize }
 //   The kernel that decides a level's successor sets the conditional handles (no dispatch
@@ -251,16 +251,11 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
   cudaGraph_t g = nullptr;
   CK(h, cudaGraphCreate(&g, 0));
   h->graph = g;
-  cudaGraphConditionalHandle hw, h0, h1, h2;
+  cudaGraphConditionalHandle hw, ht;
   CK(h, cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault));
-  CK(h, cudaGraphConditionalHandleCreate(&h0, g, 0, cudaGraphCondAssignDefault));
-  CK(h, cudaGraphConditionalHandleCreate(&h1, g, 0, cudaGraphCondAssignDefault));
-  h2 = 0;
-  if (h->P.direction) CK(h, cudaGraphConditionalHandleCreate(&h2, g, 0, cudaGraphCondAssignDefault));
+  CK(h, cudaGraphConditionalHandleCreate(&ht, g, 7, cudaGraphCondAssignDefault));
   h->P.h_while = hw;
-  h->P.h_t0 = h0;
-  h->P.h_t1 = h1;
-  h->P.h_t2 = h2;
+  h->P.h_tier = ht;
   h->P.use_graph = 1;
 
   cudaGraphNodeParams wp = {};
@@ -302,40 +297,27 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
     k.kernelParams = args;
     return k;
   };
-  cudaGraphNode_t n0, n1;
-  cudaGraphNodeParams ip0 = {};
-  ip0.type = cudaGraphNodeTypeConditional;
-  ip0.conditional.handle = h0;
-  ip0.conditional.type = cudaGraphCondTypeIf;
-  ip0.conditional.size = 1;
-  CK(h, cudaGraphAddNode(&n0, body, nullptr, 0, &ip0));
-  cudaGraph_t b0 = ip0.conditional.phGraph_out[0];
+  // one SWITCH per WHILE iteration: body 0 tier 0, body 1 top-down, body 2 bottom-up
+  cudaGraphNodeParams sp = {};
+  sp.type = cudaGraphNodeTypeConditional;
+  sp.conditional.handle = ht;
+  sp.conditional.type = cudaGraphCondTypeSwitch;
+  sp.conditional.size = h->P.direction ? 3 : 2;
+  cudaGraphNode_t snode;
+  CK(h, cudaGraphAddNode(&snode, body, nullptr, 0, &sp));
+  cudaGraph_t b0 = sp.conditional.phGraph_out[0];
+  cudaGraph_t b1 = sp.conditional.phGraph_out[1];
   cudaGraphNode_t ks;
   cudaKernelNodeParams kks = kparams((void *)k_small, 1, KS_THREADS, h->ks_smem);
   CK(h, cudaGraphAddKernelNode(&ks, b0, nullptr, 0, &kks));
-
-  cudaGraphNodeParams ip1 = {};
-  ip1.type = cudaGraphNodeTypeConditional;
-  ip1.conditional.handle = h1;
-  ip1.conditional.type = cudaGraphCondTypeIf;
-  ip1.conditional.size = 1;
-  CK(h, cudaGraphAddNode(&n1, body, &n0, 1, &ip1));
-  cudaGraph_t b1 = ip1.conditional.phGraph_out[0];
   cudaGraphNode_t kx, kc;
   cudaKernelNodeParams kkx = kparams((void *)k_explore, h->P.p_max, KD_THREADS, 0);
   CK(h, cudaGraphAddKernelNode(&kx, b1, nullptr, 0, &kkx));
   cudaKernelNodeParams kkc = kparams((void *)k_compact, h->P.p_max, KD_THREADS, 0);
   CK(h, cudaGraphAddKernelNode(&kc, b1, &kx, 1, &kkc));
-
-  if (h->P.direction) {  // NEXT-3: IF(bottom-up) { k_fb_clear; k_fb_set; k_bottom_up }
-    cudaGraphNodeParams ip2 = {};
-    ip2.type = cudaGraphNodeTypeConditional;
-    ip2.conditional.handle = h2;
-    ip2.conditional.type = cudaGraphCondTypeIf;
-    ip2.conditional.size = 1;
-    cudaGraphNode_t n2, fc, fs, bu;
-    CK(h, cudaGraphAddNode(&n2, body, &n1, 1, &ip2));
-    cudaGraph_t b2 = ip2.conditional.phGraph_out[0];
+  if (h->P.direction) {  // NEXT-3: body 2 { k_fb_clear; k_fb_set; k_bottom_up }
+    cudaGraph_t b2 = sp.conditional.phGraph_out[2];
+    cudaGraphNode_t fc, fs, bu;
     cudaKernelNodeParams kfc = kparams((void *)k_fb_clear, h->num_sms * 4, 256, 0);
     CK(h, cudaGraphAddKernelNode(&fc, b2, nullptr, 0, &kfc));
     cudaKernelNodeParams kfs = kparams((void *)k_fb_set, h->num_sms * 4, 256, 0);

@@ -156,7 +156,8 @@ struct Params {
   long long nnz;
   int32_t col_vec;              // col is 16-byte aligned: vectorised loads allowed
   int32_t use_graph;
-  unsigned long long h_while, h_t0, h_t1, h_t2;  // cudaGraphConditionalHandle values
+  unsigned long long h_while, h_tier;  // cudaGraphConditionalHandle values (WHILE; SWITCH on
+                                       // the tier: body 0 tier 0, 1 top-down, 2 bottom-up)
 };
 
 // ---- PTX helpers ------------------------------------------------------------------------
@@ -376,14 +377,12 @@ __device__ void record_stat(const Params &P, Ctl *c, int32_t level, int32_t n_l,
 }
 
 // Graph mode: the thread that decides the next level's tier also steers the captured loop --
-// WHILE (more levels) and the three IF nodes (tier 0 / top-down / bottom-up) that follow one
-// another inside a WHILE iteration.  No separate dispatch kernel.
+// WHILE (more levels) and one SWITCH node inside a WHILE iteration that runs the tier's body
+// (tier 0 / top-down / bottom-up; one conditional evaluation per level).  No dispatch kernel.
 __device__ void steer(const Params &P, int tier) {
   if (!P.use_graph) return;
-  cudaGraphSetConditional((cudaGraphConditionalHandle)P.h_t0, tier == TIER_SMALL ? 1u : 0u);
-  cudaGraphSetConditional((cudaGraphConditionalHandle)P.h_t1, tier == TIER_LARGE ? 1u : 0u);
-  if (P.direction)
-    cudaGraphSetConditional((cudaGraphConditionalHandle)P.h_t2, tier == TIER_BU ? 1u : 0u);
+  const unsigned body = tier == TIER_SMALL ? 0u : tier == TIER_LARGE ? 1u : tier == TIER_BU ? 2u : 7u;
+  cudaGraphSetConditional((cudaGraphConditionalHandle)P.h_tier, body);
   cudaGraphSetConditional((cudaGraphConditionalHandle)P.h_while, tier != TIER_DONE ? 1u : 0u);
 }
 

@@ -17,3 +17,14 @@ for rep in range(5):
     print(f"run {rep}: total {ev[0].elapsed_time(ev[1])*1e3:.1f} us, levels {len(st)}, "
           f"L0 {(st['t_end_ns'][0]-st['t_begin_ns'][0])/1e3:.1f} us, "
           f"L0 end->last level end {(st['t_end_ns'][-1]-st['t_end_ns'][0])/1e3:.1f} us")
+# per level: launch gap before k_explore (from the previous level's end), explore, compact
+st = bfs.level_stats()
+for r in st:
+    if r['tier'] == 1:
+        print(f"  L{r['level']} tier1 n={r['n_l']} e={r['e_l']}: gap-to-explore "
+              f"{(r['t_explore_begin_ns'] - r['t_begin_ns']) / 1e3:.1f} us, explore "
+              f"{(r['t_explore_end_ns'] - r['t_explore_begin_ns']) / 1e3:.1f} us, compact+gap "
+              f"{(r['t_end_ns'] - r['t_explore_end_ns']) / 1e3:.1f} us")
+    else:
+        print(f"  L{r['level']} tier{r['tier']} n={r['n_l']} e={r['e_l']}: "
+              f"{(r['t_end_ns'] - r['t_begin_ns']) / 1e3:.1f} us")
