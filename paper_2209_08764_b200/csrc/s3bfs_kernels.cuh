@@ -360,6 +360,22 @@ __device__ Pair lookback(unsigned long long *status, int tile, Pair agg) {
 // ---- (f) level-adaptive sizing: the tier and P_l of the level held in ctl ------------------
 // P_l = min(P_max, ceil(e_l / grain)) -- the GPU form of P_l <- Min(P, e_l) (Fig1 L16):
 // a "core" here is a CTA that streams >= grain edges.  variant 1 = work-insensitive.
+// Tier 0 keeps the record counter in a register across its levels (a global read-after-write
+// of num_levels per level sat on the critical path of every one-vertex level).
+__device__ __forceinline__ void record_stat_at(const Params &P, int &k, int32_t level, int32_t n_l,
+                                               int32_t e_l, int32_t tier, int32_t cand,
+                                               int32_t kept, unsigned long long t0,
+                                               unsigned long long t1) {
+  if (!P.collect_stats) return;
+  if (k < P.stats_cap) {
+    s3bfs_level_stat r;
+    r.level = level; r.n_l = n_l; r.e_l = e_l; r.tier = tier; r.grid = 1;
+    r.candidates = cand; r.kept = kept; r.pad = 0; r.t_begin_ns = t0; r.t_end_ns = t1;
+    r.t_explore_begin_ns = 0; r.t_explore_end_ns = 0;
+    P.stats[k] = r;
+  }
+  ++k;
+}
 __device__ void record_stat(const Params &P, Ctl *c, int32_t level, int32_t n_l, int32_t e_l,
                             int32_t tier, int32_t grid, int32_t cand, int32_t kept,
                             unsigned long long t0, unsigned long long t1,
@@ -981,7 +997,7 @@ __global__ void __launch_bounds__(KD_THREADS) k_merge_keep(Params P, const int4 
 // the Owner check (R4), without the Owner round trip.  Returns when the next level is not
 // tiny (or empty), leaving that frontier in shared memory and its (n, e, level) in st[].
 __device__ void tiny_levels(const Params &P, Ctl *c, int32_t *sf, int32_t *srs, int32_t *sex,
-                            int32_t *st, unsigned long long &t_prev, long long &m_add) {
+                            int32_t *st, unsigned long long &t_prev, long long &m_add, int &nrec) {
   const int lane = threadIdx.x & 31;
   const int32_t *__restrict__ col = P.col;
   int n_l = st[0], e_l = st[1], L = st[2];
@@ -1021,7 +1037,7 @@ __device__ void tiny_levels(const Params &P, Ctl *c, int32_t *sf, int32_t *srs, 
     const int nfe = __shfl_sync(0xffffffffu, inc - d, src);
     if (lane == 0) {
       const unsigned long long t = globaltimer();
-      record_stat(P, c, L, n_l, e_l, TIER_SMALL, 1, ncand, n_next, t_prev, t);
+      record_stat_at(P, nrec, L, n_l, e_l, TIER_SMALL, ncand, n_next, t_prev, t);
       t_prev = t;
       m_add += e_next;
     }
@@ -1077,6 +1093,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
   unsigned long long t_prev = c->t_prev;
   if (tid == 0 && L == 0) c->t_dbg[2] = globaltimer();
   long long m_add = 0;  // degrees of the frontiers created here (thread 0)
+  int nrec = c->num_levels;  // stats records (thread 0), written back before decide()
   for (int i = tid; i < n_l; i += KS_THREADS) {
     sf[i] = P.f[cur][i];
     srs[i] = P.frs[cur][i];
@@ -1089,7 +1106,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
     if (n_l <= 32 && e_l <= 32) {  // tiny levels: warp 0 alone, no CTA barrier per level
       if (tid == 0) { s_tiny[0] = n_l; s_tiny[1] = e_l; s_tiny[2] = L; }
       __syncwarp();
-      if (warp == 0) tiny_levels(P, c, sf, srs, sex, s_tiny, t_prev, m_add);
+      if (warp == 0) tiny_levels(P, c, sf, srs, sex, s_tiny, t_prev, m_add, nrec);
       __syncthreads();
       n_l = s_tiny[0];
       e_l = s_tiny[1];
@@ -1238,7 +1255,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
     if (tid == 0) {
       sex[n_next] = e_next;
       const unsigned long long t = globaltimer();
-      record_stat(P, c, L, n_l, e_l, TIER_SMALL, 1, s_tot[2], n_next, t_prev, t);
+      record_stat_at(P, nrec, L, n_l, e_l, TIER_SMALL, s_tot[2], n_next, t_prev, t);
       t_prev = t;
       m_add += e_next;
     }
@@ -1258,6 +1275,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
     if (tid == 0) P.fex[cur][n_l] = e_l;
   }
   if (tid == 0) {
+    c->num_levels = nrec;
     c->level = L;
     c->t_prev = t_prev;
     c->m_visited += m_add;
