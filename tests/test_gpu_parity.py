@@ -297,3 +297,29 @@ def test_clones_run_concurrently(cfg_kw):
     for h in clones[1:]:              # clones still usable after the source is gone
         check_traversal(g, h, srcs[0], stats=False)
         h.close()
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(reorder=-1, tier0_max_edges=-1)],
+                         ids=["default", "no-reorder-tier1"])
+def test_maximum_size_sparse(kw):
+    """Maximum-size edge case: n = 2^28 - 5 (ragged: not a multiple of 32/128/16), a few
+    hundred thousand arcs spread over the whole id range (64-bit index arithmetic in create,
+    k_init, the relabel sort, the hashed claim slots and k_finalize), a high-id hub and a long
+    path crossing the range; levels bit-exact with the oracle, parents by the certificate."""
+    n = (1 << 28) - 5
+    rng = np.random.default_rng(28)
+    hub = n - 1
+    path = np.sort(rng.choice(n - 1, 3000, replace=False))
+    leaves = rng.choice(n - 1, 100_000, replace=False)
+    e = np.concatenate([np.stack([path[:-1], path[1:]], 1),
+                        np.stack([np.full(leaves.size, hub), leaves], 1),
+                        np.array([[hub, path[0]]])]).astype(np.int64)
+    g = graphgen.from_edges(n, e, name="max-sparse")
+    ro, col = to_dev(g)
+    bfs = pkg.S3BFS(ro, col, pkg.Options(**kw))
+    for s in (int(path[-1]), hub, int(leaves[0])):
+        check_traversal(g, bfs, s, stats=False)
+    unreached = int(np.setdiff1d(np.arange(5), np.concatenate([path, leaves, [hub]]))[0])
+    lv, _ = check_traversal(g, bfs, unreached, stats=False)  # isolated source: only itself
+    assert (lv >= 0).sum() == 1
+    bfs.close()
