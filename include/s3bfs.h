@@ -86,13 +86,16 @@ typedef struct {
                               the s3bfs_dist_* calls below, not s3bfs_run.  Needs loop_mode 2
                               semantics (set implicitly), tier 0 off (implicit), direction 0 */
   int32_t dist_rank;       /* NEXT-4: 0 <= dist_rank < dist_size */
-  int32_t reserved[1];
+  int32_t cluster_max_edges; /* cluster tier (one 8-CTA thread-block cluster running
+                              consecutive levels with T0 < e_l <= this and n_l <= 8192 in one
+                              launch).  0 -> 32768 (the maximum); < 0 -> off.  With it on, the
+                              default T0 (tier0_max_edges = 0) is 4096 */
 } s3bfs_options;
 
 /* One record per BFS level (the SPEC LevelStats analogue).  n_l = |frontier|
  * (Fig1 L9), e_l = sum of its degrees (Fig1 L15), tier 0 = single CTA, 1 = full kernels,
  * 2 = a last level with e_l = 0 (nothing explored), 3 = bottom-up (NEXT-3), grid = CTAs used
- * (P_l), candidates =
+ * (P_l; tier 4 = the cluster tier, grid = its CTAs), candidates =
  * discoveries incl. benign-race duplicates, kept = n_{l+1} after owner dedup.  Times are
  * %globaltimer ns: level start (= previous level's end, so launch gaps count) and end; for
  * tier 1 also k_explore's start (its CTA 0) and k_compact's start (its CTA 0), whose

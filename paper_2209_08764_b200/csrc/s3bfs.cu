@@ -8,6 +8,7 @@
 //                         SWITCH(tier): 0 { k_small }                      (f) tier 0
 //                                       1 { k_explore; k_compact }         (c)(d) / (e)(a)(b)
 //                                       2 { k_fb_clear; k_fb_set; k_bottom_up }   NEXT-3
+//                                       3 { k_cluster: consecutive mid-size levels }  (f)
 //                       }
 //                       k_finalize }
 //   The kernel that decides a level's successor sets the conditional handles (no dispatch
@@ -54,7 +55,7 @@ struct s3bfs_ctx {
   const int32_t *ro_int = nullptr;  // row offsets of the internal CSR
   size_t ws_bytes = 0;
   int64_t cand_cap = 0;
-  size_t ks_smem = 0;
+  size_t ks_smem = 0, kc_smem = 0;
   int loop_graph = 1;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -302,7 +303,7 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
   sp.type = cudaGraphNodeTypeConditional;
   sp.conditional.handle = ht;
   sp.conditional.type = cudaGraphCondTypeSwitch;
-  sp.conditional.size = h->P.direction ? 3 : 2;
+  sp.conditional.size = 4;  // body 2 stays empty without NEXT-3
   cudaGraphNode_t snode;
   CK(h, cudaGraphAddNode(&snode, body, nullptr, 0, &sp));
   cudaGraph_t b0 = sp.conditional.phGraph_out[0];
@@ -315,6 +316,12 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
   CK(h, cudaGraphAddKernelNode(&kx, b1, nullptr, 0, &kkx));
   cudaKernelNodeParams kkc = kparams((void *)k_compact, h->P.p_max, KD_THREADS, 0);
   CK(h, cudaGraphAddKernelNode(&kc, b1, &kx, 1, &kkc));
+  {  // body 3: the cluster tier (one 8-CTA cluster, consecutive mid-size levels)
+    cudaGraph_t b3 = sp.conditional.phGraph_out[3];
+    cudaGraphNode_t kcl;
+    cudaKernelNodeParams kkcl = kparams((void *)k_cluster, KC_CL, KC_THREADS, h->kc_smem);
+    CK(h, cudaGraphAddKernelNode(&kcl, b3, nullptr, 0, &kkcl));
+  }
   if (h->P.direction) {  // NEXT-3: body 2 { k_fb_clear; k_fb_set; k_bottom_up }
     cudaGraph_t b2 = sp.conditional.phGraph_out[2];
     cudaGraphNode_t fc, fs, bu;
@@ -412,7 +419,12 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   int p_max = h->num_sms * occ;  // every CTA resident: the look-back never waits on a CTA
   if (h->opt.max_ctas > 0 && h->opt.max_ctas < p_max) p_max = h->opt.max_ctas;
   const int grain = h->opt.edges_per_cta > 0 ? h->opt.edges_per_cta : 2048;
-  int t0 = h->opt.tier0_max_edges == 0 ? KS_ECAP : h->opt.tier0_max_edges;
+  // cluster tier: T0 < e_l <= tc_max (one 8-CTA cluster); tier 0 keeps the small levels
+  int tc_max = h->opt.cluster_max_edges == 0 ? KC_CL * KC_ECTA : h->opt.cluster_max_edges;
+  if (tc_max > KC_CL * KC_ECTA) tc_max = KC_CL * KC_ECTA;
+  if (h->opt.cluster_max_edges < 0 || h->opt.variant == 1) tc_max = -1;
+  int t0 = h->opt.tier0_max_edges == 0 ? (tc_max > 0 ? S3BFS_T0_WITH_CLUSTER : KS_ECAP)
+                                       : h->opt.tier0_max_edges;
   if (t0 > KS_ECAP) t0 = KS_ECAP;
   if (h->opt.variant == 1) t0 = -1;
   h->loop_graph = h->opt.loop_mode == 2 ? 0 : 1;
@@ -425,6 +437,7 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
       return bail(fail(h, S3BFS_ERR_UNSUPPORTED, "dist_size > 1 with direction = 1"));
     h->loop_graph = 0;
     t0 = -1;
+    tc_max = -1;
   }
   const int collect = h->opt.collect_stats >= 0 ? 1 : 0;
 
@@ -487,6 +500,7 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   P.p_max = p_max;
   P.grain = grain;
   P.t0 = t0;
+  P.tc_max = tc_max;
   P.variant = h->opt.variant == 1 ? 1 : 0;
   P.collect_stats = collect;
   P.use_graph = 0;
@@ -570,6 +584,9 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   h->ks_smem = (size_t)(3 * KS_NCAP + 4 + 2 * KS_ECAP) * 4;
   if ((e = cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->ks_smem)) != cudaSuccess)
     return bail(cuda_fail(h, e, "cudaFuncSetAttribute(k_small)"));
+  h->kc_smem = (size_t)(3 * KC_FCAP + 4 + 2 * KC_ECTA) * 4;
+  if ((e = cudaFuncSetAttribute(k_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->kc_smem)) != cudaSuccess)
+    return bail(cuda_fail(h, e, "cudaFuncSetAttribute(k_cluster)"));
 
   if (h->loop_graph) {
     s3bfs_status s = build_graph(h);
@@ -635,7 +652,7 @@ s3bfs_status s3bfs_run(s3bfs_handle h, int32_t source, int32_t *level, int32_t *
     CK(h, cudaStreamSynchronize(stream));
     if (pending >= 0) {
       float a = 0.f, b = 0.f;
-      if (pending == TIER_SMALL) {
+      if (pending == TIER_SMALL || pending == TIER_CLUSTER) {
         CK(h, cudaEventElapsedTime(&a, h->ev[0], h->ev[1]));
         h->kt.small_ms += a;
         h->kt.small_launches++;
@@ -662,6 +679,9 @@ s3bfs_status s3bfs_run(s3bfs_handle h, int32_t source, int32_t *level, int32_t *
     if (h->time_kernels) CK(h, cudaEventRecord(h->ev[0], stream));
     if (c.tier == TIER_SMALL) {
       k_small<<<1, KS_THREADS, h->ks_smem, stream>>>(h->P);
+      if (h->time_kernels) CK(h, cudaEventRecord(h->ev[1], stream));
+    } else if (c.tier == TIER_CLUSTER) {
+      k_cluster<<<KC_CL, KC_THREADS, h->kc_smem, stream>>>(h->P);
       if (h->time_kernels) CK(h, cudaEventRecord(h->ev[1], stream));
     } else if (c.tier == TIER_BU) {
       k_fb_clear<<<h->num_sms * 4, 256, 0, stream>>>(h->P);

@@ -26,6 +26,7 @@
 //   k_find_start (c) alone  test entry: the same warp search, one warp per worker.
 #pragma once
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
 #include <stdint.h>
 
 #include "../../include/s3bfs.h"
@@ -66,6 +67,9 @@ namespace s3bfs {
 #ifndef S3BFS_COL_HINT
 #define S3BFS_COL_HINT 1  // col loads carry the L2 evict-first policy
 #endif
+#ifndef S3BFS_T0_WITH_CLUSTER
+#define S3BFS_T0_WITH_CLUSTER 4096  // default T0 when the cluster tier is on (measured crossover)
+#endif
 #ifndef S3BFS_BM_NC
 #define S3BFS_BM_NC 1     // bitmap probes through the non-coherent (read-only) path
 #endif
@@ -83,7 +87,13 @@ constexpr int SCAN_THREADS = 512;
 constexpr int SCAN_ITEMS = 8;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 
-constexpr int TIER_SMALL = 0, TIER_LARGE = 1, TIER_DONE = 2, TIER_BU = 3;
+constexpr int TIER_SMALL = 0, TIER_LARGE = 1, TIER_DONE = 2, TIER_BU = 3, TIER_CLUSTER = 4;
+// cluster tier (f, SURVEY 8(a) "optional middle tier"): one cluster of KC_CL CTAs
+constexpr int KC_CL = 8;                         // CTAs per cluster (portable size)
+constexpr int KC_THREADS = 1024;
+constexpr int KC_ECTA = 4096;                    // level edges per CTA (e_l <= 32,768)
+constexpr int KC_FCAP = 8192;                    // replicated frontier capacity
+constexpr int KC_IPT = KC_ECTA / KC_THREADS;
 constexpr int BU_W = 4;   // bottom-up: bitmap words per warp round
 constexpr int BU_P = 2;   // bottom-up: in-neighbours probed per vertex per round
 
@@ -146,6 +156,7 @@ struct Params {
   s3bfs_level_stat *stats;
   int32_t stats_cap;
   int32_t p_max, grain, t0, variant, collect_stats;
+  int32_t tc_max;               // cluster tier: levels with t0 < e_l <= tc_max (< 0: off)
   int32_t direction, do_alpha, do_beta;  // NEXT-3 switch rule (Beamer): alpha, beta
   int32_t n_scan;               // bottom-up scans internal ids [0, n_scan): the ones with deg > 0
   int32_t dist_size, dist_rank; // NEXT-4 (replicated graph, level edges split over ranks); 1, 0
@@ -369,7 +380,8 @@ __device__ __forceinline__ void record_stat_at(const Params &P, int &k, int32_t 
   if (!P.collect_stats) return;
   if (k < P.stats_cap) {
     s3bfs_level_stat r;
-    r.level = level; r.n_l = n_l; r.e_l = e_l; r.tier = tier; r.grid = 1;
+    r.level = level; r.n_l = n_l; r.e_l = e_l; r.tier = tier;
+    r.grid = tier == TIER_CLUSTER ? KC_CL : 1;
     r.candidates = cand; r.kept = kept; r.pad = 0; r.t_begin_ns = t0; r.t_end_ns = t1;
     r.t_explore_begin_ns = 0; r.t_explore_end_ns = 0;
     P.stats[k] = r;
@@ -397,7 +409,8 @@ __device__ void record_stat(const Params &P, Ctl *c, int32_t level, int32_t n_l,
 // (tier 0 / top-down / bottom-up; one conditional evaluation per level).  No dispatch kernel.
 __device__ void steer(const Params &P, int tier) {
   if (!P.use_graph) return;
-  const unsigned body = tier == TIER_SMALL ? 0u : tier == TIER_LARGE ? 1u : tier == TIER_BU ? 2u : 7u;
+  const unsigned body = tier == TIER_SMALL ? 0u : tier == TIER_LARGE ? 1u : tier == TIER_BU ? 2u
+                      : tier == TIER_CLUSTER ? 3u : 7u;
   cudaGraphSetConditional((cudaGraphConditionalHandle)P.h_tier, body);
   cudaGraphSetConditional((cudaGraphConditionalHandle)P.h_while, tier != TIER_DONE ? 1u : 0u);
 }
@@ -435,6 +448,11 @@ __device__ void decide_tier(const Params &P, Ctl *c, int32_t n_l, int32_t e_l) {
   if (P.variant == 0 && P.t0 >= 0 && e_l <= P.t0 && n_l <= KS_NCAP) {
     c->tier = TIER_SMALL;
     c->p_l = 1;
+    return;
+  }
+  if (P.variant == 0 && e_l <= P.tc_max && n_l <= KC_FCAP) {
+    c->tier = TIER_CLUSTER;
+    c->p_l = KC_CL;
     return;
   }
   // NEXT-4: with dist_size ranks, this rank explores edges [e_lo, e_hi) of the level
@@ -1277,6 +1295,193 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
   if (tid == 0) {
     c->num_levels = nrec;
     c->level = L;
+    c->t_prev = t_prev;
+    c->m_visited += m_add;
+    c->fb_valid = 0;
+    c->bu = 0;
+    decide(P, c, n_l, e_l);
+  }
+}
+
+// ---- cluster tier: k_cluster ------------------------------------------------------------------
+// SURVEY 8(a)/(f)'s optional middle tier: one thread-block cluster of KC_CL CTAs runs
+// consecutive mid-size levels (T0 < e_l <= tc_max, n_l <= KC_FCAP) inside one launch -- no
+// kernel launch and no captured-loop iteration per level, and KC_CL SMs instead of tier 0's
+// one.  Every CTA holds the whole frontier in its shared memory (replicated through
+// distributed shared memory); CTA r explores edges [r e_l / KC_CL, (r+1) e_l / KC_CL) with the
+// k_small step (search of the degree scan, col, visited word, Owner = global edge index);
+// after a cluster barrier it checks Owner through L2 (another SM wrote it), keeps its
+// vertices, and the CTAs exchange their (kept, degree-sum) totals through DSMEM; each CTA then
+// writes its kept vertices into every CTA's frontier (continuing) or into the global frontier
+// (the level that leaves the tier).  Same per-level contract as k_small / k_explore+k_compact.
+__global__ void __cluster_dims__(KC_CL, 1, 1) __launch_bounds__(KC_THREADS, 1) k_cluster(Params P) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  Ctl *c = P.ctl;
+  if (c->tier != TIER_CLUSTER) return;  // read before any CTA of the cluster can change it
+  extern __shared__ int32_t smem[];
+  int32_t *sf = smem;                 // frontier caller ids (replicated)
+  int32_t *srs = sf + KC_FCAP;        // internal row starts
+  int32_t *sex = srs + KC_FCAP;       // exclusive degree scan, KC_FCAP + 1 entries
+  int32_t *cv = sex + KC_FCAP + 4;    // candidate per local edge (or -1)
+  int32_t *cpv = cv + KC_ECTA;        // its discoverer (caller id)
+  __shared__ int32_t s_wk[KC_THREADS / 32], s_wd[KC_THREADS / 32], s_wc[KC_THREADS / 32];
+  __shared__ int32_t s_tot[3];        // this CTA's kept, degree sum, candidates
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rank = (int)cl.block_rank();
+  const int32_t *__restrict__ col = P.col;
+  int4 *__restrict__ vinfo = P.vinfo;
+  const uint32_t *__restrict__ bm = P.bm;
+  int n_l = c->n_l, e_l = c->e_l, L = c->level;
+  const int cur = c->cur, nxt = cur ^ 1;
+  unsigned long long t_prev = c->t_prev;
+  int nrec = c->num_levels;
+  long long m_add = 0;
+  for (int i = tid; i < n_l; i += KC_THREADS) {
+    sf[i] = P.f[cur][i];
+    srs[i] = P.frs[cur][i];
+    sex[i] = P.fex[cur][i];
+  }
+  if (tid == 0) sex[n_l] = e_l;
+  cl.sync();  // every CTA has read the control block and its frontier copy
+  for (;;) {
+    const int lo = (int)((long long)e_l * rank / KC_CL);
+    const int ne = (int)((long long)e_l * (rank + 1) / KC_CL) - lo;  // <= KC_ECTA
+    // (c)+(d): local edge k -> global edge lo + k -> frontier slot by binary search
+    int ncand = 0;
+    int ev[KC_IPT], ux[KC_IPT];
+#pragma unroll
+    for (int i = 0; i < KC_IPT; ++i) {
+      const int k = tid + i * KC_THREADS;
+      ev[i] = -1;
+      ux[i] = 0;
+      if (k < ne) {
+        const int e = lo + k;
+        int a = 0, z = n_l;
+        while (z - a > 1) {
+          const int mid = (a + z) >> 1;
+          if (sex[mid] <= e) a = mid; else z = mid;
+        }
+        ux[i] = sf[a];
+        ev[i] = __ldg(col + srs[a] + (e - sex[a]));
+      }
+    }
+    uint32_t wv[KC_IPT];
+#pragma unroll
+    for (int i = 0; i < KC_IPT; ++i) wv[i] = ev[i] >= 0 ? __ldcg(bm + (ev[i] >> 5)) : 0xffffffffu;
+#pragma unroll
+    for (int i = 0; i < KC_IPT; ++i) {
+      const int k = tid + i * KC_THREADS;
+      if (k < ne) {
+        const int v = ev[i];
+        int w = -1;
+        if (!((wv[i] >> (v & 31)) & 1u)) {
+          st_weak(owner_of(vinfo, v), lo + k);  // Owner[v] <- global edge index (benign race)
+          w = v;
+          ++ncand;
+        }
+        cv[k] = w;
+        cpv[k] = ux[i];
+      }
+    }
+    __threadfence();  // Owner stores reach L2 before any CTA of the cluster checks them
+    cl.sync();
+    // (e): owner check through L2 (the winner may sit on another SM), blocked items
+    const int ipt = (ne + KC_THREADS - 1) / KC_THREADS;
+    const int k0 = tid * ipt;
+    int kv[KC_IPT], kr[KC_IPT], kd[KC_IPT];
+    int4 vis[KC_IPT];
+#pragma unroll
+    for (int i = 0; i < KC_IPT; ++i) {
+      const int k = k0 + i;
+      const int v = (i < ipt && k < ne) ? cv[k] : -1;
+      kv[i] = v;
+      vis[i] = v >= 0 ? __ldcg(vinfo + v) : make_int4(0, 0, 0, -1);
+    }
+    int cnt = 0, dsum = 0;
+#pragma unroll
+    for (int i = 0; i < KC_IPT; ++i) {
+      const int k = k0 + i;
+      const int v = kv[i];
+      kv[i] = -1;
+      kr[i] = 0;
+      kd[i] = 0;
+      if (v >= 0 && vis[i].w == lo + k) {
+        kv[i] = vis[i].z; kr[i] = vis[i].x; kd[i] = vis[i].y;
+        P.lp[v] = make_int2(L + 1, cpv[k]);          // d[v] <- l, parent (Fig1 L18)
+        atomicOr(P.bm + (v >> 5), 1u << (v & 31));   // exact visited bit (not discovery)
+        ++cnt;
+        dsum += kd[i];
+      }
+    }
+    // CTA scan of (cnt, dsum)
+    const int ik = warp_incl_scan(cnt), id = warp_incl_scan(dsum);
+    const int wc = P.collect_stats ? warp_sum(ncand) : 0;
+    if (lane == 31) { s_wk[warp] = ik; s_wd[warp] = id; }
+    if (lane == 0) s_wc[warp] = wc;
+    __syncthreads();
+    if (warp == 0) {
+      const int a = s_wk[lane], d = s_wd[lane];
+      const int ia = warp_incl_scan(a), idd = warp_incl_scan(d);
+      const int ctot = warp_sum(s_wc[lane]);
+      s_wk[lane] = ia - a;
+      s_wd[lane] = idd - d;
+      if (lane == 31) { s_tot[0] = ia; s_tot[1] = idd; s_tot[2] = ctot; }
+    }
+    cl.sync();  // every CTA's totals are published (DSMEM)
+    int koff = 0, doff = 0, n_next = 0, e_next = 0, c_all = 0;
+#pragma unroll
+    for (int r = 0; r < KC_CL; ++r) {  // the cluster's exclusive scan over CTA totals
+      const int32_t *t = cl.map_shared_rank(s_tot, r);
+      const int k = t[0], d = t[1];
+      if (r < rank) { koff += k; doff += d; }
+      n_next += k;
+      e_next += d;
+      c_all += t[2];
+    }
+    const bool stay = n_next > 0 && e_next > 0 && e_next > P.t0 && e_next <= P.tc_max &&
+                      n_next <= KC_FCAP;
+    int kpos = koff + s_wk[warp] + ik - cnt, dpos = doff + s_wd[warp] + id - dsum;
+#pragma unroll
+    for (int i = 0; i < KC_IPT; ++i) {
+      if (kv[i] >= 0) {
+        if (stay) {  // the next level stays here: write every CTA's frontier copy
+#pragma unroll
+          for (int r = 0; r < KC_CL; ++r) {
+            cl.map_shared_rank(sf, r)[kpos] = kv[i];
+            cl.map_shared_rank(srs, r)[kpos] = kr[i];
+            cl.map_shared_rank(sex, r)[kpos] = dpos;
+          }
+        } else {     // the level leaves the tier: the global frontier for the next tier
+          P.f[nxt][kpos] = kv[i];
+          P.frs[nxt][kpos] = kr[i];
+          P.fex[nxt][kpos] = dpos;
+        }
+        ++kpos;
+        dpos += kd[i];
+      }
+    }
+    if (tid == 0) {
+      if (stay) sex[n_next] = e_next;
+      else if (rank == 0) P.fex[nxt][n_next] = e_next;
+    }
+    if (rank == 0 && tid == 0) {
+      const unsigned long long t = globaltimer();
+      record_stat_at(P, nrec, L, n_l, e_l, TIER_CLUSTER, c_all, n_next, t_prev, t);
+      t_prev = t;
+      m_add += e_next;
+    }
+    cl.sync();  // frontier copies complete (and every CTA done with the old ones)
+    ++L;
+    n_l = n_next;
+    e_l = e_next;
+    if (!stay) break;
+  }
+  if (rank == 0 && tid == 0) {  // leave the tier: hand over the control block
+    __threadfence();
+    c->num_levels = nrec;
+    c->level = L;
+    c->cur = nxt;
     c->t_prev = t_prev;
     c->m_visited += m_add;
     c->fb_valid = 0;

@@ -26,6 +26,10 @@ SETTINGS = [
     ("host-loop", dict(debug_poison=1, loop_mode=2, tier0_max_edges=512)),
     ("work-insensitive", dict(debug_poison=1, variant=1)),
     ("grain-4096-T0-1", dict(debug_poison=1, tier0_max_edges=1, edges_per_cta=4096)),
+    # cluster tier (one 8-CTA cluster, consecutive levels): nearly every mid-size level / off
+    ("cluster-T0-16", dict(debug_poison=1, tier0_max_edges=16)),
+    ("cluster-only-host", dict(debug_poison=1, tier0_max_edges=-1, loop_mode=2)),
+    ("no-cluster", dict(debug_poison=1, cluster_max_edges=-1)),
     ("no-reorder", dict(debug_poison=1, reorder=-1, tier0_max_edges=64)),
     # NEXT-3 direction optimisation: bottom-up on every level / switching back and forth
     ("bu-always", dict(debug_poison=1, tier0_max_edges=-1, direction=1, do_alpha=1 << 30,
