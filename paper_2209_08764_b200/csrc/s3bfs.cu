@@ -457,8 +457,10 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   const size_t o_crd = take((size_t)h->cand_cap * 8);
   const size_t bm_bytes = ((size_t)n + 127) / 128 * 16;  // 16 B padded (vector clears)
   const size_t o_bm = take(bm_bytes + 16);  // + the sentinel block (Params::v_sent)
-  size_t claim_n = 16;  // claim slots: a power of two >= n (claim_slot's hash is mod 2^k)
-  while (claim_n < (size_t)n) claim_n <<= 1;
+  // claim slots: a power of two >= max(n, a floor) (claim_slot's hash is mod 2^k); the floor
+  // spreads a small graph's tags over more L2 lines (fewer same-line probes and stores)
+  size_t claim_n = 16;
+  while (claim_n < (size_t)n || claim_n < (size_t)S3BFS_CLAIM_MIN_BYTES) claim_n <<= 1;
   const size_t o_claim = take(claim_n);
   const size_t o_fb0 = take(bm_bytes), o_fb1 = take(bm_bytes);
   const size_t o_wcnt = take((size_t)p_max * KD_WARPS * 4);

@@ -70,6 +70,9 @@ namespace s3bfs {
 #ifndef S3BFS_T0_WITH_CLUSTER
 #define S3BFS_T0_WITH_CLUSTER 4096  // default T0 when the cluster tier is on (measured crossover)
 #endif
+#ifndef S3BFS_CLAIM_MIN_BYTES
+#define S3BFS_CLAIM_MIN_BYTES (8u << 20)  // claim array floor (measured, DESIGN R26)
+#endif
 #ifndef S3BFS_BM_NC
 #define S3BFS_BM_NC 1     // bitmap probes through the non-coherent (read-only) path
 #endif
