@@ -73,6 +73,12 @@ namespace s3bfs {
 #ifndef S3BFS_CLAIM_MIN_BYTES
 #define S3BFS_CLAIM_MIN_BYTES (8u << 20)  // claim array floor (measured, DESIGN R26)
 #endif
+#ifndef S3BFS_BU_W
+#define S3BFS_BU_W 4
+#endif
+#ifndef S3BFS_BU_P
+#define S3BFS_BU_P 2
+#endif
 #ifndef S3BFS_BM_NC
 #define S3BFS_BM_NC 1     // bitmap probes through the non-coherent (read-only) path
 #endif
@@ -97,8 +103,8 @@ constexpr int KC_THREADS = 1024;
 constexpr int KC_ECTA = 4096;                    // level edges per CTA (e_l <= 32,768)
 constexpr int KC_FCAP = 8192;                    // replicated frontier capacity
 constexpr int KC_IPT = KC_ECTA / KC_THREADS;
-constexpr int BU_W = 4;   // bottom-up: bitmap words per warp round
-constexpr int BU_P = 2;   // bottom-up: in-neighbours probed per vertex per round
+constexpr int BU_W = S3BFS_BU_W;   // bottom-up: bitmap words per warp round
+constexpr int BU_P = S3BFS_BU_P;   // bottom-up: in-neighbours probed per vertex per round
 
 // Device control block: the paper's loop state (Fig1 L8-L11, L15-L16) kept on the device so
 // the level loop needs no host round trip.
