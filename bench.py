@@ -124,11 +124,15 @@ class ClockSampler:
 
 def launches_from_stats(st) -> int:
     """Kernel launches of one traversal in graph mode: k_init, one k_small per run of
-    tier-0 levels, k_explore + k_compact per top-down level, k_fb_clear + k_fb_set +
-    k_bottom_up per bottom-up level (NEXT-3), k_finalize."""
-    tiers = [int(t) for t in st["tier"] if t in (0, 1, 3)]
-    segs0 = sum(1 for i, t in enumerate(tiers) if t == 0 and (i == 0 or tiers[i - 1] != 0))
-    return 1 + segs0 + 2 * tiers.count(1) + 3 * tiers.count(3) + 1
+    tier-0 levels, one k_cluster per run of cluster-tier levels, k_explore + k_compact per
+    top-down level, k_fb_clear + k_fb_set + k_bottom_up per bottom-up level (NEXT-3),
+    k_finalize."""
+    tiers = [int(t) for t in st["tier"] if t in (0, 1, 3, 4)]
+
+    def runs(tier):
+        return sum(1 for i, t in enumerate(tiers) if t == tier and (i == 0 or tiers[i - 1] != tier))
+
+    return 1 + runs(0) + runs(4) + 2 * tiers.count(1) + 3 * tiers.count(3) + 1
 
 
 def shard_sources(srcs, rank: int, world: int) -> list:

@@ -46,12 +46,6 @@ namespace s3bfs {
 #ifndef S3BFS_KX_FAST
 #define S3BFS_KX_FAST 1   // uniform-row fast path
 #endif
-#ifndef S3BFS_KS_LOCKSTEP
-#define S3BFS_KS_LOCKSTEP 0
-#endif
-#ifndef S3BFS_KS_BATCHED
-#define S3BFS_KS_BATCHED 1
-#endif
 #ifndef S3BFS_KX_RANK
 #define S3BFS_KX_RANK 1   // rank (REDUX + POPC) edge->row mapping for multi-row batches
 #endif
@@ -1147,18 +1141,6 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
     int ev[KS_IPT], ux[KS_IPT], lo[KS_IPT], hi[KS_IPT];
 #pragma unroll
     for (int i = 0; i < KS_IPT; ++i) { lo[i] = 0; hi[i] = n_l; }
-#if S3BFS_KS_LOCKSTEP
-    for (int span = n_l; span > 1; span = (span + 1) >> 1) {  // the KS_IPT searches in lock-step
-#pragma unroll
-      for (int i = 0; i < KS_IPT; ++i) {
-        const int e = tid + i * KS_THREADS;
-        if (hi[i] - lo[i] > 1) {
-          const int mid = (lo[i] + hi[i]) >> 1;
-          if (sex[mid] <= e) lo[i] = mid; else hi[i] = mid;
-        }
-      }
-    }
-#else
 #pragma unroll
     for (int i = 0; i < KS_IPT; ++i) {
       const int e = tid + i * KS_THREADS;
@@ -1169,7 +1151,6 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
         }
       }
     }
-#endif
 #pragma unroll
     for (int i = 0; i < KS_IPT; ++i) {
       const int e = tid + i * KS_THREADS;
@@ -1205,7 +1186,6 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
     const int e0 = tid * ipt;
     int kv[KS_IPT], kr[KS_IPT], kd[KS_IPT];
     int cnt = 0, dsum = 0;
-#if S3BFS_KS_BATCHED
     int4 vis[KS_IPT];  // all record loads first (one round trip for the thread's items)
 #pragma unroll
     for (int i = 0; i < KS_IPT; ++i) {
@@ -1227,26 +1207,6 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
         atomicOr(P.bm + (v >> 5), 1u << (v & 31));  // exact visited bit (not discovery)
       }
     }
-#else
-#pragma unroll
-    for (int i = 0; i < KS_IPT; ++i) {
-      kv[i] = -1;
-      kr[i] = 0;
-      kd[i] = 0;
-      const int e = e0 + i;
-      if (i < ipt && e < e_l) {
-        const int v = cv[e];
-        if (v >= 0) {
-          const int4 vi = ld_weak_v4(vinfo + v);  // same-SM writes: L1-coherent
-          if (vi.w == e) {
-            kv[i] = vi.z; kr[i] = vi.x; kd[i] = vi.y;
-            P.lp[v] = make_int2(L + 1, cpv[e]);         // d[v] <- l, parent (Fig1 L18)
-            atomicOr(P.bm + (v >> 5), 1u << (v & 31));  // exact visited bit (not discovery)
-          }
-        }
-      }
-    }
-#endif
 #pragma unroll
     for (int i = 0; i < KS_IPT; ++i) {
       cnt += kv[i] >= 0;
