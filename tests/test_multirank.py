@@ -55,3 +55,15 @@ def test_single_rank_is_plain():
     g, ms, tot = bench.job_throughput(2.0, 4e9, "cpu", 1)
     assert ms == 2.0 and tot == 4e9 and abs(g - 2000.0) < 1e-9
     assert bench.shard_sources([1, 2, 3], 0, 1) == [1, 2, 3]
+
+
+def test_launch_count_from_tier_sequence():
+    """bench.py's gpu_launches: k_init + one k_small per tier-0 run + one k_cluster per
+    cluster run + 2 per top-down level + 3 per bottom-up level + k_finalize (tier 2 = a last
+    level with nothing to explore launches nothing)."""
+    sys.path.insert(0, ROOT)
+    import numpy as np
+    import bench
+    st = {"tier": np.array([0, 0, 4, 4, 1, 1, 3, 1, 4, 0, 0, 2])}
+    assert bench.launches_from_stats(st) == 1 + 2 + 2 + 2 * 3 + 3 * 1 + 1
+    assert bench.launches_from_stats({"tier": np.array([2])}) == 2
