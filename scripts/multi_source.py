@@ -6,6 +6,9 @@ import json
 import os
 import sys
 
+# K concurrent streams need K hardware work queues (default 8): set before CUDA initialises
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
@@ -18,6 +21,7 @@ ap.add_argument("--ks", default="1,4,16,64")
 ap.add_argument("--traversals", type=int, default=128)
 ap.add_argument("--direction", type=int, default=0)
 ap.add_argument("--stats", type=int, default=-1)
+ap.add_argument("--cluster", type=int, default=0, help="options.cluster_max_edges (-1: off)")
 a = ap.parse_args()
 out = {"what": __doc__.strip().splitlines()[0], "configs": {}}
 for cfg in a.configs.split(","):
@@ -25,7 +29,8 @@ for cfg in a.configs.split(","):
     ro = torch.from_numpy(g.row_offsets).cuda()
     col = torch.from_numpy(g.col_indices).cuda()
     deg = (ro[1:] - ro[:-1]).to(torch.int64)
-    base = pkg.S3BFS(ro, col, pkg.Options(direction=a.direction, collect_stats=a.stats))
+    base = pkg.S3BFS(ro, col, pkg.Options(direction=a.direction, collect_stats=a.stats,
+                                           cluster_max_edges=a.cluster))
     srcs = g.sources
     m_c = {}
     lv = torch.empty(g.n, dtype=torch.int32, device="cuda")
