@@ -73,6 +73,9 @@ namespace s3bfs {
 #ifndef S3BFS_BU_P
 #define S3BFS_BU_P 2
 #endif
+#ifndef S3BFS_KC_GROUPS
+#define S3BFS_KC_GROUPS 4
+#endif
 #ifndef S3BFS_BM_NC
 #define S3BFS_BM_NC 1     // bitmap probes through the non-coherent (read-only) path
 #endif
@@ -81,7 +84,7 @@ constexpr int KD_MIN_BLOCKS = S3BFS_KD_MINB;    // CTAs per SM the register budg
 constexpr int KD_WARPS = KD_THREADS / 32;
 constexpr int KD_SLACK = 64;                    // candidate-buffer slack per CTA
 constexpr int KX_GROUPS = S3BFS_KX_GROUPS;      // 32-edge groups per batch and warp
-constexpr int KC_GROUPS = 4;                    // 32-candidate groups per k_compact round
+constexpr int KC_GROUPS = S3BFS_KC_GROUPS;      // 32-candidate groups per k_compact round
 constexpr int KS_THREADS = 1024;                // k_small CTA size
 constexpr int KS_ECAP = 8192;                   // T0 maximum (edges per tier-0 level)
 constexpr int KS_NCAP = KS_ECAP;                // frontier capacity of tier 0 (kept <= e_l)
