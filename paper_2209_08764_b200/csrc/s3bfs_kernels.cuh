@@ -216,6 +216,13 @@ __device__ __forceinline__ int4 ldg_stream4(const int32_t *p, unsigned long long
 #endif
   return v;
 }
+// 1 << k for 0 <= k < 32, else 0 (PTX shl clamps shift amounts >= 32; k < 0 is a huge
+// unsigned amount)
+__device__ __forceinline__ unsigned shl1(int k) {
+  unsigned r;
+  asm("shl.b32 %0, 1, %1;" : "=r"(r) : "r"(k));
+  return r;
+}
 // rotate right by (k mod 32): bit 0 of the result is bit (k mod 32) of w (one SHF.WRAP)
 __device__ __forceinline__ uint32_t rotr32(uint32_t w, int k) {
   uint32_t r;
@@ -661,17 +668,18 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
       // r + popc(mask & bits 0..i); the batch's first edge lies in row j0)
       const unsigned le = 0xffffffffu >> (31 - lane);  // bits 0 .. lane
       const int pfirst = __shfl_sync(0xffffffffu, wb, j0) + e;  // col index of edge e (valid)
+      const int lb = bend - e - lane;  // group g's lane is inside the batch iff 32 g < lb
       int r = j0;
 #pragma unroll
       for (int g = 0; g < KX_GROUPS; ++g) {
         const int eg = e + g * 32;
         const int rel = wex - eg;  // this window lane's row start relative to the group
-        const unsigned m = __reduce_or_sync(0xffffffffu, ((unsigned)rel < 32u) ? (1u << rel) : 0u);
+        const unsigned m = __reduce_or_sync(0xffffffffu, shl1(rel));  // starts in [eg, eg+31]
         if (g == 0) r -= (int)(m & 1u);  // a row starting exactly at e is row j0 itself
         const int j = r + __popc(m & le);
         xv[g] = __shfl_sync(0xffffffffu, wx, j);
         const int pos = __shfl_sync(0xffffffffu, wb, j) + eg + lane;
-        const bool ok = eg + lane < bend;
+        const bool ok = g * 32 < lb;
         const int t = ldg_stream(col + (ok ? pos : pfirst), pol_stream);  // unconditional
         v[g] = ok ? t : vs;
         r += __popc(m);
