@@ -1038,11 +1038,13 @@ __device__ void tiny_levels(const Params &P, Ctl *c, int32_t *sf, int32_t *srs, 
   int frs = lane < n_l ? srs[lane] : 0;
   int fex = lane < n_l ? sex[lane] : 0x7fffffff;
   for (;;) {
-    int u = 0;
+    int u = 0;  // this lane's frontier slot (a one-vertex frontier, e.g. a path: slot 0)
+    if (n_l > 1) {
 #pragma unroll
-    for (int s = 16; s >= 1; s >>= 1) {
-      const int cu = __shfl_sync(0xffffffffu, fex, u + s);
-      if (cu <= lane) u += s;
+      for (int s = 16; s >= 1; s >>= 1) {
+        const int cu = __shfl_sync(0xffffffffu, fex, u + s);
+        if (cu <= lane) u += s;
+      }
     }
     const int px = __shfl_sync(0xffffffffu, fx, u);
     const int pr = __shfl_sync(0xffffffffu, frs, u);
@@ -1061,12 +1063,22 @@ __device__ void tiny_levels(const Params &P, Ctl *c, int32_t *sf, int32_t *srs, 
       atomicOr(P.bm + (v >> 5), 1u << (v & 31));      // exact visited bit
     }
     const int d = keep ? vi.y : 0;
-    const int inc = warp_incl_scan(d);
-    const int n_next = __popc(km), e_next = __shfl_sync(0xffffffffu, inc, 31);
-    const int src = lane < n_next ? (int)__fns(km, 0, lane + 1) : 0;
-    const int nfx = __shfl_sync(0xffffffffu, vi.z, src);
-    const int nfr = __shfl_sync(0xffffffffu, vi.x, src);
-    const int nfe = __shfl_sync(0xffffffffu, inc - d, src);
+    const int n_next = __popc(km);
+    int e_next, nfx, nfr, nfe;
+    if (n_next == 1) {  // one kept vertex (a path): no scan, one source lane
+      const int src = __ffs(km) - 1;
+      e_next = __shfl_sync(0xffffffffu, d, src);
+      nfx = __shfl_sync(0xffffffffu, vi.z, src);
+      nfr = __shfl_sync(0xffffffffu, vi.x, src);
+      nfe = 0;
+    } else {
+      const int inc = warp_incl_scan(d);
+      e_next = __shfl_sync(0xffffffffu, inc, 31);
+      const int src = lane < n_next ? (int)__fns(km, 0, lane + 1) : 0;
+      nfx = __shfl_sync(0xffffffffu, vi.z, src);
+      nfr = __shfl_sync(0xffffffffu, vi.x, src);
+      nfe = __shfl_sync(0xffffffffu, inc - d, src);
+    }
     if (lane == 0) {
       const unsigned long long t = globaltimer();
       record_stat_at(P, nrec, L, n_l, e_l, TIER_SMALL, ncand, n_next, t_prev, t);
