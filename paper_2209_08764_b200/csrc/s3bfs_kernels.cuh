@@ -1054,10 +1054,14 @@ __device__ void tiny_levels(const Params &P, Ctl *c, int32_t *sf, int32_t *srs, 
     const uint32_t w = __ldcg(P.bm + (v >> 5));      // published by atomicOr at L2
     const int4 vi = __ldg(P.vinfo + v);               // issued together with the bitmap word
     const bool fresh = has && !((w >> (v & 31)) & 1u);
-    const unsigned mm = __match_any_sync(0xffffffffu, fresh ? v : -1 - lane);
-    const bool keep = fresh && lane == __ffs(mm) - 1;
-    const unsigned km = __ballot_sync(0xffffffffu, keep);
-    const int ncand = __popc(__ballot_sync(0xffffffffu, fresh));
+    const unsigned fm = __ballot_sync(0xffffffffu, fresh);
+    const int ncand = __popc(fm);
+    bool keep = fresh;  // at most one fresh lane (a path level): nothing to deduplicate
+    if (ncand > 1) {
+      const unsigned mm = __match_any_sync(0xffffffffu, fresh ? v : -1 - lane);
+      keep = fresh && lane == __ffs(mm) - 1;
+    }
+    const unsigned km = ncand > 1 ? __ballot_sync(0xffffffffu, keep) : fm;
     if (keep) {
       P.lp[v] = make_int2(L + 1, px);                 // d[v] <- l, parent (Fig1 L18)
       atomicOr(P.bm + (v >> 5), 1u << (v & 31));      // exact visited bit
