@@ -100,6 +100,8 @@ constexpr int KC_THREADS = 1024;
 constexpr int KC_ECTA = 4096;                    // level edges per CTA (e_l <= 32,768)
 constexpr int KC_FCAP = 8192;                    // replicated frontier capacity
 constexpr int KC_IPT = KC_ECTA / KC_THREADS;
+// k_small / k_cluster scan their per-warp totals with warp 0 reading one entry per lane
+static_assert(KS_THREADS == 1024 && KC_THREADS == 1024, "tier-0 / cluster CTAs must have 32 warps");
 constexpr int BU_W = S3BFS_BU_W;   // bottom-up: bitmap words per warp round
 constexpr int BU_P = S3BFS_BU_P;   // bottom-up: in-neighbours probed per vertex per round
 
