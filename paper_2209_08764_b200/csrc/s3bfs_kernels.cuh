@@ -13,14 +13,20 @@
 //   k_init     Fig1 L1-L8   visited bitmap <- {s}, claim tags <- 0, frontier = [s], d[s] = 0
 //   k_explore  (c)+(d)      Fig1 L17-L18: equal edge slices per warp, start vertex by a
 //                           32-ary warp search of the degree scan (R8), coalesced col stream,
-//                           visited test (bitmap, then a per-level claim tag), d/parent/Owner
+//                           visited test (bitmap, then a per-level claim tag at a hashed
+//                           slot, R26), d/parent/Owner
 //                           labelling with plain stores -- the benign race, no atomic
 //                           instruction.
 //   k_compact  (e)+(a)+(b)  Fig1 L19-L29 + L12-L15 of the NEXT level: keep cand[k] iff
 //                           Owner[cand[k]] == k, decoupled look-back scan of (kept, degree-sum)
 //                           pairs across CTAs, write f_next / row starts / degree scan.
 //   k_small    tier 0 (f)   one CTA runs whole levels (a)-(e) in shared memory while the level
-//                           stays tiny (P:22 -- "never use more cores than necessary").
+//                           stays tiny (P:22 -- "never use more cores than necessary");
+//                           its warp 0 alone runs levels of <= 32 edges (tiny_levels).
+//   k_cluster  (f) middle   one 8-CTA thread-block cluster runs consecutive mid-size levels,
+//                           frontier replicated through distributed shared memory.
+//   k_fb_clear/k_fb_set/k_bottom_up   NEXT-3 bottom-up levels (direction-optimising option).
+//   k_merge_min/k_merge_keep          NEXT-4 cross-rank merge (one traversal over G ranks).
 //   k_finalize              d[0:n-1] and parent in caller ids ("Returns d[0:n-1]").
 //   k_scan_u32 (b) alone    test entry: the same look-back scan over a plain int32 array.
 //   k_find_start (c) alone  test entry: the same warp search, one warp per worker.
