@@ -169,3 +169,25 @@ def test_gpu_dist_argument_checks():
         r.merge(torch.zeros((1, 4), dtype=torch.int32, device="cuda"), [2, 0], 1)
     r.close()
     plain.close()
+
+
+@pytest.mark.gpu
+def test_gpu_dist_clone():
+    """A clone of a dist handle (shared prepared graph, own workspace) runs the protocol too."""
+    pkg = pytest.importorskip("paper_2209_08764_b200")
+    import paper_2209_08764_b200.dist as pd
+    g = _graphs()[4]  # rand-directed
+    ranks = _gpu_ranks(g, 2)
+    clones = []
+    for r in ranks:
+        c = pd.DistRank.__new__(pd.DistRank)
+        c.rank, c.size, c.n, c.device, c.stream = r.rank, r.size, r.n, r.device, None
+        c.row_offsets, c.col_indices = r.row_offsets, r.col_indices
+        c.handle = pkg.s3bfs_clone(r.handle)
+        c.level, c.parent = torch.empty_like(r.level), torch.empty_like(r.parent)
+        clones.append(c)
+    for s in (0, g.n - 1):
+        for lv, pa in pd.traverse(clones, s):
+            _check(g, s, lv.cpu().numpy(), pa.cpu().numpy())
+    for c in clones + ranks:
+        c.close()

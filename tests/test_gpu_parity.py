@@ -327,3 +327,18 @@ def test_maximum_size_sparse(kw):
     lv, _ = check_traversal(g, bfs, unreached, stats=False)  # isolated source: only itself
     assert (lv >= 0).sum() == 1
     bfs.close()
+
+
+@pytest.mark.parametrize("kw", [dict(collect_stats=-1), dict(collect_stats=-1, loop_mode=2),
+                                dict(collect_stats=-1, tier0_max_edges=16)],
+                         ids=["graph", "host-loop", "cluster-T0-16"])
+def test_stats_off(kw):
+    """Per-level statistics off (no level records, tier-0/cluster record counter unused):
+    the traversal itself is unchanged."""
+    for name, g in TINY + [("rmat12", graphgen.rmat(12, 16, seed=5))]:
+        ro, col = to_dev(g)
+        bfs = pkg.S3BFS(ro, col, pkg.Options(debug_poison=1, **kw))
+        srcs = range(g.n) if g.n <= 16 else sorted({0, g.n // 3, g.n - 1})
+        for s in srcs:
+            check_traversal(g, bfs, s, stats=False)
+        bfs.close()
