@@ -33,6 +33,8 @@ extern "C" int kx_micro(const int32_t *col, int n, int n_l, int e_l, int32_t *f,
     P.pol_first = h_pol[0];
     P.pol_last = h_pol[1];
   }
+  P.dist_size = 1; P.dist_rank = 0;
+  P.v_sent = (int)(((size_t)n + 127) / 128 * 128);
   P.p_max = p_max; P.grain = grain; P.t0 = -1;
   P.nnz = 0x7fffffff;  // harness: col has 4 KB of padding (see kx_micro.py)
   P.col_vec = (((uintptr_t)col) & 15) == 0;
@@ -41,6 +43,7 @@ extern "C" int kx_micro(const int32_t *col, int n, int n_l, int e_l, int32_t *f,
   const long long chunk = ((long long)e_l + pt - 1) / pt;
   Ctl h{};
   h.level = level_no; h.n_l = n_l; h.e_l = e_l; h.cur = 0; h.tier = TIER_LARGE;
+  h.e_lo = 0; h.e_hi = e_l;  // single GPU: the whole level's edge range
   h.p_l = (int)(((long long)e_l + chunk - 1) / chunk); h.chunk = (int)chunk;
   h.wcap = (int)((chunk + KD_WARPS - 1) / KD_WARPS);
   h.level_out = level; h.parent_out = parent;
