@@ -34,7 +34,6 @@ extern "C" int kx_micro(const int32_t *col, int n, int n_l, int e_l, int32_t *f,
     P.pol_last = h_pol[1];
   }
   P.dist_size = 1; P.dist_rank = 0;
-  P.v_sent = (int)(((size_t)n + 127) / 128 * 128);
   P.p_max = p_max; P.grain = grain; P.t0 = -1;
   P.nnz = 0x7fffffff;  // harness: col has 4 KB of padding (see kx_micro.py)
   P.col_vec = (((uintptr_t)col) & 15) == 0;
