@@ -1,7 +1,7 @@
-"""One-off full-scale check (test infrastructure use of oracle/): every BASELINE source of the
+"""Test infrastructure (may use oracle/; not collected by pytest): one-off full-scale check, every BASELINE source of the
 given configs, top-down and direction-optimising, levels bit-exact and parents by certificate."""
 import sys, os, time
-sys.path.insert(0, os.getcwd())
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch, graphgen, oracle, paper_2209_08764_b200 as pkg
 for cfg in sys.argv[1:]:
     g = graphgen.make_config(cfg)
