@@ -102,6 +102,21 @@ bool is_device_ptr(const void *p) {
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// A stream-ordered temporary freed (cudaFreeAsync on its stream) when it leaves scope, so an
+// early error return cannot leak it.
+struct AsyncTmp {
+  void *p = nullptr;
+  cudaStream_t st;
+  explicit AsyncTmp(cudaStream_t s) : st(s) {}
+  AsyncTmp(const AsyncTmp &) = delete;
+  AsyncTmp &operator=(const AsyncTmp &) = delete;
+  ~AsyncTmp() {
+    if (p) cudaFreeAsync(p, st);
+  }
+  cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, bytes, st); }
+  template <class T> T *as() const { return static_cast<T *>(p); }
+};
+
 int init_grid(const s3bfs_ctx *h) {
   long long want = ((long long)h->n / 4 + 255) / 256;
   long long cap = (long long)h->num_sms * 8;
@@ -132,16 +147,18 @@ s3bfs_status build_reordered(s3bfs_ctx *h, cudaStream_t st) {
   char *g = (char *)h->gs->g2;
   int32_t *col2 = (int32_t *)(g + o_col2);
   int32_t *n2o = (int32_t *)(g + o_n2o), *o2n = (int32_t *)(g + o_o2n);
-  int32_t *deg = nullptr, *deg_sorted = nullptr, *iota = nullptr;
   int32_t *ro2 = (int32_t *)(g + o_ro2);
-  void *tmp = nullptr;
+  AsyncTmp deg_b(st), degs_b(st), iota_b(st), tmp_b(st), status_b(st), nz_b(st);
   size_t tmp_bytes = 0;
-  CK(h, cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, deg, deg_sorted, iota,
-                                                  n2o, n, 0, 32, st));
-  CK(h, cudaMallocAsync((void **)&deg, (size_t)n * 4, st));
-  CK(h, cudaMallocAsync((void **)&deg_sorted, (size_t)n * 4, st));
-  CK(h, cudaMallocAsync((void **)&iota, (size_t)n * 4, st));
-  CK(h, cudaMallocAsync(&tmp, tmp_bytes, st));
+  CK(h, cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, (int32_t *)nullptr,
+                                                  (int32_t *)nullptr, (int32_t *)nullptr, n2o,
+                                                  n, 0, 32, st));
+  CK(h, deg_b.alloc((size_t)n * 4));
+  CK(h, degs_b.alloc((size_t)n * 4));
+  CK(h, iota_b.alloc((size_t)n * 4));
+  CK(h, tmp_b.alloc(tmp_bytes));
+  int32_t *deg = deg_b.as<int32_t>(), *deg_sorted = degs_b.as<int32_t>(), *iota = iota_b.as<int32_t>();
+  void *tmp = tmp_b.p;
   const int grid = h->num_sms * 8;
   k_degrees<<<grid, 256, 0, st>>>(h->ro, n, deg, iota);
   CK(h, cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, deg, deg_sorted, iota, n2o, n,
@@ -149,24 +166,19 @@ s3bfs_status build_reordered(s3bfs_ctx *h, cudaStream_t st) {
   k_inverse_perm<<<grid, 256, 0, st>>>(n2o, n, o2n, h->ro, deg);  // deg <- internal degrees
   // ro2 = exclusive scan of the internal degrees: the look-back scan kernel (b)
   const int tiles = (int)(((long long)n + SCAN_TILE - 1) / SCAN_TILE);
-  unsigned long long *status = nullptr;
-  CK(h, cudaMallocAsync((void **)&status, (size_t)tiles * 8, st));
+  CK(h, status_b.alloc((size_t)tiles * 8));
+  unsigned long long *status = status_b.as<unsigned long long>();
   CK(h, cudaMemsetAsync(status, 0, (size_t)tiles * 8, st));
   k_scan_u32<<<tiles, SCAN_THREADS, 0, st>>>(deg, ro2, n, status);
   k_relabel_rows<<<h->num_sms * 16, 256, 0, st>>>(h->ro, h->col, n2o, o2n, ro2, n, col2);
   k_build_vinfo<<<grid, 256, 0, st>>>(ro2, n2o, n, h->P.vinfo);
-  int *d_nz = nullptr, h_nz = 0;
-  CK(h, cudaMallocAsync((void **)&d_nz, 4, st));
+  int h_nz = 0;
+  CK(h, nz_b.alloc(4));
+  int *d_nz = nz_b.as<int>();
   CK(h, cudaMemsetAsync(d_nz, 0, 4, st));
   k_count_nonzero<<<grid, 256, 0, st>>>(deg, n, d_nz);  // internal degrees, descending
   CK(h, cudaMemcpyAsync(&h_nz, d_nz, 4, cudaMemcpyDeviceToHost, st));
-  cudaFreeAsync(d_nz, st);
   CK(h, cudaGetLastError());
-  cudaFreeAsync(status, st);
-  cudaFreeAsync(tmp, st);
-  cudaFreeAsync(iota, st);
-  cudaFreeAsync(deg_sorted, st);
-  cudaFreeAsync(deg, st);
   CK(h, cudaStreamSynchronize(st));
   h->P.col = col2;
   h->P.n2o = n2o;
@@ -181,14 +193,14 @@ s3bfs_status build_reordered(s3bfs_ctx *h, cudaStream_t st) {
 s3bfs_status sort_rows(s3bfs_ctx *h, const int32_t *ro, const int32_t *in, int32_t *out,
                        cudaStream_t st) {
   if (h->nnz == 0) return S3BFS_OK;
-  void *tmp = nullptr;
+  AsyncTmp tmp(st);
   size_t bytes = 0;
   CK(h, cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, in, out, (int)h->nnz, h->n, ro,
                                            ro + 1, st));
-  CK(h, cudaMallocAsync(&tmp, bytes, st));
-  CK(h, cub::DeviceSegmentedSort::SortKeys(tmp, bytes, in, out, (int)h->nnz, h->n, ro, ro + 1,
+  CK(h, tmp.alloc(bytes));
+  CK(h, cub::DeviceSegmentedSort::SortKeys(tmp.p, bytes, in, out, (int)h->nnz, h->n, ro, ro + 1,
                                            st));
-  cudaFreeAsync(tmp, st);
+  CK(h, cudaStreamSynchronize(st));  // the sort has consumed tmp before it is released
   return S3BFS_OK;
 }
 
@@ -200,12 +212,13 @@ s3bfs_status build_in_adjacency(s3bfs_ctx *h, cudaStream_t st) {
   const int n = h->n;
   const long long nnz = h->nnz;
   const int32_t *ro = h->ro_int, *col = h->P.col;
-  unsigned long long *d_h = nullptr, hh[2] = {0, 0};
-  CK(h, cudaMallocAsync((void **)&d_h, 16, st));
+  unsigned long long hh[2] = {0, 0};
+  AsyncTmp dh_b(st), tuns_b(st), tdeg_b(st), status_b(st);
+  CK(h, dh_b.alloc(16));
+  unsigned long long *d_h = dh_b.as<unsigned long long>();
   CK(h, cudaMemsetAsync(d_h, 0, 16, st));
   k_sym_hash<<<h->num_sms * 16, 256, 0, st>>>(ro, col, n, d_h);
   CK(h, cudaMemcpyAsync(hh, d_h, 16, cudaMemcpyDeviceToHost, st));
-  cudaFreeAsync(d_h, st);
   CK(h, cudaStreamSynchronize(st));
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return o; };
@@ -222,15 +235,14 @@ s3bfs_status build_in_adjacency(s3bfs_ctx *h, cudaStream_t st) {
     h->P.tcol = tcol;
     return S3BFS_OK;
   }
-  int32_t *tunsorted = nullptr;
-  CK(h, cudaMallocAsync((void **)&tunsorted, (size_t)nnz * 4 + 16, st));
-  int32_t *tdeg = nullptr;
-  CK(h, cudaMallocAsync((void **)&tdeg, (size_t)n * 4, st));
+  CK(h, tuns_b.alloc((size_t)nnz * 4 + 16));
+  CK(h, tdeg_b.alloc((size_t)n * 4));
+  int32_t *tunsorted = tuns_b.as<int32_t>(), *tdeg = tdeg_b.as<int32_t>();
   CK(h, cudaMemsetAsync(tdeg, 0, (size_t)n * 4, st));
   k_in_degree<<<h->num_sms * 16, 256, 0, st>>>(ro, col, n, tdeg);
   const int tiles = (int)(((long long)n + SCAN_TILE - 1) / SCAN_TILE);
-  unsigned long long *status = nullptr;
-  CK(h, cudaMallocAsync((void **)&status, (size_t)tiles * 8, st));
+  CK(h, status_b.alloc((size_t)tiles * 8));
+  unsigned long long *status = status_b.as<unsigned long long>();
   CK(h, cudaMemsetAsync(status, 0, (size_t)tiles * 8, st));
   k_scan_u32<<<tiles, SCAN_THREADS, 0, st>>>(tdeg, tro, n, status);
   CK(h, cudaMemcpyAsync(tdeg, tro, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));  // cursors
@@ -238,9 +250,6 @@ s3bfs_status build_in_adjacency(s3bfs_ctx *h, cudaStream_t st) {
   CK(h, cudaGetLastError());
   s3bfs_status ss = sort_rows(h, tro, tunsorted, tcol, st);
   if (ss != S3BFS_OK) return ss;
-  cudaFreeAsync(tunsorted, st);
-  cudaFreeAsync(status, st);
-  cudaFreeAsync(tdeg, st);
   CK(h, cudaStreamSynchronize(st));
   h->P.tro = tro;
   h->P.tcol = tcol;
@@ -534,13 +543,13 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
       return bail(cuda_fail(h, e, "copy vertex records"));
   }
   if (!share && h->opt.validate_csr) {
-    int *d_err = nullptr;
     int h_err = 0;
-    if ((e = cudaMallocAsync((void **)&d_err, 4, stream)) != cudaSuccess) return bail(cuda_fail(h, e, "cudaMallocAsync"));
+    AsyncTmp err_b(stream);
+    if ((e = err_b.alloc(4)) != cudaSuccess) return bail(cuda_fail(h, e, "cudaMallocAsync"));
+    int *d_err = err_b.as<int>();
     cudaMemsetAsync(d_err, 0, 4, stream);
     k_validate<<<h->num_sms * 8, 256, 0, stream>>>(row_offsets, col_indices, n, nnz, d_err);
     cudaMemcpyAsync(&h_err, d_err, 4, cudaMemcpyDeviceToHost, stream);
-    cudaFreeAsync(d_err, stream);
     if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) return bail(cuda_fail(h, e, "validate_csr"));
     if (h_err) {
       std::string m = "CSR invalid:";
@@ -566,11 +575,12 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
     if (ts != S3BFS_OK) return bail(ts);
   }
   {  // L2 policy descriptors (uniform kernel parameters of k_explore)
-    unsigned long long *d_pol = nullptr, h_pol[2] = {0, 0};
-    if ((e = cudaMallocAsync((void **)&d_pol, 16, stream)) != cudaSuccess) return bail(cuda_fail(h, e, "cudaMallocAsync"));
+    unsigned long long h_pol[2] = {0, 0};
+    AsyncTmp pol_b(stream);
+    if ((e = pol_b.alloc(16)) != cudaSuccess) return bail(cuda_fail(h, e, "cudaMallocAsync"));
+    unsigned long long *d_pol = pol_b.as<unsigned long long>();
     k_policies<<<1, 1, 0, stream>>>(d_pol);
     cudaMemcpyAsync(h_pol, d_pol, 16, cudaMemcpyDeviceToHost, stream);
-    cudaFreeAsync(d_pol, stream);
     if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) return bail(cuda_fail(h, e, "k_policies"));
     P.pol_first = h_pol[0];
     P.pol_last = h_pol[1];
@@ -852,13 +862,13 @@ s3bfs_status s3bfs_debug_exclusive_scan(const int32_t *in, int32_t *out, int32_t
     return e == cudaSuccess ? S3BFS_OK : cuda_fail(nullptr, e, "memset");
   }
   const int tiles = (int)(((long long)n + SCAN_TILE - 1) / SCAN_TILE);
-  unsigned long long *status = nullptr;
-  cudaError_t e = cudaMallocAsync((void **)&status, (size_t)tiles * 8, stream);
+  AsyncTmp status_b(stream);
+  cudaError_t e = status_b.alloc((size_t)tiles * 8);
   if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaMallocAsync(status)");
+  unsigned long long *status = status_b.as<unsigned long long>();
   cudaMemsetAsync(status, 0, (size_t)tiles * 8, stream);
   k_scan_u32<<<tiles, SCAN_THREADS, 0, stream>>>(in, out, n, status);
   e = cudaGetLastError();
-  cudaFreeAsync(status, stream);
   return e == cudaSuccess ? S3BFS_OK : cuda_fail(nullptr, e, "k_scan_u32");
 }
 
