@@ -474,6 +474,13 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   const size_t o_fb0 = take(bm_bytes), o_fb1 = take(bm_bytes);
   const size_t o_wcnt = take((size_t)p_max * KD_WARPS * 4);
   const size_t o_status = take((size_t)p_max * 8);
+  // NEXT-3 bottom-up tiles: width = the power of two >= words / (tiles-per-CTA x P_max), at
+  // least 64 words (one BU_W-word round for each of a CTA's 16 warps)
+  const long long bu_words = (((long long)n + 127) >> 7) << 2;
+  int bu_tile_w = 64;
+  while ((long long)bu_tile_w * S3BFS_BU_TILES_PER_CTA * p_max < bu_words) bu_tile_w <<= 1;
+  const int bu_tiles = h->opt.direction == 1 ? (int)((bu_words + bu_tile_w - 1) / bu_tile_w) : 0;
+  const size_t o_bustatus = take((size_t)(bu_tiles + 1) * 8);
   const size_t o_ctl = take(sizeof(Ctl));
   const size_t o_stats = take((size_t)stats_cap * sizeof(s3bfs_level_stat));
   // NEXT-4 (dist_size > 1 only): records, per-vertex lowest keeping rank, merge look-back
@@ -506,6 +513,9 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   P.fb[1] = (uint32_t *)(base + o_fb1);
   P.wcnt = (int32_t *)(base + o_wcnt);
   P.status = (unsigned long long *)(base + o_status);
+  P.bu_status = (unsigned long long *)(base + o_bustatus);
+  P.bu_tiles = bu_tiles;
+  P.bu_tile_w = bu_tile_w;
   P.stats = (s3bfs_level_stat *)(base + o_stats);
   P.stats_cap = stats_cap;
   P.p_max = p_max;

@@ -82,6 +82,9 @@ namespace s3bfs {
 #ifndef S3BFS_KC_GROUPS
 #define S3BFS_KC_GROUPS 4
 #endif
+#ifndef S3BFS_BU_TILES_PER_CTA
+#define S3BFS_BU_TILES_PER_CTA 4  // bottom-up: about this many tiles per resident CTA
+#endif
 #ifndef S3BFS_BM_NC
 #define S3BFS_BM_NC 1     // bitmap probes through the non-coherent (read-only) path
 #endif
@@ -173,6 +176,8 @@ struct Params {
   int32_t tc_max;               // cluster tier: levels with t0 < e_l <= tc_max (< 0: off)
   int32_t direction, do_alpha, do_beta;  // NEXT-3 switch rule (Beamer): alpha, beta
   int32_t n_scan;               // bottom-up scans internal ids [0, n_scan): the ones with deg > 0
+  unsigned long long *bu_status;  // NEXT-3: look-back words of the bottom-up tiles
+  int32_t bu_tiles, bu_tile_w;  // NEXT-3: bottom-up tiles and their width (bitmap words)
   int32_t dist_size, dist_rank; // NEXT-4 (replicated graph, level edges split over ranks); 1, 0
   int4 *rec;                    // NEXT-4: this rank's kept vertices {internal id, parent, row
                                 //  start, degree}, exchanged by all-gather
@@ -1503,7 +1508,7 @@ __global__ void k_fb_clear(Params P) {
   if (c->tier != TIER_BU) return;
   const long long gs = (long long)gridDim.x * blockDim.x;
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  for (long long i = g; i < P.p_max; i += gs) P.status[i] = 0ull;  // k_bottom_up's look-back
+  for (long long i = g; i < P.bu_tiles; i += gs) P.bu_status[i] = 0ull;  // k_bottom_up's look-back
   if (c->fb_valid) return;
   const long long nw4 = ((long long)P.n + 127) >> 7;
   uint4 *fb = reinterpret_cast<uint4 *>(P.fb[c->cur]);
@@ -1533,9 +1538,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params 
   __shared__ int32_t s_k[KD_WARPS], s_d[KD_WARPS];
   __shared__ int s_last, s_tile;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_tile = (int)atomicAdd(&c->tile_ctr, 1u);  // look-back order = start order
-  __syncthreads();
-  const int b = s_tile, nb = gridDim.x;
+  const int nb = gridDim.x, nt = P.bu_tiles;
   const int cur = c->cur, nxt = cur ^ 1;
   const int new_level = c->level + 1;
   const int4 *__restrict__ vinfo = P.vinfo;
@@ -1544,8 +1547,17 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params 
   uint32_t *__restrict__ bm = P.bm;
   const int nwords = (int)((((long long)P.n + 127) >> 7) << 2);
   const int nscan = P.n_scan;
-  const int wpc = (nwords + nb - 1) / nb;
-  const int w0 = min(b * wpc, nwords), w1 = min(w0 + wpc, nwords);
+  // Tiles of bu_tile_w bitmap words (about S3BFS_BU_TILES_PER_CTA per resident CTA, >= 64),
+  // taken in start order by the resident CTAs until none is
+  // left: a tile of long fruitless scans (vertices with no frontier in-neighbour read their
+  // whole row) holds up one CTA, not the grid (CTA-sized fixed ranges left most warps waiting
+  // at the look-back barrier).
+  for (;;) {
+  if (tid == 0) s_tile = (int)atomicAdd(&c->tile_ctr, 1u);  // look-back order = start order
+  __syncthreads();
+  const int b = s_tile;
+  if (b >= nt) break;
+  const int w0 = min(b * P.bu_tile_w, nwords), w1 = min(w0 + P.bu_tile_w, nwords);
   if (b == 0 && tid == 0) c->t_kx_begin = globaltimer();
   // pass 1: BU_W words per warp round (BU_W independent probe chains per lane); every round
   // probes the next BU_P in-neighbours of each unresolved vertex, loads issued together
@@ -1613,12 +1625,12 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params 
     const int ik = warp_incl_scan(kk), id = warp_incl_scan(dd);
     const Pair agg{(uint32_t)__shfl_sync(0xffffffffu, ik, 31),
                    (uint32_t)__shfl_sync(0xffffffffu, id, 31)};
-    const Pair ex = lookback<true>(P.status, b, agg);
+    const Pair ex = lookback<true>(P.bu_status, b, agg);
     if (lane < KD_WARPS) {
       s_k[lane] = (int)ex.a + ik - kk;
       s_d[lane] = (int)ex.b + id - dd;
     }
-    if (b == nb - 1 && lane == 0) {
+    if (b == nt - 1 && lane == 0) {
       const int n_next = (int)(ex.a + agg.a), e_next = (int)(ex.b + agg.b);
       c->n_next = n_next;
       c->e_next = e_next;
@@ -1645,6 +1657,8 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params 
     koff += __popc(m);
     doff += __shfl_sync(0xffffffffu, inc, 31);
   }
+  __syncthreads();  // s_tile, s_k, s_d are reused by the next tile
+  }  // tiles
   __threadfence();
   __syncthreads();
   if (tid == 0) s_last = atomicAdd(&c->done_ctr, 1u) == (unsigned)(nb - 1);
