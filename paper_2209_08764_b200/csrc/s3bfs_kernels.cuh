@@ -85,6 +85,9 @@ namespace s3bfs {
 #ifndef S3BFS_BU_TILES_PER_CTA
 #define S3BFS_BU_TILES_PER_CTA 4  // bottom-up: about this many tiles per resident CTA
 #endif
+#ifndef S3BFS_LB_MAX_NS
+#define S3BFS_LB_MAX_NS 128  // look-back backoff cap (ns; 1024 measured 0.2-0.6 % slower)
+#endif
 #ifndef S3BFS_BM_NC
 #define S3BFS_BM_NC 1     // bitmap probes through the non-coherent (read-only) path
 #endif
@@ -378,7 +381,7 @@ __device__ Pair lookback(unsigned long long *status, int tile, Pair agg) {
     const unsigned need = firstP >= 31 ? 0xffffffffu : ((2u << firstP) - 1u);
     if (mI & need) {  // a predecessor has not published yet
       __nanosleep(ns);
-      if (ns < 1024) ns <<= 1;
+      if (ns < S3BFS_LB_MAX_NS) ns <<= 1;
       continue;
     }
     Pair v = (lane <= firstP) ? unpack<PAIR>(s) : Pair{0, 0};
