@@ -52,6 +52,9 @@ namespace s3bfs {
 #ifndef S3BFS_KX_FAST
 #define S3BFS_KX_FAST 1   // uniform-row fast path
 #endif
+#ifndef S3BFS_KX_LAZY_PARENT
+#define S3BFS_KX_LAZY_PARENT 1  // keep the window slot per group; shuffle the parent on discovery
+#endif
 #ifndef S3BFS_KX_RANK
 #define S3BFS_KX_RANK 1   // rank (REDUX + POPC) edge->row mapping for multi-row batches
 #endif
@@ -620,7 +623,8 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
     load_window(u0);
   }
   // Map the batch of edges [e, e_next) onto lanes and load their targets: v[g] = col entry of
-  // edge e + 32g + lane (-1 outside the batch), xv[g] = its frontier vertex (caller id).
+  // edge e + 32g + lane (-1 outside the batch), xv[g] = its frontier vertex: the window slot
+  // (S3BFS_KX_LAZY_PARENT; the caller id is shuffled only on discovery) or the caller id.
   auto map_load = [&](int e, int (&v)[KX_GROUPS], int (&xv)[KX_GROUPS]) -> int {
     while (lim <= e) {  // window exhausted (also skips runs of zero-degree vertices, C9)
       u0 += 32;
@@ -634,7 +638,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
     int e_next = min(e + KX_GROUPS * 32, bend);
     if (S3BFS_KX_FAST && row_end >= e_next) {
       // the whole batch lies in one frontier row (most R-MAT arcs): uniform x and base
-      const int x = __shfl_sync(0xffffffffu, wx, j0);
+      const int x = S3BFS_KX_LAZY_PARENT ? j0 : __shfl_sync(0xffffffffu, wx, j0);
       const int base = __shfl_sync(0xffffffffu, wb, j0);
       const int start = base + e;  // col index of the batch's first edge
       const int a0 = start & ~3;   // 16-byte aligned
@@ -693,7 +697,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
         const unsigned m = __reduce_or_sync(0xffffffffu, shl1(rel));  // starts in [eg, eg+31]
         if (g == 0) r -= (int)(m & 1u);  // a row starting exactly at e is row j0 itself
         const int j = r + __popc(m & le);
-        xv[g] = __shfl_sync(0xffffffffu, wx, j);
+        xv[g] = S3BFS_KX_LAZY_PARENT ? j : __shfl_sync(0xffffffffu, wx, j);
         const int pos = __shfl_sync(0xffffffffu, wb, j) + eg + lane;
         const bool ok = g * 32 < lb;
         const int t = ldg_stream(col + (ok ? pos : pfirst), pol_stream);  // unconditional
@@ -710,7 +714,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
           const int cj = __shfl_sync(0xffffffffu, wex, min(j + s, 31));
           if (j + s <= 31 && cj <= my_e) j += s;
         }
-        xv[g] = __shfl_sync(0xffffffffu, wx, j);
+        xv[g] = S3BFS_KX_LAZY_PARENT ? j : __shfl_sync(0xffffffffu, wx, j);
         const int pos = __shfl_sync(0xffffffffu, wb, j) + my_e;
         const int pf = __shfl_sync(0xffffffffu, wb, j0) + e;
         const int t = ldg_stream(col + (my_e < bend ? pos : pf), pol_stream);
@@ -744,12 +748,14 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
 #pragma unroll
       for (int g = 0; g < KX_GROUPS; ++g) {
         if (!((wneed >> g) & 1u)) continue;
+        // parent: the window slot's caller id (the window is unchanged since map_load)
+        const int par = S3BFS_KX_LAZY_PARENT ? __shfl_sync(0xffffffffu, wx, xv[g]) : xv[g];
         const bool disc = cl[g] != tag;
         const unsigned m = __ballot_sync(0xffffffffu, disc);
         if (disc) {
           const int slot = segbase + wcount + __popc(m & lanemask_lt());
           st_u8(claim + claim_slot(P, v[g]), tag);
-          st_weak_v2(lp + v[g], new_level, xv[g]);   // d[v] <- l, parent (Fig1 L18)
+          st_weak_v2(lp + v[g], new_level, par);     // d[v] <- l, parent (Fig1 L18)
           st_weak(owner_of(vinfo, v[g]), slot);      // Owner[v] <- i (benign race)
           cand[slot] = v[g];                         // Q[i].Enqueue(v)
         }
