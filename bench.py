@@ -122,17 +122,27 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def launches_from_stats(st) -> int:
+def launches_from_stats(st, td_chain: int = 1, bu_chain: int = 1) -> int:
     """Kernel launches of one traversal in graph mode: k_init, one k_small per run of
-    tier-0 levels, one k_cluster per run of cluster-tier levels, k_explore + k_compact per
-    top-down level, k_fb_clear + k_fb_set + k_bottom_up per bottom-up level (NEXT-3),
-    k_finalize."""
+    tier-0 levels, one k_cluster per run of cluster-tier levels, k_finalize, and per run of L
+    consecutive top-down (bottom-up, NEXT-3) levels ceil(L / td_chain) (ceil(L / bu_chain))
+    entries into the body, each launching td_chain (k_explore, k_compact) pairs (bu_chain
+    (k_fb_clear, k_fb_set, k_bottom_up) triples); surplus ones return at once but launch."""
     tiers = [int(t) for t in st["tier"] if t in (0, 1, 3, 4)]
 
-    def runs(tier):
-        return sum(1 for i, t in enumerate(tiers) if t == tier and (i == 0 or tiers[i - 1] != tier))
+    def run_lengths(tier):
+        out, k = [], 0
+        for i, t in enumerate(tiers):
+            if t == tier:
+                k += 1
+            if k and (t != tier or i == len(tiers) - 1):
+                out.append(k)
+                k = 0
+        return out
 
-    return 1 + runs(0) + runs(4) + 2 * tiers.count(1) + 3 * tiers.count(3) + 1
+    td = sum(-(-L // td_chain) for L in run_lengths(1)) * 2 * td_chain
+    bu = sum(-(-L // bu_chain) for L in run_lengths(3)) * 3 * bu_chain
+    return 1 + len(run_lengths(0)) + len(run_lengths(4)) + td + bu + 1
 
 
 def shard_sources(srcs, rank: int, world: int) -> list:
@@ -240,7 +250,8 @@ def main():
         pkg.s3bfs_run_ptr(bfs.handle, s, lp, pp, sp)
         st = bfs.level_stats()
         m_c = int(deg[level >= 0].sum().item())
-        per[s] = {"m_c": m_c, "levels": int(len(st)), "launches": launches_from_stats(st),
+        per[s] = {"m_c": m_c, "levels": int(len(st)), "launches": launches_from_stats(
+            st, *((info["td_chain"], info["bu_chain"]) if args.loop_mode != 2 else (1, 1))),
                   "stats": st}
     verified = {"sources": 0, "levels_bit_exact": True, "parents_valid": True}
     cpu_times, cpu_edges = [], []

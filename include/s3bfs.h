@@ -60,7 +60,7 @@ typedef struct {
   int32_t edges_per_cta;   /* grain of (f): P_l = min(P_max, ceil(e_l / grain)).  0 -> 2048 */
   int32_t tier0_max_edges; /* T0: a level with e_l <= T0 (and n_l <= 8192) runs in the
                               single-CTA tier.  0 -> 8192 (the maximum); < 0 -> tier 0 off */
-  int32_t loop_mode;       /* 0/1: level loop captured in a CUDA graph (WHILE + IF nodes);
+  int32_t loop_mode;       /* 0/1: level loop captured in a CUDA graph (WHILE + SWITCH nodes);
                               2: host-driven loop (one device->host read per level; run then
                               blocks until the traversal ends) */
   int32_t collect_stats;   /* 0/1: per-level statistics on; -1: off */
@@ -144,10 +144,14 @@ s3bfs_status s3bfs_last_error(s3bfs_handle h, const char **msg);
 s3bfs_status s3bfs_get_level_stats(s3bfs_handle h, s3bfs_level_stat *out, int32_t cap,
                                    int32_t *num_levels);
 
-/* Device-side tunables the handle resolved (for reports): P_max, grain, T0, CTA sizes. */
+/* Device-side tunables the handle resolved (for reports): P_max, grain, T0, CTA sizes, and
+ * td_chain / bu_chain = the (k_explore, k_compact) pairs / (k_fb_clear, k_fb_set,
+ * k_bottom_up) triples the captured loop runs per entry into the top-down / bottom-up body
+ * (consecutive levels of one direction; surplus ones return at once). */
 typedef struct {
   int32_t num_sms, p_max, edges_per_cta, tier0_max_edges;
   int32_t kd_threads, kd_tile_edges, ksmall_threads, ksmall_max_frontier;
+  int32_t td_chain, bu_chain;
   int64_t workspace_bytes;
 } s3bfs_info;
 s3bfs_status s3bfs_get_info(s3bfs_handle h, s3bfs_info *out);

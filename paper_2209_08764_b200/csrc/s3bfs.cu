@@ -6,13 +6,15 @@
 //   s3bfs_run:  graph { k_init (Fig1 L1-L8);
 //                       WHILE(n_l > 0) {                                   Fig1 L9
 //                         SWITCH(tier): 0 { k_small }                      (f) tier 0
-//                                       1 { k_explore; k_compact }         (c)(d) / (e)(a)(b)
-//                                       2 { k_fb_clear; k_fb_set; k_bottom_up }   NEXT-3
+//                                       1 { (k_explore; k_compact) x 4 }   (c)(d) / (e)(a)(b)
+//                                       2 { (k_fb_clear; k_fb_set; k_bottom_up) x 3 } NEXT-3
 //                                       3 { k_cluster: consecutive mid-size levels }  (f)
 //                       }
 //                       k_finalize }
 //   The kernel that decides a level's successor sets the conditional handles (no dispatch
 //   kernel); k_init's per-run arguments are patched into the executable graph per run.
+//   Bodies 1 and 2 chain S3BFS_TD_CHAIN pairs / S3BFS_BU_CHAIN triples so consecutive levels
+//   of one direction skip a conditional round trip; kernels of another tier return at once.
 //
 // The host crosses the host/device boundary once per traversal (enqueue); the level loop,
 // P_l and every per-level decision stay on the device (SURVEY.md s.8(a) row f, H6).
@@ -257,6 +259,12 @@ s3bfs_status build_in_adjacency(s3bfs_ctx *h, cudaStream_t st) {
   return S3BFS_OK;
 }
 
+#ifndef S3BFS_TD_CHAIN
+#define S3BFS_TD_CHAIN 4  // top-down (k_explore, k_compact) pairs per SWITCH body
+#endif
+#ifndef S3BFS_BU_CHAIN
+#define S3BFS_BU_CHAIN 3  // bottom-up (k_fb_clear, k_fb_set, k_bottom_up) triples per body
+#endif
 s3bfs_status build_graph(s3bfs_ctx *h) {
   cudaGraph_t g = nullptr;
   CK(h, cudaGraphCreate(&g, 0));
@@ -320,11 +328,17 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
   cudaGraphNode_t ks;
   cudaKernelNodeParams kks = kparams((void *)k_small, 1, KS_THREADS, h->ks_smem);
   CK(h, cudaGraphAddKernelNode(&ks, b0, nullptr, 0, &kks));
-  cudaGraphNode_t kx, kc;
-  cudaKernelNodeParams kkx = kparams((void *)k_explore, h->P.p_max, KD_THREADS, 0);
-  CK(h, cudaGraphAddKernelNode(&kx, b1, nullptr, 0, &kkx));
-  cudaKernelNodeParams kkc = kparams((void *)k_compact, h->P.p_max, KD_THREADS, 0);
-  CK(h, cudaGraphAddKernelNode(&kc, b1, &kx, 1, &kkc));
+  {  // body 1: S3BFS_TD_CHAIN (k_explore, k_compact) pairs -- consecutive top-down levels
+     // without a conditional round trip; a pair whose level is not top-down returns at once
+    cudaGraphNode_t kc = nullptr;
+    for (int k = 0; k < S3BFS_TD_CHAIN; ++k) {
+      cudaGraphNode_t kx;
+      cudaKernelNodeParams kkx = kparams((void *)k_explore, h->P.p_max, KD_THREADS, 0);
+      CK(h, cudaGraphAddKernelNode(&kx, b1, kc ? &kc : nullptr, kc ? 1 : 0, &kkx));
+      cudaKernelNodeParams kkc = kparams((void *)k_compact, h->P.p_max, KD_THREADS, 0);
+      CK(h, cudaGraphAddKernelNode(&kc, b1, &kx, 1, &kkc));
+    }
+  }
   {  // body 3: the cluster tier (one 8-CTA cluster, consecutive mid-size levels)
     cudaGraph_t b3 = sp.conditional.phGraph_out[3];
     cudaGraphNode_t kcl;
@@ -332,14 +346,18 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
     CK(h, cudaGraphAddKernelNode(&kcl, b3, nullptr, 0, &kkcl));
   }
   if (h->P.direction) {  // NEXT-3: body 2 { k_fb_clear; k_fb_set; k_bottom_up }
+    // S3BFS_BU_CHAIN triples: consecutive bottom-up levels without a conditional round trip
     cudaGraph_t b2 = sp.conditional.phGraph_out[2];
-    cudaGraphNode_t fc, fs, bu;
-    cudaKernelNodeParams kfc = kparams((void *)k_fb_clear, h->num_sms * 4, 256, 0);
-    CK(h, cudaGraphAddKernelNode(&fc, b2, nullptr, 0, &kfc));
-    cudaKernelNodeParams kfs = kparams((void *)k_fb_set, h->num_sms * 4, 256, 0);
-    CK(h, cudaGraphAddKernelNode(&fs, b2, &fc, 1, &kfs));
-    cudaKernelNodeParams kbu = kparams((void *)k_bottom_up, h->P.p_max, KD_THREADS, 0);
-    CK(h, cudaGraphAddKernelNode(&bu, b2, &fs, 1, &kbu));
+    cudaGraphNode_t bu = nullptr;
+    for (int k = 0; k < S3BFS_BU_CHAIN; ++k) {
+      cudaGraphNode_t fc, fs;
+      cudaKernelNodeParams kfc = kparams((void *)k_fb_clear, h->num_sms * 4, 256, 0);
+      CK(h, cudaGraphAddKernelNode(&fc, b2, bu ? &bu : nullptr, bu ? 1 : 0, &kfc));
+      cudaKernelNodeParams kfs = kparams((void *)k_fb_set, h->num_sms * 4, 256, 0);
+      CK(h, cudaGraphAddKernelNode(&fs, b2, &fc, 1, &kfs));
+      cudaKernelNodeParams kbu = kparams((void *)k_bottom_up, h->P.p_max, KD_THREADS, 0);
+      CK(h, cudaGraphAddKernelNode(&bu, b2, &fs, 1, &kbu));
+    }
   }
 
   CK(h, cudaGraphInstantiate(&h->exec, g, 0));
@@ -859,6 +877,8 @@ s3bfs_status s3bfs_get_info(s3bfs_handle h, s3bfs_info *out) {
   out->kd_tile_edges = KX_GROUPS * 32;
   out->ksmall_threads = KS_THREADS;
   out->ksmall_max_frontier = KS_NCAP;
+  out->td_chain = S3BFS_TD_CHAIN;
+  out->bu_chain = S3BFS_BU_CHAIN;
   out->workspace_bytes = (int64_t)(h->ws_bytes + (h->gs ? h->gs->b2 + h->gs->b3 : 0));
   return S3BFS_OK;
 }

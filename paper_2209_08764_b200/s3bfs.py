@@ -68,6 +68,7 @@ class Info(ctypes.Structure):
                 ("edges_per_cta", ctypes.c_int32), ("tier0_max_edges", ctypes.c_int32),
                 ("kd_threads", ctypes.c_int32), ("kd_tile_edges", ctypes.c_int32),
                 ("ksmall_threads", ctypes.c_int32), ("ksmall_max_frontier", ctypes.c_int32),
+                ("td_chain", ctypes.c_int32), ("bu_chain", ctypes.c_int32),
                 ("workspace_bytes", ctypes.c_int64)]
 
 

@@ -67,3 +67,12 @@ def test_launch_count_from_tier_sequence():
     st = {"tier": np.array([0, 0, 4, 4, 1, 1, 3, 1, 4, 0, 0, 2])}
     assert bench.launches_from_stats(st) == 1 + 2 + 2 + 2 * 3 + 3 * 1 + 1
     assert bench.launches_from_stats({"tier": np.array([2])}) == 2
+    # top-down runs [1, 1] and [1] with 4 pairs per body entry: 2 entries x 4 pairs x 2
+    assert bench.launches_from_stats(st, td_chain=4) == 1 + 2 + 2 + 2 * 4 * 2 + 3 * 1 + 1
+    five = {"tier": np.array([0, 1, 1, 1, 1, 1, 0, 2])}  # one run of 5: 2 entries of 3 pairs
+    assert bench.launches_from_stats(five, td_chain=3) == 1 + 2 + 2 * 3 * 2 + 1
+    assert bench.launches_from_stats(five, td_chain=1) == 1 + 2 + 2 * 5 + 1
+    # one bottom-up run of one level, 3 triples per entry: 1 entry x 3 x 3 launches
+    assert bench.launches_from_stats(st, td_chain=4, bu_chain=3) == 1 + 2 + 2 + 16 + 9 + 1
+    bu4 = {"tier": np.array([1, 3, 3, 3, 3, 1, 2])}  # bottom-up run of 4: 2 entries of 3
+    assert bench.launches_from_stats(bu4, td_chain=1, bu_chain=3) == 1 + 2 * 2 + 2 * 3 * 3 + 1
