@@ -122,27 +122,30 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def launches_from_stats(st, td_chain: int = 1, bu_chain: int = 1) -> int:
-    """Kernel launches of one traversal in graph mode: k_init, one k_small per run of
-    tier-0 levels, one k_cluster per run of cluster-tier levels, k_finalize, and per run of L
-    consecutive top-down (bottom-up, NEXT-3) levels ceil(L / td_chain) (ceil(L / bu_chain))
-    entries into the body, each launching td_chain (k_explore, k_compact) pairs (bu_chain
-    (k_fb_clear, k_fb_set, k_bottom_up) triples); surplus ones return at once but launch."""
-    tiers = [int(t) for t in st["tier"] if t in (0, 1, 3, 4)]
-
-    def run_lengths(tier):
-        out, k = [], 0
-        for i, t in enumerate(tiers):
-            if t == tier:
-                k += 1
-            if k and (t != tier or i == len(tiers) - 1):
-                out.append(k)
-                k = 0
-        return out
-
-    td = sum(-(-L // td_chain) for L in run_lengths(1)) * 2 * td_chain
-    bu = sum(-(-L // bu_chain) for L in run_lengths(3)) * 3 * bu_chain
-    return 1 + len(run_lengths(0)) + len(run_lengths(4)) + td + bu + 1
+def launches_from_stats(st, td_chain: int = 1, bu_chain: int = 1, universal: int = 0,
+                        direction: int = 0) -> int:
+    """Kernel launches of one traversal in graph mode, replaying the captured loop over the
+    level tiers: k_init; per WHILE iteration the SWITCH body of the current level's tier --
+    S (k_small: a whole run of tier-0 levels), C (k_cluster: a whole run of cluster levels),
+    T (k_explore + k_compact: one top-down level), B (k_fb_clear + k_fb_set + k_bottom_up:
+    one bottom-up level, NEXT-3) -- where a body is its own tier (T x td_chain, B x bu_chain)
+    or, universal, the sequence S C T^td [B^bu T^td] C S from its tier on; every kernel of a
+    body launches (idle ones return at once); then k_finalize."""
+    tiers = [{0: "S", 1: "T", 3: "B", 4: "C"}[int(t)] for t in st["tier"] if t in (0, 1, 3, 4)]
+    seq = "SC" + "T" * td_chain + ("B" * bu_chain + "T" * td_chain if direction else "") + "CS"
+    cost = {"S": 1, "C": 1, "T": 2, "B": 3}
+    n, i = 1, 0
+    while i < len(tiers):
+        t = tiers[i]
+        body = (seq[seq.index(t):] if universal
+                else t * (td_chain if t == "T" else bu_chain if t == "B" else 1))
+        for k in body:
+            n += cost[k]
+            if i < len(tiers) and tiers[i] == k:
+                i += 1
+                while k in "SC" and i < len(tiers) and tiers[i] == k:
+                    i += 1
+    return n + 1
 
 
 def shard_sources(srcs, rank: int, world: int) -> list:
@@ -251,7 +254,8 @@ def main():
         st = bfs.level_stats()
         m_c = int(deg[level >= 0].sum().item())
         per[s] = {"m_c": m_c, "levels": int(len(st)), "launches": launches_from_stats(
-            st, *((info["td_chain"], info["bu_chain"]) if args.loop_mode != 2 else (1, 1))),
+            st, *((info["td_chain"], info["bu_chain"], info["universal_body"], args.direction)
+                  if args.loop_mode != 2 else (1, 1, 0, 0))),
                   "stats": st}
     verified = {"sources": 0, "levels_bit_exact": True, "parents_valid": True}
     cpu_times, cpu_edges = [], []

@@ -262,6 +262,9 @@ s3bfs_status build_in_adjacency(s3bfs_ctx *h, cudaStream_t st) {
 #ifndef S3BFS_TD_CHAIN
 #define S3BFS_TD_CHAIN 4  // top-down (k_explore, k_compact) pairs per SWITCH body
 #endif
+#ifndef S3BFS_UNIVERSAL_BODY
+#define S3BFS_UNIVERSAL_BODY 1  // every SWITCH body chains the rest of a traversal's tiers
+#endif
 #ifndef S3BFS_BU_CHAIN
 #define S3BFS_BU_CHAIN 3  // bottom-up (k_fb_clear, k_fb_set, k_bottom_up) triples per body
 #endif
@@ -315,7 +318,19 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
     k.kernelParams = args;
     return k;
   };
-  // one SWITCH per WHILE iteration: body 0 tier 0, body 1 top-down, body 2 bottom-up
+  // One SWITCH per WHILE iteration selects the body of the tier the next level runs in:
+  // body 0 tier 0, body 1 top-down, body 2 bottom-up (NEXT-3), body 3 the cluster tier.
+  // Each body is a chain of tier kernels; every kernel returns at once unless the current
+  // level is of its tier, so a chain runs consecutive levels of changing tiers kernel to
+  // kernel, without a conditional round trip (k_small / k_cluster run a whole run of their
+  // levels per launch, a (k_explore, k_compact) pair or a bottom-up triple one level).
+  // S3BFS_UNIVERSAL_BODY: body t is the canonical sequence of a traversal from tier t on,
+  //   S C T^td C S (top-down) or S C T^td B^bu T^td C S (direction-optimising);
+  // otherwise body t = its own tier only (S, T^td, B^bu, C).
+  const std::string seq = std::string("SC") + std::string(S3BFS_TD_CHAIN, 'T') +
+      (h->P.direction ? std::string(S3BFS_BU_CHAIN, 'B') + std::string(S3BFS_TD_CHAIN, 'T')
+                      : std::string()) + "CS";
+  const char body_tier[4] = {'S', 'T', 'B', 'C'};
   cudaGraphNodeParams sp = {};
   sp.type = cudaGraphNodeTypeConditional;
   sp.conditional.handle = ht;
@@ -323,40 +338,36 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
   sp.conditional.size = 4;  // body 2 stays empty without NEXT-3
   cudaGraphNode_t snode;
   CK(h, cudaGraphAddNode(&snode, body, nullptr, 0, &sp));
-  cudaGraph_t b0 = sp.conditional.phGraph_out[0];
-  cudaGraph_t b1 = sp.conditional.phGraph_out[1];
-  cudaGraphNode_t ks;
-  cudaKernelNodeParams kks = kparams((void *)k_small, 1, KS_THREADS, h->ks_smem);
-  CK(h, cudaGraphAddKernelNode(&ks, b0, nullptr, 0, &kks));
-  {  // body 1: S3BFS_TD_CHAIN (k_explore, k_compact) pairs -- consecutive top-down levels
-     // without a conditional round trip; a pair whose level is not top-down returns at once
-    cudaGraphNode_t kc = nullptr;
-    for (int k = 0; k < S3BFS_TD_CHAIN; ++k) {
-      cudaGraphNode_t kx;
-      cudaKernelNodeParams kkx = kparams((void *)k_explore, h->P.p_max, KD_THREADS, 0);
-      CK(h, cudaGraphAddKernelNode(&kx, b1, kc ? &kc : nullptr, kc ? 1 : 0, &kkx));
-      cudaKernelNodeParams kkc = kparams((void *)k_compact, h->P.p_max, KD_THREADS, 0);
-      CK(h, cudaGraphAddKernelNode(&kc, b1, &kx, 1, &kkc));
-    }
-  }
-  {  // body 3: the cluster tier (one 8-CTA cluster, consecutive mid-size levels)
-    cudaGraph_t b3 = sp.conditional.phGraph_out[3];
-    cudaGraphNode_t kcl;
-    cudaKernelNodeParams kkcl = kparams((void *)k_cluster, KC_CL, KC_THREADS, h->kc_smem);
-    CK(h, cudaGraphAddKernelNode(&kcl, b3, nullptr, 0, &kkcl));
-  }
-  if (h->P.direction) {  // NEXT-3: body 2 { k_fb_clear; k_fb_set; k_bottom_up }
-    // S3BFS_BU_CHAIN triples: consecutive bottom-up levels without a conditional round trip
-    cudaGraph_t b2 = sp.conditional.phGraph_out[2];
-    cudaGraphNode_t bu = nullptr;
-    for (int k = 0; k < S3BFS_BU_CHAIN; ++k) {
-      cudaGraphNode_t fc, fs;
-      cudaKernelNodeParams kfc = kparams((void *)k_fb_clear, h->num_sms * 4, 256, 0);
-      CK(h, cudaGraphAddKernelNode(&fc, b2, bu ? &bu : nullptr, bu ? 1 : 0, &kfc));
-      cudaKernelNodeParams kfs = kparams((void *)k_fb_set, h->num_sms * 4, 256, 0);
-      CK(h, cudaGraphAddKernelNode(&fs, b2, &fc, 1, &kfs));
-      cudaKernelNodeParams kbu = kparams((void *)k_bottom_up, h->P.p_max, KD_THREADS, 0);
-      CK(h, cudaGraphAddKernelNode(&bu, b2, &fs, 1, &kbu));
+  for (int bi = 0; bi < 4; ++bi) {
+    if (bi == 2 && !h->P.direction) continue;
+    const char t = body_tier[bi];
+    std::string chain = S3BFS_UNIVERSAL_BODY ? seq.substr(seq.find(t))
+                      : t == 'T' ? std::string(S3BFS_TD_CHAIN, 'T')
+                      : t == 'B' ? std::string(S3BFS_BU_CHAIN, 'B') : std::string(1, t);
+    cudaGraph_t bg = sp.conditional.phGraph_out[bi];
+    cudaGraphNode_t prev = nullptr;
+    auto add = [&](void *fn, int grid, int block, size_t smem) -> s3bfs_status {
+      cudaGraphNode_t nd;
+      cudaKernelNodeParams kp = kparams(fn, grid, block, smem);
+      CK(h, cudaGraphAddKernelNode(&nd, bg, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
+      prev = nd;
+      return S3BFS_OK;
+    };
+    for (const char k : chain) {
+      s3bfs_status r = S3BFS_OK;
+      if (k == 'S') {
+        r = add((void *)k_small, 1, KS_THREADS, h->ks_smem);
+      } else if (k == 'C') {
+        r = add((void *)k_cluster, KC_CL, KC_THREADS, h->kc_smem);
+      } else if (k == 'T') {
+        r = add((void *)k_explore, h->P.p_max, KD_THREADS, 0);
+        if (r == S3BFS_OK) r = add((void *)k_compact, h->P.p_max, KD_THREADS, 0);
+      } else {  // 'B'
+        r = add((void *)k_fb_clear, h->num_sms * 4, 256, 0);
+        if (r == S3BFS_OK) r = add((void *)k_fb_set, h->num_sms * 4, 256, 0);
+        if (r == S3BFS_OK) r = add((void *)k_bottom_up, h->P.p_max, KD_THREADS, 0);
+      }
+      if (r != S3BFS_OK) return r;
     }
   }
 
@@ -879,6 +890,8 @@ s3bfs_status s3bfs_get_info(s3bfs_handle h, s3bfs_info *out) {
   out->ksmall_max_frontier = KS_NCAP;
   out->td_chain = S3BFS_TD_CHAIN;
   out->bu_chain = S3BFS_BU_CHAIN;
+  out->universal_body = S3BFS_UNIVERSAL_BODY;
+  out->reserved = 0;
   out->workspace_bytes = (int64_t)(h->ws_bytes + (h->gs ? h->gs->b2 + h->gs->b3 : 0));
   return S3BFS_OK;
 }

@@ -76,3 +76,12 @@ def test_launch_count_from_tier_sequence():
     assert bench.launches_from_stats(st, td_chain=4, bu_chain=3) == 1 + 2 + 2 + 16 + 9 + 1
     bu4 = {"tier": np.array([1, 3, 3, 3, 3, 1, 2])}  # bottom-up run of 4: 2 entries of 3
     assert bench.launches_from_stats(bu4, td_chain=1, bu_chain=3) == 1 + 2 * 2 + 2 * 3 * 3 + 1
+    # universal bodies (S C T^td C S from the entry tier on): [S S T T T S] runs in one entry
+    td = {"tier": np.array([0, 0, 1, 1, 1, 0, 2])}
+    assert bench.launches_from_stats(td, td_chain=4, universal=1) == 1 + (1 + 1 + 8 + 1 + 1) + 1
+    # a top-down run longer than the chain re-enters at T: S C T^2 C S, then T^2 C S
+    td5 = {"tier": np.array([0, 1, 1, 1, 0])}
+    assert bench.launches_from_stats(td5, td_chain=2, universal=1) == 1 + 8 + 6 + 1
+    # direction-optimising sequence S C T^1 B^2 T^1 C S; entry at B for a bottom-up start
+    do = {"tier": np.array([1, 3, 3, 1, 4, 0])}
+    assert bench.launches_from_stats(do, 1, 2, universal=1, direction=1) == 1 + (2 + 6 + 2 + 1 + 1) + 1
