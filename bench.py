@@ -123,22 +123,24 @@ class ClockSampler:
 
 
 def launches_from_stats(st, td_chain: int = 1, bu_chain: int = 1, universal: int = 0,
-                        direction: int = 0) -> int:
+                        direction: int = 0, prologue: int = 0) -> int:
     """Kernel launches of one traversal in graph mode, replaying the captured loop over the
     level tiers: k_init; per WHILE iteration the SWITCH body of the current level's tier --
     S (k_small: a whole run of tier-0 levels), C (k_cluster: a whole run of cluster levels),
     T (k_explore + k_compact: one top-down level), B (k_fb_clear + k_fb_set + k_bottom_up:
     one bottom-up level, NEXT-3) -- where a body is its own tier (T x td_chain, B x bu_chain)
-    or, universal, the sequence S C T^td [B^bu T^td] C S from its tier on; every kernel of a
-    body launches (idle ones return at once); then k_finalize."""
+    or, universal, the sequence S C T^td [B^bu T^td] C S from its tier on; with prologue that
+    whole sequence first runs once between k_init and the loop; every kernel of a chain
+    launches (idle ones return at once); then k_finalize."""
     tiers = [{0: "S", 1: "T", 3: "B", 4: "C"}[int(t)] for t in st["tier"] if t in (0, 1, 3, 4)]
     seq = "SC" + "T" * td_chain + ("B" * bu_chain + "T" * td_chain if direction else "") + "CS"
     cost = {"S": 1, "C": 1, "T": 2, "B": 3}
-    n, i = 1, 0
-    while i < len(tiers):
-        t = tiers[i]
-        body = (seq[seq.index(t):] if universal
+    n, i, first = 1, 0, bool(prologue)
+    while i < len(tiers) or first:
+        t = tiers[i] if i < len(tiers) else "S"
+        body = (seq if first else seq[seq.index(t):] if universal
                 else t * (td_chain if t == "T" else bu_chain if t == "B" else 1))
+        first = False
         for k in body:
             n += cost[k]
             if i < len(tiers) and tiers[i] == k:
@@ -254,8 +256,8 @@ def main():
         st = bfs.level_stats()
         m_c = int(deg[level >= 0].sum().item())
         per[s] = {"m_c": m_c, "levels": int(len(st)), "launches": launches_from_stats(
-            st, *((info["td_chain"], info["bu_chain"], info["universal_body"], args.direction)
-                  if args.loop_mode != 2 else (1, 1, 0, 0))),
+            st, *((info["td_chain"], info["bu_chain"], info["universal_body"], args.direction,
+                   info["prologue"]) if args.loop_mode != 2 else (1, 1, 0, 0, 0))),
                   "stats": st}
     verified = {"sources": 0, "levels_bit_exact": True, "parents_valid": True}
     cpu_times, cpu_edges = [], []

@@ -149,11 +149,13 @@ s3bfs_status s3bfs_get_level_stats(s3bfs_handle h, s3bfs_level_stat *out, int32_
  * k_bottom_up) triples the captured loop runs per entry into the top-down / bottom-up body
  * (consecutive levels of one direction; surplus ones return at once); universal_body = 1:
  * every body continues with the kernels of the tiers that usually follow (S C T^td [B^bu
- * T^td] C S from its own tier on, S = k_small, C = k_cluster, T = pair, B = triple). */
+ * T^td] C S from its own tier on, S = k_small, C = k_cluster, T = pair, B = triple);
+ * prologue = 1 (top-down handles): that whole sequence also runs once between k_init and the
+ * WHILE node, so a typical traversal needs no conditional round trip at all. */
 typedef struct {
   int32_t num_sms, p_max, edges_per_cta, tier0_max_edges;
   int32_t kd_threads, kd_tile_edges, ksmall_threads, ksmall_max_frontier;
-  int32_t td_chain, bu_chain, universal_body, reserved;
+  int32_t td_chain, bu_chain, universal_body, prologue;
   int64_t workspace_bytes;
 } s3bfs_info;
 s3bfs_status s3bfs_get_info(s3bfs_handle h, s3bfs_info *out);

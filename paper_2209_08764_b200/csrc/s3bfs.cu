@@ -265,9 +265,13 @@ s3bfs_status build_in_adjacency(s3bfs_ctx *h, cudaStream_t st) {
 #ifndef S3BFS_UNIVERSAL_BODY
 #define S3BFS_UNIVERSAL_BODY 1  // every SWITCH body chains the rest of a traversal's tiers
 #endif
+#ifndef S3BFS_GRAPH_PROLOGUE
+#define S3BFS_GRAPH_PROLOGUE 1  // the canonical tier sequence once before the WHILE node
+#endif
 #ifndef S3BFS_BU_CHAIN
 #define S3BFS_BU_CHAIN 3  // bottom-up (k_fb_clear, k_fb_set, k_bottom_up) triples per body
 #endif
+bool graph_prologue(const s3bfs_ctx *h) { return S3BFS_GRAPH_PROLOGUE && !h->P.direction; }
 s3bfs_status build_graph(s3bfs_ctx *h) {
   cudaGraph_t g = nullptr;
   CK(h, cudaGraphCreate(&g, 0));
@@ -296,19 +300,6 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
     ki.kernelParams = iargs;
     CK(h, cudaGraphAddKernelNode(&h->init_node, g, nullptr, 0, &ki));
   }
-  cudaGraphNode_t wnode;
-  CK(h, cudaGraphAddNode(&wnode, g, &h->init_node, 1, &wp));
-  cudaGraph_t body = wp.conditional.phGraph_out[0];
-
-  {  // after the loop: d[0:n-1] and parent in caller ids
-    cudaKernelNodeParams kf = {};
-    kf.func = (void *)k_finalize;
-    kf.gridDim = dim3(finalize_grid(h));
-    kf.blockDim = dim3(256);
-    kf.kernelParams = args;
-    cudaGraphNode_t fnode;
-    CK(h, cudaGraphAddKernelNode(&fnode, g, &wnode, 1, &kf));
-  }
   auto kparams = [&](void *fn, int grid, int block, size_t smem) {
     cudaKernelNodeParams k = {};
     k.func = fn;
@@ -318,34 +309,17 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
     k.kernelParams = args;
     return k;
   };
-  // One SWITCH per WHILE iteration selects the body of the tier the next level runs in:
-  // body 0 tier 0, body 1 top-down, body 2 bottom-up (NEXT-3), body 3 the cluster tier.
-  // Each body is a chain of tier kernels; every kernel returns at once unless the current
-  // level is of its tier, so a chain runs consecutive levels of changing tiers kernel to
-  // kernel, without a conditional round trip (k_small / k_cluster run a whole run of their
-  // levels per launch, a (k_explore, k_compact) pair or a bottom-up triple one level).
-  // S3BFS_UNIVERSAL_BODY: body t is the canonical sequence of a traversal from tier t on,
-  //   S C T^td C S (top-down) or S C T^td B^bu T^td C S (direction-optimising);
-  // otherwise body t = its own tier only (S, T^td, B^bu, C).
+  // A chain of tier kernels: every kernel returns at once unless the current level is of its
+  // tier, so a chain runs consecutive levels of changing tiers kernel to kernel, without a
+  // conditional round trip (k_small / k_cluster run a whole run of their levels per launch,
+  // a (k_explore, k_compact) pair or a bottom-up triple one level).  S = k_small, C =
+  // k_cluster, T = top-down pair, B = bottom-up triple.  The canonical sequence of a
+  // traversal is S C T^td C S (top-down) or S C T^td B^bu T^td C S (direction-optimising).
   const std::string seq = std::string("SC") + std::string(S3BFS_TD_CHAIN, 'T') +
       (h->P.direction ? std::string(S3BFS_BU_CHAIN, 'B') + std::string(S3BFS_TD_CHAIN, 'T')
                       : std::string()) + "CS";
-  const char body_tier[4] = {'S', 'T', 'B', 'C'};
-  cudaGraphNodeParams sp = {};
-  sp.type = cudaGraphNodeTypeConditional;
-  sp.conditional.handle = ht;
-  sp.conditional.type = cudaGraphCondTypeSwitch;
-  sp.conditional.size = 4;  // body 2 stays empty without NEXT-3
-  cudaGraphNode_t snode;
-  CK(h, cudaGraphAddNode(&snode, body, nullptr, 0, &sp));
-  for (int bi = 0; bi < 4; ++bi) {
-    if (bi == 2 && !h->P.direction) continue;
-    const char t = body_tier[bi];
-    std::string chain = S3BFS_UNIVERSAL_BODY ? seq.substr(seq.find(t))
-                      : t == 'T' ? std::string(S3BFS_TD_CHAIN, 'T')
-                      : t == 'B' ? std::string(S3BFS_BU_CHAIN, 'B') : std::string(1, t);
-    cudaGraph_t bg = sp.conditional.phGraph_out[bi];
-    cudaGraphNode_t prev = nullptr;
+  auto add_chain = [&](cudaGraph_t bg, const std::string &chain, cudaGraphNode_t prev,
+                       cudaGraphNode_t *last) -> s3bfs_status {
     auto add = [&](void *fn, int grid, int block, size_t smem) -> s3bfs_status {
       cudaGraphNode_t nd;
       cudaKernelNodeParams kp = kparams(fn, grid, block, smem);
@@ -369,6 +343,51 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
       }
       if (r != S3BFS_OK) return r;
     }
+    if (last) *last = prev;
+    return S3BFS_OK;
+  };
+  // S3BFS_GRAPH_PROLOGUE (top-down handles): the canonical sequence runs once straight after
+  // k_init, so a typical traversal never enters the WHILE body (the WHILE only evaluates its
+  // condition).  Not with direction optimisation: its 29-launch sequence costs more idle
+  // launches than the round trips it saves (R-MAT 20 -3 %, ER -2 %).
+  cudaGraphNode_t pre = h->init_node;
+  if (graph_prologue(h)) {
+    s3bfs_status r = add_chain(g, seq, h->init_node, &pre);
+    if (r != S3BFS_OK) return r;
+  }
+  cudaGraphNode_t wnode;
+  CK(h, cudaGraphAddNode(&wnode, g, &pre, 1, &wp));
+  cudaGraph_t body = wp.conditional.phGraph_out[0];
+
+  {  // after the loop: d[0:n-1] and parent in caller ids
+    cudaKernelNodeParams kf = {};
+    kf.func = (void *)k_finalize;
+    kf.gridDim = dim3(finalize_grid(h));
+    kf.blockDim = dim3(256);
+    kf.kernelParams = args;
+    cudaGraphNode_t fnode;
+    CK(h, cudaGraphAddKernelNode(&fnode, g, &wnode, 1, &kf));
+  }
+  // One SWITCH per WHILE iteration selects the body of the tier the next level runs in:
+  // body 0 tier 0, body 1 top-down, body 2 bottom-up (NEXT-3), body 3 the cluster tier.
+  // S3BFS_UNIVERSAL_BODY: body t is the canonical sequence from tier t on; otherwise body t
+  // = its own tier only (S, T^td, B^bu, C).
+  const char body_tier[4] = {'S', 'T', 'B', 'C'};
+  cudaGraphNodeParams sp = {};
+  sp.type = cudaGraphNodeTypeConditional;
+  sp.conditional.handle = ht;
+  sp.conditional.type = cudaGraphCondTypeSwitch;
+  sp.conditional.size = 4;  // body 2 stays empty without NEXT-3
+  cudaGraphNode_t snode;
+  CK(h, cudaGraphAddNode(&snode, body, nullptr, 0, &sp));
+  for (int bi = 0; bi < 4; ++bi) {
+    if (bi == 2 && !h->P.direction) continue;
+    const char t = body_tier[bi];
+    const std::string chain = S3BFS_UNIVERSAL_BODY ? seq.substr(seq.find(t))
+                            : t == 'T' ? std::string(S3BFS_TD_CHAIN, 'T')
+                            : t == 'B' ? std::string(S3BFS_BU_CHAIN, 'B') : std::string(1, t);
+    s3bfs_status r = add_chain(sp.conditional.phGraph_out[bi], chain, nullptr, nullptr);
+    if (r != S3BFS_OK) return r;
   }
 
   CK(h, cudaGraphInstantiate(&h->exec, g, 0));
@@ -891,7 +910,7 @@ s3bfs_status s3bfs_get_info(s3bfs_handle h, s3bfs_info *out) {
   out->td_chain = S3BFS_TD_CHAIN;
   out->bu_chain = S3BFS_BU_CHAIN;
   out->universal_body = S3BFS_UNIVERSAL_BODY;
-  out->reserved = 0;
+  out->prologue = graph_prologue(h) ? 1 : 0;
   out->workspace_bytes = (int64_t)(h->ws_bytes + (h->gs ? h->gs->b2 + h->gs->b3 : 0));
   return S3BFS_OK;
 }

@@ -69,7 +69,7 @@ class Info(ctypes.Structure):
                 ("kd_threads", ctypes.c_int32), ("kd_tile_edges", ctypes.c_int32),
                 ("ksmall_threads", ctypes.c_int32), ("ksmall_max_frontier", ctypes.c_int32),
                 ("td_chain", ctypes.c_int32), ("bu_chain", ctypes.c_int32),
-                ("universal_body", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("universal_body", ctypes.c_int32), ("prologue", ctypes.c_int32),
                 ("workspace_bytes", ctypes.c_int64)]
 
 

@@ -85,3 +85,11 @@ def test_launch_count_from_tier_sequence():
     # direction-optimising sequence S C T^1 B^2 T^1 C S; entry at B for a bottom-up start
     do = {"tier": np.array([1, 3, 3, 1, 4, 0])}
     assert bench.launches_from_stats(do, 1, 2, universal=1, direction=1) == 1 + (2 + 6 + 2 + 1 + 1) + 1
+    # prologue: the whole sequence once after k_init (S C T^4 C S = 12 launches), then the loop
+    assert bench.launches_from_stats(td, td_chain=4, universal=1, prologue=1) == 1 + 12 + 1
+    assert bench.launches_from_stats(td5, td_chain=2, universal=1, prologue=1) == 1 + 8 + 6 + 1
+    # a first level that is already top-down: S and C idle in the prologue
+    assert bench.launches_from_stats({"tier": np.array([1, 0])}, 4, universal=1,
+                                     prologue=1) == 1 + 12 + 1
+    # an empty level sequence still launches the prologue
+    assert bench.launches_from_stats({"tier": np.array([2])}, 4, universal=1, prologue=1) == 14
