@@ -49,6 +49,9 @@ namespace s3bfs {
 #ifndef S3BFS_KX_GROUPS
 #define S3BFS_KX_GROUPS 8
 #endif
+#ifndef S3BFS_KS_SCAN1
+#define S3BFS_KS_SCAN1 1  // k_small: one-barrier block scan (0: warp-0 scan + 2nd barrier)
+#endif
 #ifndef S3BFS_KX_FAST
 #define S3BFS_KX_FAST 1   // uniform-row fast path
 #endif
@@ -1267,6 +1270,23 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
     if (lane == 31) { s_wk[warp] = ik; s_wd[warp] = id; }
     if (lane == 0) s_wc[warp] = wc;
     __syncthreads();
+#if S3BFS_KS_SCAN1
+    // every warp scans the 32 warp totals itself (one CTA barrier per scan instead of two; the
+    // totals are rewritten only after the level's closing barrier)
+    int kpos, dpos, n_next, e_next;
+    {
+      const int a = s_wk[lane], d = s_wd[lane];
+      const int ia = warp_incl_scan(a), idd = warp_incl_scan(d);
+      kpos = __shfl_sync(0xffffffffu, ia - a, warp) + ik - cnt;
+      dpos = __shfl_sync(0xffffffffu, idd - d, warp) + id - dsum;
+      n_next = __shfl_sync(0xffffffffu, ia, 31);
+      e_next = __shfl_sync(0xffffffffu, idd, 31);
+      if (warp == 0 && P.collect_stats) {
+        const int ctot = warp_sum(s_wc[lane]);
+        if (lane == 0) s_tot[2] = ctot;
+      }
+    }
+#else
     if (warp == 0) {
       const int a = s_wk[lane], d = s_wd[lane];
       const int ia = warp_incl_scan(a), idd = warp_incl_scan(d);
@@ -1278,6 +1298,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
     __syncthreads();
     int kpos = s_wk[warp] + ik - cnt, dpos = s_wd[warp] + id - dsum;
     const int n_next = s_tot[0], e_next = s_tot[1];
+#endif
 #pragma unroll
     for (int i = 0; i < KS_IPT; ++i) {
       if (kv[i] >= 0) {
