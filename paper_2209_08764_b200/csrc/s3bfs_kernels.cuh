@@ -52,6 +52,9 @@ namespace s3bfs {
 #ifndef S3BFS_KS_SCAN1
 #define S3BFS_KS_SCAN1 1  // k_small: one-barrier block scan (0: warp-0 scan + 2nd barrier)
 #endif
+#ifndef S3BFS_KC_FENCE
+#define S3BFS_KC_FENCE 0  // k_cluster: extra __threadfence before the owner-check barrier
+#endif
 #ifndef S3BFS_KX_FAST
 #define S3BFS_KX_FAST 1   // uniform-row fast path
 #endif
@@ -1423,8 +1426,11 @@ __global__ void __cluster_dims__(KC_CL, 1, 1) __launch_bounds__(KC_THREADS, 1) k
         cpv[k] = ux[i];
       }
     }
-    __threadfence();  // Owner stores reach L2 before any CTA of the cluster checks them
-    cl.sync();
+#if S3BFS_KC_FENCE
+    __threadfence();
+#endif
+    cl.sync();  // its arrive is a release (MEMBAR.ALL.GPU in SASS): the Owner stores reach L2
+                // before any CTA of the cluster checks them
     // (e): owner check through L2 (the winner may sit on another SM), blocked items
     const int ipt = (ne + KC_THREADS - 1) / KC_THREADS;
     const int k0 = tid * ipt;
