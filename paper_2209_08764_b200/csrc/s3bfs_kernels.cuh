@@ -55,6 +55,9 @@ namespace s3bfs {
 #ifndef S3BFS_KC_FENCE
 #define S3BFS_KC_FENCE 0  // k_cluster: extra __threadfence before the owner-check barrier
 #endif
+#ifndef S3BFS_KC_PUSH
+#define S3BFS_KC_PUSH 1  // k_cluster: CTA totals pushed into every CTA's table (0: 8 DSMEM reads)
+#endif
 #ifndef S3BFS_KX_FAST
 #define S3BFS_KX_FAST 1   // uniform-row fast path
 #endif
@@ -1368,7 +1371,11 @@ __global__ void __cluster_dims__(KC_CL, 1, 1) __launch_bounds__(KC_THREADS, 1) k
   int32_t *cv = sex + KC_FCAP + 4;    // candidate per local edge (or -1)
   int32_t *cpv = cv + KC_ECTA;        // its discoverer (caller id)
   __shared__ int32_t s_wk[KC_THREADS / 32], s_wd[KC_THREADS / 32], s_wc[KC_THREADS / 32];
+#if S3BFS_KC_PUSH
+  __shared__ int32_t s_all[KC_CL][3];  // every CTA's (kept, degree sum, candidates), pushed here
+#else
   __shared__ int32_t s_tot[3];        // this CTA's kept, degree sum, candidates
+#endif
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rank = (int)cl.block_rank();
   const int32_t *__restrict__ col = P.col;
@@ -1471,13 +1478,25 @@ __global__ void __cluster_dims__(KC_CL, 1, 1) __launch_bounds__(KC_THREADS, 1) k
       const int ctot = warp_sum(s_wc[lane]);
       s_wk[lane] = ia - a;
       s_wd[lane] = idd - d;
+#if S3BFS_KC_PUSH
+      const int tk = __shfl_sync(0xffffffffu, ia, 31), td = __shfl_sync(0xffffffffu, idd, 31);
+      if (lane < KC_CL) {  // lane r pushes the totals into CTA r's table (DSMEM stores)
+        int32_t *t = cl.map_shared_rank(&s_all[rank][0], lane);
+        t[0] = tk; t[1] = td; t[2] = ctot;
+      }
+#else
       if (lane == 31) { s_tot[0] = ia; s_tot[1] = idd; s_tot[2] = ctot; }
+#endif
     }
     cl.sync();  // every CTA's totals are published (DSMEM)
     int koff = 0, doff = 0, n_next = 0, e_next = 0, c_all = 0;
 #pragma unroll
     for (int r = 0; r < KC_CL; ++r) {  // the cluster's exclusive scan over CTA totals
+#if S3BFS_KC_PUSH
+      const int32_t *t = &s_all[r][0];
+#else
       const int32_t *t = cl.map_shared_rank(s_tot, r);
+#endif
       const int k = t[0], d = t[1];
       if (r < rank) { koff += k; doff += d; }
       n_next += k;
