@@ -89,7 +89,7 @@ typedef struct {
   int32_t cluster_max_edges; /* cluster tier (one 8-CTA thread-block cluster running
                               consecutive levels with T0 < e_l <= this and n_l <= 8192 in one
                               launch).  0 -> 32768 (the maximum); < 0 -> off.  With it on, the
-                              default T0 (tier0_max_edges = 0) is 4096 */
+                              default T0 (tier0_max_edges = 0) is 2048 */
 } s3bfs_options;
 
 /* One record per BFS level (the SPEC LevelStats analogue).  n_l = |frontier|

@@ -80,7 +80,7 @@ namespace s3bfs {
 #define S3BFS_COL_HINT 1  // col loads carry the L2 evict-first policy
 #endif
 #ifndef S3BFS_T0_WITH_CLUSTER
-#define S3BFS_T0_WITH_CLUSTER 4096  // default T0 when the cluster tier is on (measured crossover)
+#define S3BFS_T0_WITH_CLUSTER 2048  // default T0 when the cluster tier is on (measured crossover)
 #endif
 #ifndef S3BFS_CLAIM_MIN_BYTES
 #define S3BFS_CLAIM_MIN_BYTES (8u << 20)  // claim array floor (measured, DESIGN R26)
