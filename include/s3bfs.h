@@ -90,6 +90,11 @@ typedef struct {
                               consecutive levels with T0 < e_l <= this and n_l <= 8192 in one
                               launch).  0 -> 32768 (the maximum); < 0 -> off.  With it on, the
                               default T0 (tier0_max_edges = 0) is 2048 */
+  int32_t hub_vertices;    /* visited test of k_explore (Fig1 L18 "if d[v] = infinity"): internal
+                              ids below this count (the highest-degree vertices, whose visited
+                              bits stay L1-resident) are tested in the visited bitmap first, all
+                              others directly by their 1-byte discovery tag (one probe).  0 ->
+                              the default (2^20); < 0 -> every vertex through the bitmap first */
 } s3bfs_options;
 
 /* One record per BFS level (the SPEC LevelStats analogue).  n_l = |frontier|

@@ -557,6 +557,13 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   P.v_sent = (int32_t)(bm_bytes * 8);
   P.claim = (uint8_t *)(base + o_claim);
   P.claim_mask = (uint32_t)(claim_n - 1);
+  // k_explore's visited test: ids < hub through the bitmap first (hot, L1-resident words once
+  // the graph is degree-ordered), the rest by their discovery tag alone (R26)
+  {
+    const long long hv = h->opt.hub_vertices;
+    long long hub = hv < 0 ? n : hv > 0 ? hv : (h->opt.reorder >= 0 ? (1LL << 20) : n);
+    P.hub = (int32_t)(hub < n ? hub : n);
+  }
   P.fb[0] = (uint32_t *)(base + o_fb0);
   P.fb[1] = (uint32_t *)(base + o_fb1);
   P.wcnt = (int32_t *)(base + o_wcnt);

@@ -61,9 +61,6 @@ namespace s3bfs {
 #ifndef S3BFS_KX_FAST
 #define S3BFS_KX_FAST 1   // uniform-row fast path
 #endif
-#ifndef S3BFS_KX_LAZY_PARENT
-#define S3BFS_KX_LAZY_PARENT 1  // keep the window slot per group; shuffle the parent on discovery
-#endif
 #ifndef S3BFS_KX_RANK
 #define S3BFS_KX_RANK 1   // rank (REDUX + POPC) edge->row mapping for multi-row batches
 #endif
@@ -126,6 +123,7 @@ constexpr int KC_FCAP = 8192;                    // replicated frontier capacity
 constexpr int KC_IPT = KC_ECTA / KC_THREADS;
 // k_small / k_cluster scan their per-warp totals with warp 0 reading one entry per lane
 static_assert(KS_THREADS == 1024 && KC_THREADS == 1024, "tier-0 / cluster CTAs must have 32 warps");
+static_assert(KX_GROUPS % 4 == 0, "k_explore packs 4 window slots per register");
 constexpr int BU_W = S3BFS_BU_W;   // bottom-up: bitmap words per warp round
 constexpr int BU_P = S3BFS_BU_P;   // bottom-up: in-neighbours probed per vertex per round
 
@@ -178,9 +176,11 @@ struct Params {
                                 //  as kernel parameters they are uniform (no per-load R2UR)
   int32_t v_sent;               // sentinel vertex id (first bit of that block): k_explore's
                                 //  masked lanes probe it and need no validity test
-  uint8_t *claim;               // per-vertex tag of the level that discovered it (k_explore),
-                                //  at slot claim_slot(v) (scattered, see there)
+  uint8_t *claim;               // per-vertex discovery tag: nonzero once v was discovered (in
+                                //  any level, by any kernel), at slot claim_slot(v) (scattered)
   uint32_t claim_mask;          // claim array size - 1 (a power of two >= n)
+  int32_t hub;                  // k_explore: ids < hub are tested in the bitmap first, the
+                                //  others by their discovery tag alone (one probe)
   uint32_t *fb[2];              // NEXT-3: frontier bitmaps (bottom-up levels only)
   const int32_t *tro, *tcol;    // NEXT-3: in-adjacency (internal ids) the bottom-up step scans
   int32_t *wcnt;
@@ -284,8 +284,62 @@ __device__ __forceinline__ int ld_cg_u8(const uint8_t *p) {
   asm volatile("ld.global.cg.u8 %0, [%1];" : "=r"(v) : "l"(p));
   return (int)v;
 }
+// k_explore's one probe per arc (Fig1 L18 "if d[v] = infinity"): a hub id (or the sentinel)
+// reads its visited-bitmap word through the read-only path (L1-resident for the hottest ids),
+// any other id reads its discovery tag at L2 (evict-last: the tags must outlive the col
+// stream).  The caller decodes: a bit of the word, or tag == 0 ("not discovered yet").
+#ifndef S3BFS_PROBE1
+#define S3BFS_PROBE1 1  // one 32-bit load per probe (tag word or bitmap word); 0: two predicated loads
+#endif
+__device__ __forceinline__ uint32_t probe_status(int v, int hub, uint32_t tag_span,
+                                                 const uint8_t *tags, uint32_t tag_mask,
+                                                 const uint32_t *bm, unsigned long long pol) {
+  // the tag-or-bitmap choice ((v - hub) < tag_span, unsigned) and both addresses (tag slot =
+  // (v * 0x9E3779B1) mod 2^k, see claim_slot; word = v >> 5) are formed inside, so no
+  // predicate or 64-bit address of a group stays live across the batch's probes
+  uint32_t r;
+#if S3BFS_PROBE1
+  // one weak 32-bit load: the aligned word holding v's tag byte, or v's bitmap word.  The
+  // caller shifts the tag byte down ((slot & 3) * 8).
+  asm("{\n\t.reg .pred p;\n\t.reg .u32 s;\n\t.reg .u64 a;\n\t"
+      "sub.s32 s, %1, %2;\n\t"
+      "setp.lt.u32 p, s, %3;\n\t"
+      "@p mul.lo.u32 s, %1, -1640531535;\n\t"
+      "@p and.b32 s, s, %4;\n\t"
+      "@p and.b32 s, s, -4;\n\t"
+      "@p cvt.u64.u32 a, s;\n\t"
+      "@p add.u64 a, a, %5;\n\t"
+      "@!p shr.s32 s, %1, 5;\n\t"
+      "@!p mul.wide.s32 a, s, 4;\n\t"
+      "@!p add.u64 a, a, %6;\n\t"
+      "ld.global.L2::cache_hint.u32 %0, [a], %7;\n\t}"
+      : "=r"(r)
+      : "r"(v), "r"(hub), "r"(tag_span), "r"(tag_mask), "l"(tags), "l"(bm), "l"(pol));
+#else
+  asm("{\n\t.reg .pred p;\n\t.reg .u32 s;\n\t.reg .u64 a;\n\t"
+      "sub.s32 s, %1, %2;\n\t"
+      "setp.lt.u32 p, s, %3;\n\t"
+      "@p mul.lo.u32 s, %1, -1640531535;\n\t"
+      "@p and.b32 s, s, %4;\n\t"
+      "@p cvt.u64.u32 a, s;\n\t"
+      "@p add.u64 a, a, %5;\n\t"
+      "@p ld.global.cg.L2::cache_hint.u8 %0, [a], %7;\n\t"
+      "@!p shr.s32 s, %1, 5;\n\t"
+      "@!p mul.wide.s32 a, s, 4;\n\t"
+      "@!p add.u64 a, a, %6;\n\t"
+      "@!p ld.global.nc.L2::cache_hint.u32 %0, [a], %7;\n\t}"
+      : "=r"(r)
+      : "r"(v), "r"(hub), "r"(tag_span), "r"(tag_mask), "l"(tags), "l"(bm), "l"(pol));
+#endif
+  return r;
+}
 __device__ __forceinline__ void st_u8(uint8_t *p, int v) {
   asm volatile("st.global.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// a vertex kept by a kernel other than k_explore (tier 0, cluster tier, bottom-up, NEXT-4
+// merge) gets its discovery tag too: k_explore tests non-hub ids by the tag alone
+__device__ __forceinline__ void mark_tag(const Params &P, int v) {
+  st_u8(P.claim + claim_slot(P, v), 1);
 }
 __device__ __forceinline__ void st_weak(int32_t *p, int v) {
   asm volatile("st.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -529,9 +583,13 @@ __global__ void k_init(Params P, int32_t s, int32_t *level, int32_t *parent) {
     if (i == (si >> 7)) (&w.x)[(si >> 5) & 3] = 1u << (si & 31);
     reinterpret_cast<uint4 *>(P.bm)[i] = w;
   }
-  const long long nc = ((long long)P.claim_mask + 16) >> 4;  // claim tags <- 0 (all slots)
-  for (long long i = gtid; i < nc; i += gstride)
-    reinterpret_cast<uint4 *>(P.claim)[i] = make_uint4(0, 0, 0, 0);
+  const long long nc = ((long long)P.claim_mask + 16) >> 4;  // claim tags <- 0 (all slots),
+  const uint32_t ss = claim_slot(P, si);                       // but the source's (discovered)
+  for (long long i = gtid; i < nc; i += gstride) {
+    uint4 z = make_uint4(0, 0, 0, 0);
+    if (i == (long long)(ss >> 4)) (&z.x)[(ss >> 2) & 3] = 1u << (8 * (ss & 3));
+    reinterpret_cast<uint4 *>(P.claim)[i] = z;
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     Ctl *c = P.ctl;
     const int4 vs = P.vinfo[si];
@@ -602,6 +660,8 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   const uint32_t *__restrict__ bm = P.bm;
   uint8_t *__restrict__ claim = P.claim;
   const int vs = P.v_sent;  // masked lanes' target: its visited bit is always set
+  const int hub = P.hub;                              // ids < hub: bitmap first
+  const uint32_t tag_span = (uint32_t)(P.n - P.hub);  // ids in [hub, n): tag only
 
   if (tid == 0) {
     P.status[b] = 0ull;  // reset k_compact's look-back word for this level
@@ -632,9 +692,9 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
     load_window(u0);
   }
   // Map the batch of edges [e, e_next) onto lanes and load their targets: v[g] = col entry of
-  // edge e + 32g + lane (-1 outside the batch), xv[g] = its frontier vertex: the window slot
-  // (S3BFS_KX_LAZY_PARENT; the caller id is shuffled only on discovery) or the caller id.
-  auto map_load = [&](int e, int (&v)[KX_GROUPS], int (&xv)[KX_GROUPS]) -> int {
+  // edge e + 32g + lane (-1 outside the batch), byte g of xs = its frontier vertex's window slot
+  // (the caller id is shuffled only on discovery).
+  auto map_load = [&](int e, int (&v)[KX_GROUPS], uint32_t (&xs)[KX_GROUPS / 4]) -> int {
     while (lim <= e) {  // window exhausted (also skips runs of zero-degree vertices, C9)
       u0 += 32;
       load_window(u0);
@@ -647,12 +707,12 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
     int e_next = min(e + KX_GROUPS * 32, bend);
     if (S3BFS_KX_FAST && row_end >= e_next) {
       // the whole batch lies in one frontier row (most R-MAT arcs): uniform x and base
-      const int x = S3BFS_KX_LAZY_PARENT ? j0 : __shfl_sync(0xffffffffu, wx, j0);
+      const int x = j0;
       const int base = __shfl_sync(0xffffffffu, wb, j0);
       const int start = base + e;  // col index of the batch's first edge
       const int a0 = start & ~3;   // 16-byte aligned
 #pragma unroll
-      for (int g = 0; g < KX_GROUPS; ++g) xv[g] = x;
+      for (int k = 0; k < KX_GROUPS / 4; ++k) xs[k] = (uint32_t)x * 0x01010101u;
       if (S3BFS_KX_VEC && P.col_vec && (long long)a0 + KX_GROUPS * 32 <= P.nnz) {
         // vectorised streaming: lane i loads 16 B at a0 + 4*(i + 32k), i.e. each warp
         // instruction fetches 512 contiguous bytes of the row; edges outside
@@ -706,7 +766,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
         const unsigned m = __reduce_or_sync(0xffffffffu, shl1(rel));  // starts in [eg, eg+31]
         if (g == 0) r -= (int)(m & 1u);  // a row starting exactly at e is row j0 itself
         const int j = r + __popc(m & le);
-        xv[g] = S3BFS_KX_LAZY_PARENT ? j : __shfl_sync(0xffffffffu, wx, j);
+        xs[g >> 2] |= (uint32_t)j << (8 * (g & 3));
         const int pos = __shfl_sync(0xffffffffu, wb, j) + eg + lane;
         const bool ok = g * 32 < lb;
         const int t = ldg_stream(col + (ok ? pos : pfirst), pol_stream);  // unconditional
@@ -723,7 +783,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
           const int cj = __shfl_sync(0xffffffffu, wex, min(j + s, 31));
           if (j + s <= 31 && cj <= my_e) j += s;
         }
-        xv[g] = S3BFS_KX_LAZY_PARENT ? j : __shfl_sync(0xffffffffu, wx, j);
+        xs[g >> 2] |= (uint32_t)j << (8 * (g & 3));
         const int pos = __shfl_sync(0xffffffffu, wb, j) + my_e;
         const int pf = __shfl_sync(0xffffffffu, wb, j0) + e;
         const int t = ldg_stream(col + (my_e < bend ? pos : pf), pol_stream);
@@ -734,32 +794,52 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   };
   int e = e_begin;
   while (e < e_end) {
-    int v[KX_GROUPS], xv[KX_GROUPS];
-    e = map_load(e, v, xv);
-    // visited test: the bitmap (visited before this level), branch-free (a masked slot
-    // probes the always-set sentinel bit)
-    uint32_t needm = 0;
+    int v[KX_GROUPS];
+    uint32_t xs[KX_GROUPS / 4];  // window slots of the groups' frontier vertices, one byte each
+#pragma unroll
+    for (int k = 0; k < KX_GROUPS / 4; ++k) xs[k] = 0;
+    e = map_load(e, v, xs);
+    // visited test (Fig1 L18), one probe per arc: a hub id reads the visited bitmap (exact at
+    // level start, hot words L1-resident), any other id its discovery tag, which is nonzero once
+    // some worker discovered it in this or an earlier level.  Masked slots probe the sentinel
+    // (a bitmap bit that is always set), so the test is branch-free.
+    uint32_t needm = 0;  // hub ids not visited at level start: their tag decides
+    uint32_t discm = 0;  // ids found undiscovered: candidates (Fig1 L19-L22)
 #pragma unroll
     for (int g = 0; g < KX_GROUPS; ++g) {
-      const uint32_t w = S3BFS_BM_NC ? ldg_status_u32(bm + (v[g] >> 5), pol_status)
-                                     : ld_status_u32(bm + (v[g] >> 5), pol_status);
-      needm |= (~rotr32(w, v[g]) & 1u) << g;  // bit (v mod 32) of w, inverted
+      const uint32_t r = probe_status(v[g], hub, tag_span, claim, P.claim_mask, bm, pol_status);
+      const bool via_tag = (uint32_t)(v[g] - hub) < tag_span;
+      const uint32_t bit_clear = ~rotr32(r, v[g]) & 1u;
+#if S3BFS_PROBE1
+      const uint32_t tagv = (r >> (((uint32_t)v[g] * 0x9E3779B1u & 3u) * 8)) & 0xffu;
+#else
+      const uint32_t tagv = r;
+#endif
+      needm |= (via_tag ? 0u : bit_clear) << g;
+      discm |= (via_tag ? (uint32_t)(tagv == 0u) : 0u) << g;
     }
-    // claim/discovery only for the groups where some lane met a vertex not visited at level
-    // start (warp-uniform skip: on the heavy levels most batches have one or two such groups)
     const unsigned wneed = __reduce_or_sync(0xffffffffu, needm);
-    if (wneed) {
-      int cl[KX_GROUPS];  // claim tags of the vertices not visited at level start
+    if (wneed) {  // warp-uniform skip: after the first levels the hubs are all visited
 #pragma unroll
-      for (int g = 0; g < KX_GROUPS; ++g)
-        if ((wneed >> g) & 1u)
-          cl[g] = ((needm >> g) & 1u) ? ld_cg_u8(claim + claim_slot(P, v[g])) : tag;
+      for (int h = 0; h < KX_GROUPS; h += 4) {  // 4 tag loads in flight (register budget)
+        int cl[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+          cl[g] = ((needm >> (h + g)) & 1u) ? ld_cg_u8(claim + claim_slot(P, v[h + g])) : 1;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) discm |= (uint32_t)(cl[g] == 0) << (h + g);
+      }
+    }
+    // discovery only for the groups where some lane found an undiscovered vertex (warp-uniform
+    // skip: on the heavy levels most batches have none or one or two such groups)
+    const unsigned wdisc = __reduce_or_sync(0xffffffffu, discm);
+    if (wdisc) {
 #pragma unroll
       for (int g = 0; g < KX_GROUPS; ++g) {
-        if (!((wneed >> g) & 1u)) continue;
+        if (!((wdisc >> g) & 1u)) continue;
         // parent: the window slot's caller id (the window is unchanged since map_load)
-        const int par = S3BFS_KX_LAZY_PARENT ? __shfl_sync(0xffffffffu, wx, xv[g]) : xv[g];
-        const bool disc = cl[g] != tag;
+        const int par = __shfl_sync(0xffffffffu, wx, (xs[g >> 2] >> (8 * (g & 3))) & 31u);
+        const bool disc = (discm >> g) & 1u;
         const unsigned m = __ballot_sync(0xffffffffu, disc);
         if (disc) {
           const int slot = segbase + wcount + __popc(m & lanemask_lt());
@@ -993,6 +1073,7 @@ __global__ void __launch_bounds__(KD_THREADS) k_merge_keep(Params P, const int4 
     if (keep[g]) {
       P.minrank[rv[g].x] = 0x7fffffff;  // the unique keeper resets it for the next level
       P.lp[rv[g].x] = make_int2(new_level, rv[g].y);
+      mark_tag(P, rv[g].x);
     }
     bm_publish(P.bm, keep[g], rv[g].x, lane);  // ranks that did not keep v learn its bit here
     kept += __popc(__ballot_sync(0xffffffffu, keep[g]));
@@ -1083,7 +1164,9 @@ __device__ void tiny_levels(const Params &P, Ctl *c, int32_t *sf, int32_t *srs, 
     const bool has = lane < e_l;
     const int v = has ? __ldg(col + pr + (lane - pe)) : 0;
     const uint32_t w = __ldcg(P.bm + (v >> 5));      // published by atomicOr at L2
-    const int4 vi = __ldg(P.vinfo + v);               // issued together with the bitmap word
+    // issued together with the bitmap word; through L2 (ld.global.cg), never the read-only
+    // path: k_small's block levels store Owner into the same 16-byte record in this launch
+    const int4 vi = __ldcg(P.vinfo + v);
     const bool fresh = has && !((w >> (v & 31)) & 1u);
     const unsigned fm = __ballot_sync(0xffffffffu, fresh);
     const int ncand = __popc(fm);
@@ -1096,6 +1179,7 @@ __device__ void tiny_levels(const Params &P, Ctl *c, int32_t *sf, int32_t *srs, 
     if (keep) {
       P.lp[v] = make_int2(L + 1, px);                 // d[v] <- l, parent (Fig1 L18)
       atomicOr(P.bm + (v >> 5), 1u << (v & 31));      // exact visited bit
+      mark_tag(P, v);
     }
     const int d = keep ? vi.y : 0;
     const int n_next = __popc(km);
@@ -1126,6 +1210,9 @@ __device__ void tiny_levels(const Params &P, Ctl *c, int32_t *sf, int32_t *srs, 
     ++L;
     n_l = n_next;
     e_l = e_next;
+    // orders this level's bitmap atomics / tag and record stores before the next level's
+    // probes by the other lanes (shuffles and votes do not order memory, PTX model)
+    __syncwarp();
     if (n_l == 0 || e_l == 0 || n_l > 32 || e_l > lim_e) break;
   }
   if (lane < n_l) {
@@ -1263,6 +1350,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
         kv[i] = vis[i].z; kr[i] = vis[i].x; kd[i] = vis[i].y;
         P.lp[v] = make_int2(L + 1, cpv[e]);         // d[v] <- l, parent (Fig1 L18)
         atomicOr(P.bm + (v >> 5), 1u << (v & 31));  // exact visited bit (not discovery)
+        mark_tag(P, v);
       }
     }
 #pragma unroll
@@ -1462,6 +1550,7 @@ __global__ void __cluster_dims__(KC_CL, 1, 1) __launch_bounds__(KC_THREADS, 1) k
         kv[i] = vis[i].z; kr[i] = vis[i].x; kd[i] = vis[i].y;
         P.lp[v] = make_int2(L + 1, cpv[k]);          // d[v] <- l, parent (Fig1 L18)
         atomicOr(P.bm + (v >> 5), 1u << (v & 31));   // exact visited bit (not discovery)
+        mark_tag(P, v);
         ++cnt;
         dsum += kd[i];
       }
@@ -1661,7 +1750,10 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params 
       const int w = wb + i;
       const int v = (w << 5) + lane;
       const bool found = pu[i] >= 0;
-      if (found) P.lp[v] = make_int2(new_level, __ldg(vinfo + pu[i]).z);  // d, parent (caller)
+      if (found) {
+        P.lp[v] = make_int2(new_level, __ldg(vinfo + pu[i]).z);  // d, parent (caller)
+        mark_tag(P, v);
+      }
       const unsigned m = __ballot_sync(0xffffffffu, found);
       if (lane == 0 && w < w1) {
         if (m) bm[w] = bw[i] | m;  // this warp owns word w

@@ -44,7 +44,8 @@ class Options(ctypes.Structure):
                 ("time_kernels", ctypes.c_int32), ("reorder", ctypes.c_int32),
                 ("direction", ctypes.c_int32), ("do_alpha", ctypes.c_int32),
                 ("do_beta", ctypes.c_int32), ("dist_size", ctypes.c_int32),
-                ("dist_rank", ctypes.c_int32), ("cluster_max_edges", ctypes.c_int32)]
+                ("dist_rank", ctypes.c_int32), ("cluster_max_edges", ctypes.c_int32),
+                ("hub_vertices", ctypes.c_int32)]
 
 
 class LevelStat(ctypes.Structure):

@@ -76,8 +76,14 @@ for key, lib, h in handles:
     tot_ms = sum(p["ms"] for p in per)
     tot_e = sum(edges[s] for s in srcs)
     results[key] = {"gteps": tot_e / tot_ms / 1e6, "per": per}
-    print(f"{key:32s} GTEPS {tot_e / tot_ms / 1e6:7.2f}  ms/src " +
-          " ".join(f"{p['ms']:.3f}" for p in per), flush=True)
+    t1 = [x for s in srcs for x in levels[key][s] if x[2] == 1]
+    kx_us = sum(x[3] for x in t1)
+    kc_us = sum(x[4] for x in t1)
+    alg = sum(8 * x[1] + 16 * x[5] for x in t1)
+    frac = alg / (kx_us * 1e-6) / 6.5498e12 if kx_us else 0.0
+    print(f"{key:32s} GTEPS {tot_e / tot_ms / 1e6:7.2f}  kx {kx_us:8.0f} us kc {kc_us:7.0f} us "
+          f"frac(kx, in-graph) {frac:.3f}  ms/src " + " ".join(f"{p['ms']:.3f}" for p in per),
+          flush=True)
     worst = max(per, key=lambda p: p["ms"])
     for p in per[:2] + ([worst] if worst not in per[:2] else []):
         print("    src", p["src"], " ".join(f"[e={x[1]/1e6:.1f}M kx={x[3]:.0f} kc={x[4]:.0f} c={x[5]/1e6:.2f}M k={x[6]/1e6:.2f}M]"

@@ -116,5 +116,11 @@ def test_product_path_never_touches_the_oracle():
 
 
 def test_options_struct_matches_header():
-    assert ctypes.sizeof(pkg.Options) == 16 * 4
+    # the ctypes mirror must list the header's int32 fields in the header's order
+    hdr = open(HEADER).read()
+    body = hdr[hdr.index("typedef struct {\n  int32_t edges_per_cta"):]
+    body = body[: body.index("} s3bfs_options;")]
+    names = re.findall(r"int32_t\s+(\w+);", re.sub(r"/\*.*?\*/", "", body, flags=re.S))
+    assert [f[0] for f in pkg.Options._fields_] == names
+    assert ctypes.sizeof(pkg.Options) == len(names) * 4
     assert ctypes.sizeof(pkg.LevelStat) == 8 * 4 + 4 * 8

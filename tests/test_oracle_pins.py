@@ -294,6 +294,76 @@ def test_fig1_levels_and_accounting(seed):
             assert el.sum() == sum(1 for (u, _) in garcs if exp[u] >= 0)   # P:41 accounting
 
 
+def _grid_corner_profile(R, C):
+    """Closed form for a 4-neighbour R x C grid BFS'd from corner (0,0) (level = r + c):
+    n_l = min(l, R-1, C-1, R+C-2-l) + 1 (anti-diagonal length), and e_l = 4 n_l minus one
+    missing neighbour per border side the diagonal touches -- no level array involved."""
+    L = R + C - 1
+    nl = [min(l, R - 1, C - 1, R + C - 2 - l) + 1 for l in range(L)]
+    el = [4 * nl[l] - (l <= C - 1) - (R - 1 <= l) - (l <= R - 1) - (C - 1 <= l) for l in range(L)]
+    return nl, el
+
+
+@pytest.mark.parametrize("R,C", [(1024, 1024), (7, 3), (3, 7), (1, 9), (2, 2)])
+def test_level_profile_grid_corner_closed_form(R, C):
+    """oracle_level_profile's n_l / e_l (Fig1 L9, L15) and m_c pinned to
+    the grid's closed forms; a rectangular grid catches a transposed r/c, the 1024^2 case is
+    BASELINE configs[1] (n_l = l+1 up to 1023, then 2047-l; max e_l 4,092)."""
+    g = graphgen.grid(R, C)
+    level, _ = oracle.bfs(g.row_offsets, g.col_indices, 0)
+    nl, el, mc, nc = oracle.level_profile(g.row_offsets, level)
+    exp_nl, exp_el = _grid_corner_profile(R, C)
+    assert nl.tolist() == exp_nl
+    assert el.tolist() == exp_el
+    # P:41 accounting: the grid is connected, so every arc of the CSR is in the component
+    assert mc == g.nnz == 2 * (R * (C - 1) + C * (R - 1)) and nc == R * C
+    if (R, C) == (1024, 1024):
+        assert max(el) == 4092 and nl[1023] == 1024 and nl[2046] == 1
+
+
+def test_level_profile_grid_centre_closed_form():
+    """From the centre (512, 512) of the 1024^2 grid (BASELINE configs[1], R21): the L1 ball
+    stays interior up to l = 510, so n_l = 4l and e_l = 16 l; at l = 511 it is still whole
+    but (1023, 512) and (512, 1023) sit on the border (e = 16*511 - 2); the whole profile
+    sums to n and to the arc count of the grid."""
+    g = graphgen.grid(1024, 1024)
+    level, _ = oracle.bfs(g.row_offsets, g.col_indices, 524_800)
+    nl, el, mc, nc = oracle.level_profile(g.row_offsets, level)
+    assert len(nl) == 1025 and nl[0] == 1 and el[0] == 4
+    for l in range(1, 511):
+        assert nl[l] == 4 * l and el[l] == 16 * l, l
+    assert nl[511] == 4 * 511 and el[511] == 16 * 511 - 2
+    assert nl.sum() == nc == 1 << 20
+    assert el.sum() == mc == 4_190_208 == g.nnz
+
+
+def test_level_profile_spec_examples():
+    """SPEC S:274 (directed path: n_l [1,1,1,1], e_l [1,1,1,0]) and S:275 (star with 100
+    leaves: n_l [1,100], e_l [100,0]) -- the out-degree sums of Fig1 L13/L15.  A profile that
+    summed in-degrees (or shifted the level by one) gives [0,1,1,1] / [0,100] and fails."""
+    for ex in GOLDEN["run_bfs_stats"]:
+        if "star_leaves" in ex:
+            k = ex["star_leaves"]
+            g = csr(k + 1, [(0, j) for j in range(1, k + 1)], directed=True)
+        else:
+            g = csr(ex["n"], ex["edges"], directed=ex["directed"])
+        level, _ = oracle.bfs(g.row_offsets, g.col_indices, ex["source"])
+        nl, el, mc, nc = oracle.level_profile(g.row_offsets, level)
+        assert nl.tolist() == ex["n_l"] and el.tolist() == ex["e_l"], ex["cite"]
+        assert mc == sum(ex["e_l"]) == g.nnz and nc == sum(ex["n_l"]), ex["cite"]
+
+
+def test_level_profile_two_components_and_unreached():
+    """Unreached vertices (-1) contribute to nothing: a path 0-1-2 plus a disjoint K4 on
+    3..6 from source 0 gives n_l [1,1,1], e_l [1,2,1] (undirected path degrees), m_c = 4 arcs
+    of the path only (P:41 counts the source's component), n_c = 3."""
+    edges = [(0, 1), (1, 2)] + [(a, b) for a in range(3, 7) for b in range(a + 1, 7)]
+    g = csr(7, edges, directed=False)
+    level, _ = oracle.bfs(g.row_offsets, g.col_indices, 0)
+    nl, el, mc, nc = oracle.level_profile(g.row_offsets, level)
+    assert nl.tolist() == [1, 1, 1] and el.tolist() == [1, 2, 1] and mc == 4 and nc == 3
+
+
 def test_level_profile_vs_direct_counts():
     g = graphgen.rmat(10, 8, seed=9)
     s = int(np.argmax(np.diff(g.row_offsets)))
