@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="s3bfs", choices=["s3bfs", "reference"])
     ap.add_argument("--config", default="rmat24", choices=list(CONFIG_INDEX))
-    ap.add_argument("--oracle-sources", type=int, default=4,
+    ap.add_argument("--oracle-sources", type=int, default=3,
                     help="sources checked bit-exactly against (and timed on) the oracle")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--detail-out", default="")
@@ -170,6 +170,45 @@ def job_throughput(my_ms: float, my_edges: float, dev, world: int):
     return tot / (max_ms / 1e3) / 1e9, max_ms, tot
 
 
+def cpu_baseline(g, srcs, args, flags, per):
+    """the oracle (serial FIFO BFS) on the host cores, same CSR in host memory,
+    same sources.  Single core: per source the median of 3 runs; value = sum of m_c/2 over
+    the sample / sum of the medians.  Throughput: N threads at once, each its own source (no
+    shared mutable state), aggregate m_c/2 over the wall time; N = min(cores, sources)."""
+    import concurrent.futures as cf
+
+    import oracle
+    sample = srcs[: max(1, min(args.oracle_sources, len(srcs)))]
+    meds, edges = [], 0
+    for s in sample:
+        reps = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            oracle.bfs(g.row_offsets, g.col_indices, s)
+            reps.append(time.perf_counter() - t0)
+        meds.append(statistics.median(reps))
+        edges += per[s]["m_c"] // 2
+    single = edges / sum(meds) / 1e9
+    cores = os.cpu_count() or 1
+    nthr = max(1, min(cores, len(srcs)))
+    tp_srcs = [srcs[k % len(srcs)] for k in range(nthr)]
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(nthr) as ex:  # ctypes drops the GIL inside oracle_bfs
+        list(ex.map(lambda s: oracle.bfs(g.row_offsets, g.col_indices, s), tp_srcs))
+    wall = time.perf_counter() - t0
+    tp = sum(per[s]["m_c"] // 2 for s in tp_srcs) / wall / 1e9
+    return {"value": single, "unit": "GTEPS", "cores": 1, "kind": "oracle",
+            "sample": f"oracle_bfs (serial FIFO BFS, {flags}), median of 3 runs from each of "
+                      f"the first {len(sample)} of {len(srcs)} {args.config} sources "
+                      f"({3 * sum(meds):.1f} s of CPU work)",
+            "cpu_model": oracle.cpu_model(), "host_cores_total": cores,
+            "throughput": {"value": tp, "unit": "GTEPS", "threads": nthr,
+                           "what": f"{nthr} host threads at once, each one traversal from its "
+                                   f"own source (the config's sources in order); aggregate "
+                                   f"m_c/2 over the wall time ({wall:.1f} s)"},
+            "median_ms_per_source": [m * 1e3 for m in meds]}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -260,29 +299,26 @@ def main():
                    info["prologue"]) if args.loop_mode != 2 else (1, 1, 0, 0, 0))),
                   "stats": st}
     verified = {"sources": 0, "levels_bit_exact": True, "parents_valid": True}
-    cpu_times, cpu_edges = [], []
+    cpu = None
     oracle_levels = {}
     if rank == 0 and args.oracle_sources > 0:
         import oracle
+        flags = oracle.use_native()  # -O3 -march=native, built on this host
         for s in srcs[: args.oracle_sources]:
             pkg.s3bfs_run_ptr(bfs.handle, s, lp, pp, sp)
             torch.cuda.synchronize()
             lv, pa = level.cpu().numpy(), parent.cpu().numpy()
-            t0 = time.perf_counter()
             ref, _ = oracle.bfs(g.row_offsets, g.col_indices, s)
-            cpu_times.append(time.perf_counter() - t0)
             oracle_levels[s] = ref
-            _, _, m_c, _ = oracle.level_profile(g.row_offsets, ref)
-            cpu_edges.append(m_c // 2)
             ok = bool(np.array_equal(lv, ref))
             code, _ = oracle.check_bfs(g.row_offsets, g.col_indices, s, lv, pa)
+            _, _, m_c, _ = oracle.level_profile(g.row_offsets, ref)
             verified["sources"] += 1
-            verified["levels_bit_exact"] &= ok
+            verified["levels_bit_exact"] &= ok and m_c == per[s]["m_c"]
             verified["parents_valid"] &= code == 0
-            if m_c != per[s]["m_c"]:
-                verified["levels_bit_exact"] = False
         if not (verified["levels_bit_exact"] and verified["parents_valid"]):
             print(f"VERIFICATION FAILED: {verified}", file=sys.stderr, flush=True)
+        cpu = cpu_baseline(g, srcs, args, flags, per)
 
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -468,15 +504,36 @@ def main():
                                  [p["stats"]["tier"] == 1]).sum()) / 1e6 for p in per.values())
         step_total = sum(float(p["stats"]["t_end_ns"][-1] - p["stats"]["t_begin_ns"][0]) / 1e6
                          for p in per.values())
-        traffic = None
+        # ncu-measured DRAM bytes per k_explore launch (profiles/ncu_traffic.json, keyed by
+        # config; written by scripts/ncu_traffic.py from an ncu capture of this bench command)
+        traffic, traffic_detail = None, None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
             try:
-                traffic = json.load(open(tp)).get(args.config)
+                traffic_detail = json.load(open(tp)).get(args.config)
+                traffic = traffic_detail["dram_bytes_per_launch"] if traffic_detail else None
             except Exception:  # noqa: BLE001
-                traffic = None
+                traffic, traffic_detail = None, None
+        # per tier-1 level (in-graph CTA-0 stamps of the bench's own traversals): the same
+        # algorithmic bytes over that level's k_explore span, for the levels that carry the work
+        lvl = []
+        for s_, p in per.items():
+            stt = p["stats"]
+            for r in stt[(stt["tier"] == 1) & (stt["e_l"] >= 1_000_000)]:
+                us = float(r["t_explore_end_ns"] - r["t_explore_begin_ns"]) / 1e3
+                b = 8 * int(r["e_l"]) + 16 * int(r["candidates"])
+                lvl.append({"source": int(s_), "level": int(r["level"]), "e_l": int(r["e_l"]),
+                            "candidates": int(r["candidates"]), "us": us,
+                            "frac": b / (us * 1e-6) / (peak * 1e9) if us > 0 else None})
+        detail["heavy_levels"] = lvl
+        fr = sorted(x["frac"] for x in lvl if x["frac"])
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "kernel": "k_explore",
+                "frac_of_8tbs": achieved / 8000.0,
+                "traffic_detail": traffic_detail,
+                "heavy_level_frac": ({"levels": len(fr), "min": fr[0], "median": fr[len(fr) // 2],
+                                      "max": fr[-1], "what": "tier-1 levels with e_l >= 1e6, "
+                                      "in-graph CTA-0 stamps, same byte model"} if fr else None),
                 "peak_source": peak_src, "launches": ex_launch,
                 "bytes_per_launch": alg_bytes / max(ex_launch, 1),
                 "avg_launch_ms": ex_ms / max(ex_launch, 1),
@@ -487,13 +544,6 @@ def main():
                                    "host_loop_wall_ms": step_ms_hl}
 
     if rank == 0:
-        cpu = None
-        if cpu_times:
-            cg = sum(cpu_edges) / sum(cpu_times) / 1e9
-            cpu = {"value": cg, "unit": "GTEPS", "cores": 1, "kind": "oracle",
-                   "sample": f"oracle_bfs (serial FIFO BFS, C -O3, 1 thread), 1 run from each of "
-                             f"the first {len(cpu_times)} of {len(srcs)} {args.config} sources "
-                             f"({sum(cpu_times):.1f} s)"}
         line = {
             "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,

@@ -95,6 +95,10 @@ typedef struct {
                               bits stay L1-resident) are tested in the visited bitmap first, all
                               others directly by their 1-byte discovery tag (one probe).  0 ->
                               the default (2^20); < 0 -> every vertex through the bitmap first */
+  int32_t tag_mode_pct;    /* that split ("tag mode") is used on a level while fewer than this
+                              percentage of all arcs end at visited vertices (the discovery-heavy
+                              levels); other levels test every target's visited bit first.
+                              0 -> the default (80); > 100 -> every level; < 0 -> never */
 } s3bfs_options;
 
 /* One record per BFS level (the SPEC LevelStats analogue).  n_l = |frontier|

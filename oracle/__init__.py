@@ -26,21 +26,47 @@ _P32 = ctypes.POINTER(ctypes.c_int32)
 _P64 = ctypes.POINTER(ctypes.c_int64)
 
 
-def build(force: bool = False) -> str:
-    """Compile liboracle.so (gcc -O3).  Building the checker is not using it."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O3", "-std=c11", "-shared", "-fPIC",
-                               "-Wall", "-Wextra", "-o", tmp, _SRC])
-        os.replace(tmp, _LIB)
-    return _LIB
+_NATIVE_LIB = os.path.join(_HERE, "liboracle_native.so")
+_use_native = False
+
+
+def build(force: bool = False, native: bool = False) -> str:
+    """Compile liboracle.so (gcc -O3; portable, built wherever the tests run).  With native,
+    liboracle_native.so with -O3 -march=native (SURVEY 8(d) D7's flags for the timed CPU
+    baseline), built on the machine that runs it.  Building the checker is not using it."""
+    lib = _NATIVE_LIB if native else _LIB
+    if force or not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(_SRC):
+        tmp = lib + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O3", *(["-march=native"] if native else []), "-std=c11",
+                               "-shared", "-fPIC", "-Wall", "-Wextra", "-o", tmp, _SRC])
+        os.replace(tmp, lib)
+    return lib
+
+
+def use_native() -> str:
+    """Switch this process to the -march=native build (bench.py's CPU baseline legs only).
+    Returns the compiler flags in use."""
+    global _use_native, _lib
+    build(force=True, native=True)
+    _use_native, _lib = True, None
+    return "gcc -O3 -march=native -std=c11"
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def _load():
     global _lib
     if _lib is None:
-        build()
-        lib = ctypes.CDLL(_LIB)
+        path = build(native=_use_native)
+        lib = ctypes.CDLL(path)
         lib.oracle_bfs.argtypes = [ctypes.c_int32, _P32, _P32, ctypes.c_int32, _P32, _P32]
         lib.oracle_inclusive_scan.argtypes = [_P32, ctypes.c_int64, _P32]
         lib.oracle_exclusive_scan.argtypes = [_P32, ctypes.c_int64, _P32]

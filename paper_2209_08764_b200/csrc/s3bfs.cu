@@ -168,9 +168,9 @@ s3bfs_status build_reordered(s3bfs_ctx *h, cudaStream_t st) {
   k_inverse_perm<<<grid, 256, 0, st>>>(n2o, n, o2n, h->ro, deg);  // deg <- internal degrees
   // ro2 = exclusive scan of the internal degrees: the look-back scan kernel (b)
   const int tiles = (int)(((long long)n + SCAN_TILE - 1) / SCAN_TILE);
-  CK(h, status_b.alloc((size_t)tiles * 8));
+  CK(h, status_b.alloc((size_t)(tiles + 1) * 8));  // + the tile counter
   unsigned long long *status = status_b.as<unsigned long long>();
-  CK(h, cudaMemsetAsync(status, 0, (size_t)tiles * 8, st));
+  CK(h, cudaMemsetAsync(status, 0, (size_t)(tiles + 1) * 8, st));
   k_scan_u32<<<tiles, SCAN_THREADS, 0, st>>>(deg, ro2, n, status);
   k_relabel_rows<<<h->num_sms * 16, 256, 0, st>>>(h->ro, h->col, n2o, o2n, ro2, n, col2);
   k_build_vinfo<<<grid, 256, 0, st>>>(ro2, n2o, n, h->P.vinfo);
@@ -243,9 +243,9 @@ s3bfs_status build_in_adjacency(s3bfs_ctx *h, cudaStream_t st) {
   CK(h, cudaMemsetAsync(tdeg, 0, (size_t)n * 4, st));
   k_in_degree<<<h->num_sms * 16, 256, 0, st>>>(ro, col, n, tdeg);
   const int tiles = (int)(((long long)n + SCAN_TILE - 1) / SCAN_TILE);
-  CK(h, status_b.alloc((size_t)tiles * 8));
+  CK(h, status_b.alloc((size_t)(tiles + 1) * 8));  // + the tile counter
   unsigned long long *status = status_b.as<unsigned long long>();
-  CK(h, cudaMemsetAsync(status, 0, (size_t)tiles * 8, st));
+  CK(h, cudaMemsetAsync(status, 0, (size_t)(tiles + 1) * 8, st));
   k_scan_u32<<<tiles, SCAN_THREADS, 0, st>>>(tdeg, tro, n, status);
   CK(h, cudaMemcpyAsync(tdeg, tro, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));  // cursors
   k_transpose<<<h->num_sms * 16, 256, 0, st>>>(ro, col, n, tdeg, tunsorted);
@@ -563,6 +563,8 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
     const long long hv = h->opt.hub_vertices;
     long long hub = hv < 0 ? n : hv > 0 ? hv : (h->opt.reorder >= 0 ? (1LL << 20) : n);
     P.hub = (int32_t)(hub < n ? hub : n);
+    const int tp = h->opt.tag_mode_pct;
+    P.tag_pct = tp == 0 ? S3BFS_TAG_MODE_PCT : tp < 0 ? -1 : tp;
   }
   P.fb[0] = (uint32_t *)(base + o_fb0);
   P.fb[1] = (uint32_t *)(base + o_fb1);
@@ -932,10 +934,10 @@ s3bfs_status s3bfs_debug_exclusive_scan(const int32_t *in, int32_t *out, int32_t
   }
   const int tiles = (int)(((long long)n + SCAN_TILE - 1) / SCAN_TILE);
   AsyncTmp status_b(stream);
-  cudaError_t e = status_b.alloc((size_t)tiles * 8);
+  cudaError_t e = status_b.alloc((size_t)(tiles + 1) * 8);  // + the tile counter
   if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaMallocAsync(status)");
   unsigned long long *status = status_b.as<unsigned long long>();
-  cudaMemsetAsync(status, 0, (size_t)tiles * 8, stream);
+  cudaMemsetAsync(status, 0, (size_t)(tiles + 1) * 8, stream);
   k_scan_u32<<<tiles, SCAN_THREADS, 0, stream>>>(in, out, n, status);
   e = cudaGetLastError();
   return e == cudaSuccess ? S3BFS_OK : cuda_fail(nullptr, e, "k_scan_u32");

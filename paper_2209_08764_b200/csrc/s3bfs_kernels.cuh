@@ -35,6 +35,8 @@
 #include <cooperative_groups.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "../../include/s3bfs.h"
 
 namespace s3bfs {
@@ -81,6 +83,9 @@ namespace s3bfs {
 #endif
 #ifndef S3BFS_CLAIM_MIN_BYTES
 #define S3BFS_CLAIM_MIN_BYTES (8u << 20)  // claim array floor (measured, DESIGN R26)
+#endif
+#ifndef S3BFS_TAG_MODE_PCT
+#define S3BFS_TAG_MODE_PCT 80  // default of opts.tag_mode_pct
 #endif
 #ifndef S3BFS_BU_W
 #define S3BFS_BU_W 4
@@ -149,6 +154,8 @@ struct Ctl {
   int32_t source;
   int32_t bu;               // NEXT-3: the current level runs bottom-up
   int32_t fb_valid;         // fb[cur] already holds the current frontier (a bottom-up product)
+  int32_t probe_tags;       // k_explore's visited test of this level: tag mode (1) or bitmap
+                            // mode (0), see k_explore; set by decide_tier
   long long m_visited;      // sum of the degrees of all visited vertices (Beamer's m_u = m - it)
   int32_t *level_out, *parent_out;
   unsigned long long t_prev;
@@ -179,8 +186,9 @@ struct Params {
   uint8_t *claim;               // per-vertex discovery tag: nonzero once v was discovered (in
                                 //  any level, by any kernel), at slot claim_slot(v) (scattered)
   uint32_t claim_mask;          // claim array size - 1 (a power of two >= n)
-  int32_t hub;                  // k_explore: ids < hub are tested in the bitmap first, the
-                                //  others by their discovery tag alone (one probe)
+  int32_t hub;                  // k_explore tag mode: ids < hub are tested in the bitmap
+                                //  first, the others by their discovery tag alone (one probe)
+  int32_t tag_pct;              // tag mode while m_visited < tag_pct % of nnz (< 0: never)
   uint32_t *fb[2];              // NEXT-3: frontier bitmaps (bottom-up levels only)
   const int32_t *tro, *tcol;    // NEXT-3: in-adjacency (internal ids) the bottom-up step scans
   int32_t *wcnt;
@@ -288,50 +296,10 @@ __device__ __forceinline__ int ld_cg_u8(const uint8_t *p) {
 // reads its visited-bitmap word through the read-only path (L1-resident for the hottest ids),
 // any other id reads its discovery tag at L2 (evict-last: the tags must outlive the col
 // stream).  The caller decodes: a bit of the word, or tag == 0 ("not discovered yet").
-#ifndef S3BFS_PROBE1
-#define S3BFS_PROBE1 1  // one 32-bit load per probe (tag word or bitmap word); 0: two predicated loads
-#endif
-__device__ __forceinline__ uint32_t probe_status(int v, int hub, uint32_t tag_span,
-                                                 const uint8_t *tags, uint32_t tag_mask,
-                                                 const uint32_t *bm, unsigned long long pol) {
-  // the tag-or-bitmap choice ((v - hub) < tag_span, unsigned) and both addresses (tag slot =
-  // (v * 0x9E3779B1) mod 2^k, see claim_slot; word = v >> 5) are formed inside, so no
-  // predicate or 64-bit address of a group stays live across the batch's probes
-  uint32_t r;
-#if S3BFS_PROBE1
-  // one weak 32-bit load: the aligned word holding v's tag byte, or v's bitmap word.  The
-  // caller shifts the tag byte down ((slot & 3) * 8).
-  asm("{\n\t.reg .pred p;\n\t.reg .u32 s;\n\t.reg .u64 a;\n\t"
-      "sub.s32 s, %1, %2;\n\t"
-      "setp.lt.u32 p, s, %3;\n\t"
-      "@p mul.lo.u32 s, %1, -1640531535;\n\t"
-      "@p and.b32 s, s, %4;\n\t"
-      "@p and.b32 s, s, -4;\n\t"
-      "@p cvt.u64.u32 a, s;\n\t"
-      "@p add.u64 a, a, %5;\n\t"
-      "@!p shr.s32 s, %1, 5;\n\t"
-      "@!p mul.wide.s32 a, s, 4;\n\t"
-      "@!p add.u64 a, a, %6;\n\t"
-      "ld.global.L2::cache_hint.u32 %0, [a], %7;\n\t}"
-      : "=r"(r)
-      : "r"(v), "r"(hub), "r"(tag_span), "r"(tag_mask), "l"(tags), "l"(bm), "l"(pol));
-#else
-  asm("{\n\t.reg .pred p;\n\t.reg .u32 s;\n\t.reg .u64 a;\n\t"
-      "sub.s32 s, %1, %2;\n\t"
-      "setp.lt.u32 p, s, %3;\n\t"
-      "@p mul.lo.u32 s, %1, -1640531535;\n\t"
-      "@p and.b32 s, s, %4;\n\t"
-      "@p cvt.u64.u32 a, s;\n\t"
-      "@p add.u64 a, a, %5;\n\t"
-      "@p ld.global.cg.L2::cache_hint.u8 %0, [a], %7;\n\t"
-      "@!p shr.s32 s, %1, 5;\n\t"
-      "@!p mul.wide.s32 a, s, 4;\n\t"
-      "@!p add.u64 a, a, %6;\n\t"
-      "@!p ld.global.nc.L2::cache_hint.u32 %0, [a], %7;\n\t}"
-      : "=r"(r)
-      : "r"(v), "r"(hub), "r"(tag_span), "r"(tag_mask), "l"(tags), "l"(bm), "l"(pol));
-#endif
-  return r;
+__device__ __forceinline__ int ld_cg_u8_hint(const uint8_t *p, unsigned long long pol) {
+  unsigned v;
+  asm volatile("ld.global.cg.L2::cache_hint.u8 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return (int)v;
 }
 __device__ __forceinline__ void st_u8(uint8_t *p, int v) {
   asm volatile("st.global.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -562,6 +530,10 @@ __device__ void decide_tier(const Params &P, Ctl *c, int32_t n_l, int32_t e_l) {
   if (p_l < 1) p_l = 1;  // an empty slice still runs one (idle) CTA: k_compact reports 0
   c->e_lo = (int32_t)e_lo;
   c->e_hi = (int32_t)e_hi;
+  // k_explore's visited test: tag mode while few arcs end at visited vertices (m_visited =
+  // degrees of all visited vertices, the frontier included; arc ends for a symmetric graph)
+  c->probe_tags = P.hub < P.n && P.tag_pct >= 0 &&
+                  (double)c->m_visited * 100.0 < (double)P.nnz * (double)P.tag_pct;
   c->tier = TIER_LARGE;
   c->p_l = (int32_t)p_l;
   c->chunk = (int32_t)chunk;
@@ -792,66 +764,82 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
     }
     return e_next;
   };
-  int e = e_begin;
-  while (e < e_end) {
-    int v[KX_GROUPS];
-    uint32_t xs[KX_GROUPS / 4];  // window slots of the groups' frontier vertices, one byte each
-#pragma unroll
-    for (int k = 0; k < KX_GROUPS / 4; ++k) xs[k] = 0;
-    e = map_load(e, v, xs);
-    // visited test (Fig1 L18), one probe per arc: a hub id reads the visited bitmap (exact at
-    // level start, hot words L1-resident), any other id its discovery tag, which is nonzero once
-    // some worker discovered it in this or an earlier level.  Masked slots probe the sentinel
-    // (a bitmap bit that is always set), so the test is branch-free.
-    uint32_t needm = 0;  // hub ids not visited at level start: their tag decides
-    uint32_t discm = 0;  // ids found undiscovered: candidates (Fig1 L19-L22)
+  // Discovery of the batch's groups flagged in discm (Fig1 L18-L22): plain stores -- the tag,
+  // {d, parent}, Owner = the candidate slot, and the candidate itself (benign race, R4).
+  auto discover = [&](const int (&v)[KX_GROUPS], const uint32_t (&xs)[KX_GROUPS / 4],
+                      uint32_t discm) {
+    const unsigned wdisc = __reduce_or_sync(0xffffffffu, discm);
+    if (!wdisc) return;  // warp-uniform skip: most batches of the heavy levels find nothing
 #pragma unroll
     for (int g = 0; g < KX_GROUPS; ++g) {
-      const uint32_t r = probe_status(v[g], hub, tag_span, claim, P.claim_mask, bm, pol_status);
-      const bool via_tag = (uint32_t)(v[g] - hub) < tag_span;
-      const uint32_t bit_clear = ~rotr32(r, v[g]) & 1u;
-#if S3BFS_PROBE1
-      const uint32_t tagv = (r >> (((uint32_t)v[g] * 0x9E3779B1u & 3u) * 8)) & 0xffu;
-#else
-      const uint32_t tagv = r;
-#endif
-      needm |= (via_tag ? 0u : bit_clear) << g;
-      discm |= (via_tag ? (uint32_t)(tagv == 0u) : 0u) << g;
-    }
-    const unsigned wneed = __reduce_or_sync(0xffffffffu, needm);
-    if (wneed) {  // warp-uniform skip: after the first levels the hubs are all visited
-#pragma unroll
-      for (int h = 0; h < KX_GROUPS; h += 4) {  // 4 tag loads in flight (register budget)
-        int cl[4];
-#pragma unroll
-        for (int g = 0; g < 4; ++g)
-          cl[g] = ((needm >> (h + g)) & 1u) ? ld_cg_u8(claim + claim_slot(P, v[h + g])) : 1;
-#pragma unroll
-        for (int g = 0; g < 4; ++g) discm |= (uint32_t)(cl[g] == 0) << (h + g);
+      if (!((wdisc >> g) & 1u)) continue;
+      // parent: the window slot's caller id (the window is unchanged since map_load)
+      const int par = __shfl_sync(0xffffffffu, wx, (xs[g >> 2] >> (8 * (g & 3))) & 31u);
+      const bool disc = (discm >> g) & 1u;
+      const unsigned m = __ballot_sync(0xffffffffu, disc);
+      if (disc) {
+        const int slot = segbase + wcount + __popc(m & lanemask_lt());
+        st_u8(claim + claim_slot(P, v[g]), tag);
+        st_weak_v2(lp + v[g], new_level, par);     // d[v] <- l, parent (Fig1 L18)
+        st_weak(owner_of(vinfo, v[g]), slot);      // Owner[v] <- i (benign race)
+        cand[slot] = v[g];                         // Q[i].Enqueue(v)
       }
+      wcount += __popc(m);
     }
-    // discovery only for the groups where some lane found an undiscovered vertex (warp-uniform
-    // skip: on the heavy levels most batches have none or one or two such groups)
-    const unsigned wdisc = __reduce_or_sync(0xffffffffu, discm);
-    if (wdisc) {
+  };
+  // The level's visited test (Fig1 L18 "if d[v] = infinity"), chosen per level by
+  // decide_tier from the share of arcs that end at visited vertices:
+  //  bitmap mode (most targets visited, the heavy levels): every target's visited bit (exact
+  //    at level start; hub words L1-resident), then the discovery tag of the few clear ones;
+  //  tag mode (most targets new, the discovery-heavy levels): a hub id (< P.hub) reads its
+  //    bit first, any other id only its discovery tag (nonzero once discovered) -- one probe
+  //    instead of two for the arcs that reach new vertices.
+  // Masked slots probe the sentinel (its bit is always set), so the tests are branch-free.
+  auto run = [&](auto tag_mode) {
+    constexpr bool TAGS = decltype(tag_mode)::value;
+    int e = e_begin;
+    while (e < e_end) {
+      int v[KX_GROUPS];
+      uint32_t xs[KX_GROUPS / 4];  // window slots of the groups' frontier vertices, a byte each
 #pragma unroll
-      for (int g = 0; g < KX_GROUPS; ++g) {
-        if (!((wdisc >> g) & 1u)) continue;
-        // parent: the window slot's caller id (the window is unchanged since map_load)
-        const int par = __shfl_sync(0xffffffffu, wx, (xs[g >> 2] >> (8 * (g & 3))) & 31u);
-        const bool disc = (discm >> g) & 1u;
-        const unsigned m = __ballot_sync(0xffffffffu, disc);
-        if (disc) {
-          const int slot = segbase + wcount + __popc(m & lanemask_lt());
-          st_u8(claim + claim_slot(P, v[g]), tag);
-          st_weak_v2(lp + v[g], new_level, par);     // d[v] <- l, parent (Fig1 L18)
-          st_weak(owner_of(vinfo, v[g]), slot);      // Owner[v] <- i (benign race)
-          cand[slot] = v[g];                         // Q[i].Enqueue(v)
+      for (int k = 0; k < KX_GROUPS / 4; ++k) xs[k] = 0;
+      e = map_load(e, v, xs);
+      uint32_t needm = 0;  // targets whose discovery tag decides (bit clear at level start)
+      uint32_t discm = 0;  // targets found undiscovered: candidates (Fig1 L19-L22)
+      if constexpr (TAGS) {
+#pragma unroll
+        for (int g = 0; g < KX_GROUPS; ++g) {
+          const bool via_tag = (uint32_t)(v[g] - hub) < tag_span;
+          uint32_t r;
+          if (via_tag) r = (uint32_t)ld_cg_u8_hint(claim + claim_slot(P, v[g]), pol_status);
+          else r = ldg_status_u32(bm + (v[g] >> 5), pol_status);
+          needm |= (via_tag ? 0u : (~rotr32(r, v[g]) & 1u)) << g;
+          discm |= (via_tag ? (uint32_t)(r == 0u) : 0u) << g;
         }
-        wcount += __popc(m);
+      } else {
+#pragma unroll
+        for (int g = 0; g < KX_GROUPS; ++g) {
+          const uint32_t w = ldg_status_u32(bm + (v[g] >> 5), pol_status);
+          needm |= (~rotr32(w, v[g]) & 1u) << g;  // bit (v mod 32) of w, inverted
+        }
       }
+      const unsigned wneed = __reduce_or_sync(0xffffffffu, needm);
+      if (wneed) {  // warp-uniform skip
+#pragma unroll
+        for (int h = 0; h < KX_GROUPS; h += 4) {  // 4 tag loads in flight (register budget)
+          int cl[4];
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            cl[g] = ((needm >> (h + g)) & 1u) ? ld_cg_u8(claim + claim_slot(P, v[h + g])) : 1;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) discm |= (uint32_t)(cl[g] == 0) << (h + g);
+        }
+      }
+      discover(v, xs, discm);
     }
-  }
+  };
+  if (c->probe_tags) run(std::true_type{});
+  else run(std::false_type{});
   if (lane == 0) P.wcnt[b * KD_WARPS + warp] = wcount;
 }
 
@@ -1941,10 +1929,18 @@ __global__ void k_build_vinfo(const int32_t *ro, const int32_t *n2o, int n, int4
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_u32(const int32_t *__restrict__ in,
                                                            int32_t *__restrict__ out, int n,
                                                            unsigned long long *status) {
+  // status[0, gridDim.x) = look-back words, status[gridDim.x] = tile counter (all zeroed by
+  // the caller): tiles are numbered in CTA start order, so a spinning CTA only ever waits for
+  // CTAs that already started (forward progress next to concurrent traversals, as k_compact)
   __shared__ int32_t s_w[SCAN_THREADS / 32];
   __shared__ uint32_t s_ex;
+  __shared__ int s_tile;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const long long base = (long long)blockIdx.x * SCAN_TILE + (long long)tid * SCAN_ITEMS;
+  if (tid == 0)
+    s_tile = (int)atomicAdd(reinterpret_cast<unsigned int *>(status + gridDim.x), 1u);
+  __syncthreads();
+  const int tile = s_tile;
+  const long long base = (long long)tile * SCAN_TILE + (long long)tid * SCAN_ITEMS;
   int x[SCAN_ITEMS];
   int sum = 0;
 #pragma unroll
@@ -1960,9 +1956,9 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_u32(const int32_t *__rest
     const int ia = warp_incl_scan(a);
     if (lane < SCAN_THREADS / 32) s_w[lane] = ia - a;
     const Pair agg{(uint32_t)__shfl_sync(0xffffffffu, ia, 31), 0};
-    const Pair ex = lookback<false>(status, blockIdx.x, agg);
+    const Pair ex = lookback<false>(status, tile, agg);
     if (lane == 0) s_ex = ex.a;
-    if (lane == 0 && blockIdx.x == gridDim.x - 1) out[n] = (int)(ex.a + agg.a);
+    if (lane == 0 && tile == (int)gridDim.x - 1) out[n] = (int)(ex.a + agg.a);
   }
   __syncthreads();
   int run = (int)(s_ex + (uint32_t)s_w[warp] + (uint32_t)(inc - sum));

@@ -25,7 +25,8 @@ class DistRank:
     def __init__(self, row_offsets, col_indices, rank: int, size: int,
                  options: _s.Options | None = None, stream=None):
         import torch
-        o = _s.Options() if options is None else options
+        # a copy: the caller's options object is never turned into a dist configuration
+        o = _s.Options() if options is None else _s.Options.from_buffer_copy(options)
         o.dist_size, o.dist_rank = int(size), int(rank)
         self.rank, self.size = int(rank), int(size)
         self.row_offsets, self.col_indices = row_offsets, col_indices

@@ -45,7 +45,7 @@ class Options(ctypes.Structure):
                 ("direction", ctypes.c_int32), ("do_alpha", ctypes.c_int32),
                 ("do_beta", ctypes.c_int32), ("dist_size", ctypes.c_int32),
                 ("dist_rank", ctypes.c_int32), ("cluster_max_edges", ctypes.c_int32),
-                ("hub_vertices", ctypes.c_int32)]
+                ("hub_vertices", ctypes.c_int32), ("tag_mode_pct", ctypes.c_int32)]
 
 
 class LevelStat(ctypes.Structure):
@@ -188,8 +188,10 @@ def s3bfs_status_string(status: int) -> str:
     return load().s3bfs_status_string(int(status)).decode()
 
 
-def s3bfs_get_level_stats(handle, cap: int = 1 << 16) -> np.ndarray:
-    """Per-level records of the last run as a numpy structured array."""
+def s3bfs_get_level_stats(handle, cap: int = 1 << 16, return_total: bool = False):
+    """Per-level records of the last run as a numpy structured array.  The device keeps at
+    most min(n + 1, 65536) records (and this call at most ``cap``): a deeper traversal returns
+    the first records with a warning; ``return_total`` also returns the true level count."""
     buf = (LevelStat * cap)()
     num = ctypes.c_int32()
     _check(load().s3bfs_get_level_stats(handle, buf, cap, ctypes.byref(num)),
@@ -200,9 +202,12 @@ def s3bfs_get_level_stats(handle, cap: int = 1 << 16) -> np.ndarray:
                    ("t_begin_ns", "u8"), ("t_end_ns", "u8"), ("t_explore_begin_ns", "u8"),
                    ("t_explore_end_ns", "u8")])
     out = np.frombuffer(bytes(buf)[: k * ctypes.sizeof(LevelStat)], dtype=dt).copy()
-    if num.value > cap:
-        raise S3BFSError(0, "s3bfs_get_level_stats", f"{num.value} levels > cap {cap}")
-    return out
+    k = min(k, out.shape[0])
+    if num.value > out.shape[0]:
+        import warnings
+        warnings.warn(f"s3bfs_get_level_stats: {num.value} levels, first {out.shape[0]} "
+                      f"records kept", RuntimeWarning, stacklevel=2)
+    return (out, int(num.value)) if return_total else out
 
 
 def s3bfs_get_info(handle) -> dict:

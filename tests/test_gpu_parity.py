@@ -37,13 +37,18 @@ SETTINGS = [
     ("bu-mixed", dict(debug_poison=1, tier0_max_edges=16, direction=1, do_alpha=64, do_beta=3)),
     ("bu-no-reorder", dict(debug_poison=1, reorder=-1, tier0_max_edges=-1, direction=1,
                            do_alpha=1 << 30, do_beta=-1)),
-    # k_explore's visited test: ids >= hub_vertices by their discovery tag alone (tiny graphs
-    # are below the default 2^20, so these force the tag path: tags written by every tier)
-    ("hub-1-tier1", dict(debug_poison=1, hub_vertices=1, tier0_max_edges=-1)),
-    ("hub-5-T0-16", dict(debug_poison=1, hub_vertices=5, tier0_max_edges=16)),
-    ("hub-3-bu-mixed", dict(debug_poison=1, hub_vertices=3, tier0_max_edges=16, direction=1,
-                            do_alpha=64, do_beta=3)),
-    ("hub-all-bitmap", dict(debug_poison=1, hub_vertices=-1, tier0_max_edges=-1)),
+    # k_explore's tag mode (ids >= hub_vertices tested by their discovery tag alone): tiny
+    # graphs are below the default 2^20 hub ids, so these force it -- on every level, on a mix
+    # of levels (50 %), after tier-0 / cluster / bottom-up levels (tags written by every tier)
+    ("tags-hub1-tier1", dict(debug_poison=1, hub_vertices=1, tag_mode_pct=101,
+                             tier0_max_edges=-1)),
+    ("tags-hub5-T0-16", dict(debug_poison=1, hub_vertices=5, tag_mode_pct=101,
+                             tier0_max_edges=16)),
+    ("tags-hub3-mixed-levels", dict(debug_poison=1, hub_vertices=3, tag_mode_pct=50,
+                                    tier0_max_edges=-1)),
+    ("tags-hub3-bu-mixed", dict(debug_poison=1, hub_vertices=3, tag_mode_pct=101,
+                                tier0_max_edges=16, direction=1, do_alpha=64, do_beta=3)),
+    ("tags-never", dict(debug_poison=1, tag_mode_pct=-1, tier0_max_edges=-1)),
 ]
 
 
