@@ -94,7 +94,7 @@ typedef struct {
                               ids below this count (the highest-degree vertices, whose visited
                               bits stay L1-resident) are tested in the visited bitmap first, all
                               others directly by their 1-byte discovery tag (one probe).  0 ->
-                              the default (2^20); < 0 -> every vertex through the bitmap first */
+                              the default (2^19); < 0 -> every vertex through the bitmap first */
   int32_t tag_mode_pct;    /* that split ("tag mode") is used on a level while fewer than this
                               percentage of all arcs end at visited vertices (the discovery-heavy
                               levels); other levels test every target's visited bit first.

@@ -561,7 +561,7 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   // the graph is degree-ordered), the rest by their discovery tag alone (R26)
   {
     const long long hv = h->opt.hub_vertices;
-    long long hub = hv < 0 ? n : hv > 0 ? hv : (h->opt.reorder >= 0 ? (1LL << 20) : n);
+    long long hub = hv < 0 ? n : hv > 0 ? hv : (h->opt.reorder >= 0 ? (1LL << 19) : n);
     P.hub = (int32_t)(hub < n ? hub : n);
     const int tp = h->opt.tag_mode_pct;
     P.tag_pct = tp == 0 ? S3BFS_TAG_MODE_PCT : tp < 0 ? -1 : tp;

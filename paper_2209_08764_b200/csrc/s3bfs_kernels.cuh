@@ -532,7 +532,7 @@ __device__ void decide_tier(const Params &P, Ctl *c, int32_t n_l, int32_t e_l) {
   c->e_hi = (int32_t)e_hi;
   // k_explore's visited test: tag mode while few arcs end at visited vertices (m_visited =
   // degrees of all visited vertices, the frontier included; arc ends for a symmetric graph)
-  c->probe_tags = P.hub < P.n && P.tag_pct >= 0 &&
+  c->probe_tags = P.tag_pct >= 0 &&
                   (double)c->m_visited * 100.0 < (double)P.nnz * (double)P.tag_pct;
   c->tier = TIER_LARGE;
   c->p_l = (int32_t)p_l;
@@ -767,7 +767,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   // Discovery of the batch's groups flagged in discm (Fig1 L18-L22): plain stores -- the tag,
   // {d, parent}, Owner = the candidate slot, and the candidate itself (benign race, R4).
   auto discover = [&](const int (&v)[KX_GROUPS], const uint32_t (&xs)[KX_GROUPS / 4],
-                      uint32_t discm) {
+                      uint32_t discm, auto with_tags) {
     const unsigned wdisc = __reduce_or_sync(0xffffffffu, discm);
     if (!wdisc) return;  // warp-uniform skip: most batches of the heavy levels find nothing
 #pragma unroll
@@ -779,7 +779,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
       const unsigned m = __ballot_sync(0xffffffffu, disc);
       if (disc) {
         const int slot = segbase + wcount + __popc(m & lanemask_lt());
-        st_u8(claim + claim_slot(P, v[g]), tag);
+        if constexpr (decltype(with_tags)::value) st_u8(claim + claim_slot(P, v[g]), tag);
         st_weak_v2(lp + v[g], new_level, par);     // d[v] <- l, parent (Fig1 L18)
         st_weak(owner_of(vinfo, v[g]), slot);      // Owner[v] <- i (benign race)
         cand[slot] = v[g];                         // Q[i].Enqueue(v)
@@ -789,11 +789,17 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   };
   // The level's visited test (Fig1 L18 "if d[v] = infinity"), chosen per level by
   // decide_tier from the share of arcs that end at visited vertices:
-  //  bitmap mode (most targets visited, the heavy levels): every target's visited bit (exact
-  //    at level start; hub words L1-resident), then the discovery tag of the few clear ones;
   //  tag mode (most targets new, the discovery-heavy levels): a hub id (< P.hub) reads its
-  //    bit first, any other id only its discovery tag (nonzero once discovered) -- one probe
-  //    instead of two for the arcs that reach new vertices.
+  //    visited bit (exact at level start; hub words L1-resident) and, if clear, its discovery
+  //    tag; any other id reads only its tag (nonzero once discovered, in this or an earlier
+  //    level).  A discoverer stores the tag, so a vertex that many frontier arcs reach in this
+  //    level is enqueued about once, not once per arc;
+  //  bitmap mode (most targets visited, the heavy levels that follow): the visited bit alone,
+  //    the paper's d[v] test on d as it stood at level start.  The few new targets of such a
+  //    level have low degree, so racing discoverers are rare; each enqueues the vertex and
+  //    the Owner check keeps one (R4) -- no second dependent load on the ~98 % of
+  //    batches that meet some new vertex (measured).  No later level reads the
+  //    tags (the share of visited arcs only grows), so none are written.
   // Masked slots probe the sentinel (its bit is always set), so the tests are branch-free.
   auto run = [&](auto tag_mode) {
     constexpr bool TAGS = decltype(tag_mode)::value;
@@ -820,8 +826,10 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
 #pragma unroll
         for (int g = 0; g < KX_GROUPS; ++g) {
           const uint32_t w = ldg_status_u32(bm + (v[g] >> 5), pol_status);
-          needm |= (~rotr32(w, v[g]) & 1u) << g;  // bit (v mod 32) of w, inverted
+          discm |= (~rotr32(w, v[g]) & 1u) << g;  // bit (v mod 32) of w, inverted
         }
+        discover(v, xs, discm, std::false_type{});
+        continue;
       }
       const unsigned wneed = __reduce_or_sync(0xffffffffu, needm);
       if (wneed) {  // warp-uniform skip
@@ -835,7 +843,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
           for (int g = 0; g < 4; ++g) discm |= (uint32_t)(cl[g] == 0) << (h + g);
         }
       }
-      discover(v, xs, discm);
+      discover(v, xs, discm, std::true_type{});
     }
   };
   if (c->probe_tags) run(std::true_type{});

@@ -19,7 +19,7 @@ for r in csv.DictReader(rows):
     v = float(r["Metric Value"].replace(",", ""))
     unit = r["Metric Unit"]
     if r["Metric Name"] == "gpu__time_duration.sum":
-        v = v * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(unit, 1.0)
+        v = v * {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "second": 1e3}.get(unit, 1.0)
     elif unit in ("Kbyte", "Mbyte", "Gbyte"):
         v = v * {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
     launch[r["ID"]][r["Metric Name"]] = v
