@@ -637,6 +637,9 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
     h->ro_int = row_offsets;
   }
   P.col_vec = (((uintptr_t)P.col) & 15) == 0 ? 1 : 0;
+  // the internal copy is allocated with 16 bytes of slack (its last chunk may be read whole);
+  // the caller's array only up to nnz
+  P.col_cap = (share ? share->P.col_cap : (h->opt.reorder >= 0 ? nnz + 4 : nnz));
   if (P.direction && !share) {
     s3bfs_status ts = build_in_adjacency(h, stream);
     if (ts != S3BFS_OK) return bail(ts);

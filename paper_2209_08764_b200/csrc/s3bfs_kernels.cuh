@@ -208,6 +208,7 @@ struct Params {
   unsigned long long *m_status; // NEXT-4: merge look-back words
   long long nnz;
   int32_t col_vec;              // col is 16-byte aligned: vectorised loads allowed
+  long long col_cap;            // col elements that may be read (16-byte chunks up to it)
   int32_t use_graph;
   unsigned long long h_while, h_tier;  // cudaGraphConditionalHandle values (WHILE; SWITCH on
                                        // the tier: body 0 tier 0, 1 top-down, 2 bottom-up)
@@ -599,19 +600,22 @@ __global__ void k_policies(unsigned long long *out) {
 // CTA b < P_l owns global edges [b*chunk, min((b+1)*chunk, e_l)) of the level, split evenly
 // over its warps: each warp is one of the paper's workers with an (almost) equal share of the
 // level's edges (Fig1 L16-L17).  A warp finds its start vertex with the 32-ary search
-// (c), then walks its edges in batches of KX_GROUPS groups of 32 -- lane i takes edge e+i, so
-// a group reads 32 consecutive col entries (coalesced streaming, Fig1 L18).  Edge -> frontier
-// vertex mapping uses a register window of 32 consecutive frontier vertices (their
-// degree-scan entries, ids and row starts): one warp-uniform shuffle search per batch, and a
-// per-lane search only when the batch spans several rows.  No shared memory, no CTA barrier,
-// so warps progress independently.
-// Visited test (the paper's "d[v] = infinity", R1): the visited bitmap (exact at level start,
-// read-only here) and, for a clear bit, the vertex's 1-byte claim tag, which equals this
-// level's tag once some worker discovered v in this level.
-// Discovery (EXPLORE-VERTEX): claim[v] = tag, {d, parent}[v] = {l+1, x}, Owner[v] =
-// slot, cand[slot] = v -- plain stores, the paper's benign race, no atomics.  Racing
-// discoverers that all saw an old tag store the same d and a valid parent and enqueue
-// duplicates; the Owner check keeps exactly one (R4).
+// (c), then streams its edges (Fig1 L18) through a register window of 32 consecutive frontier
+// rows.
+// Streaming unit = an aligned 16-byte col chunk (4 arcs): each window row's slice of the
+// warp's edge range covers [cs, ce) of col, i.e. chunks cs/4 .. (ce-1)/4; the window's rows
+// with a non-empty slice are compacted to the front lanes, and an exclusive scan of their chunk
+// counts numbers the window's chunks.  A round gives every lane 2 chunks (one 16-byte load
+// each, 8 arcs; 256 arcs per warp): lane i's chunk c belongs to the row whose first chunk is
+// the last one <= c -- one REDUX of the rows' first-chunk bits per 32 chunks, then a popc (the
+// compacted rows start at strictly increasing chunks, so the rank is exact).  The first and
+// last chunk of a row mask the elements outside [cs, ce) (they belong to other rows).  No
+// shared memory and no CTA barrier, so warps progress independently.
+// Visited test (the paper's "d[v] = infinity", R1): see run() below.  Discovery
+// (EXPLORE-VERTEX): tag[v] = tag (tag mode), {d, parent}[v] = {l+1, x}, Owner[v] = slot,
+// cand[slot] = v -- plain stores, the paper's benign race, no atomics.  Racing discoverers
+// store the same d and a valid parent and enqueue duplicates; the Owner check keeps exactly
+// one (R4).
 __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P) {
   Ctl *c = P.ctl;
   if (c->tier != TIER_LARGE) return;
@@ -622,6 +626,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   const int n_l = c->n_l, chunk = c->chunk, cur = c->cur, wcap = c->wcap;
   const int new_level = c->level + 1;     // Fig1 L10: discoveries get l+1 (R11)
   const int tag = 1 + (c->level % 255);   // never 0, the per-run initial value
+  const bool tag_mode = c->probe_tags != 0;
   const int32_t *__restrict__ fx = P.f[cur];
   const int32_t *__restrict__ frs = P.frs[cur];
   const int32_t *__restrict__ fex = P.fex[cur];
@@ -631,9 +636,9 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   int32_t *__restrict__ cand = P.cand;
   const uint32_t *__restrict__ bm = P.bm;
   uint8_t *__restrict__ claim = P.claim;
-  const int vs = P.v_sent;  // masked lanes' target: its visited bit is always set
-  const int hub = P.hub;                              // ids < hub: bitmap first
-  const uint32_t tag_span = (uint32_t)(P.n - P.hub);  // ids in [hub, n): tag only
+  const int vs = P.v_sent;  // masked elements' target: its visited bit is always set
+  const int hub = P.hub;                              // tag mode: ids < hub bitmap first
+  const uint32_t tag_span = (uint32_t)(P.n - P.hub);  // tag mode: ids in [hub, n) tag only
 
   if (tid == 0) {
     P.status[b] = 0ull;  // reset k_compact's look-back word for this level
@@ -646,208 +651,153 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   const int segbase = (b * KD_WARPS + warp) * wcap;
   const unsigned long long pol_stream = P.pol_first;
   const unsigned long long pol_status = P.pol_last;
+  const unsigned le = 0xffffffffu >> (31 - lane);  // bits 0 .. lane
+  const bool vec = P.col_vec != 0;
+  const long long col_cap = P.col_cap;             // readable col elements (>= nnz)
   int wcount = 0;
-  int u0 = 0, wex = 0, wx = 0, wb = 0, lim = 0;
-  bool wzero = false;  // the window holds an empty row (two equal row starts)
-  auto load_window = [&](int base) {
-    const int u = base + lane;
-    wex = (u < n_l) ? __ldg(fex + u) : 0x7fffffff;
-    wx = (u < n_l) ? __ldg(fx + u) : 0;
-    wb = (u < n_l) ? __ldg(frs + u) - wex : 0;
-    lim = __ldg(fex + min(base + 32, n_l));
-    const int down = __shfl_down_sync(0xffffffffu, wex, 1);  // all lanes shuffle
-    const int nxt_start = (lane < 31) ? down : lim;
-    wzero = __any_sync(0xffffffffu, u < n_l && nxt_start == wex);
-  };
-  if (e_begin < e_end) {
-    u0 = warp_search(fex, n_l, e_begin);  // Find-StartExpPoint (c)
-    load_window(u0);
-  }
-  // Map the batch of edges [e, e_next) onto lanes and load their targets: v[g] = col entry of
-  // edge e + 32g + lane (-1 outside the batch), byte g of xs = its frontier vertex's window slot
-  // (the caller id is shuffled only on discovery).
-  auto map_load = [&](int e, int (&v)[KX_GROUPS], uint32_t (&xs)[KX_GROUPS / 4]) -> int {
-    while (lim <= e) {  // window exhausted (also skips runs of zero-degree vertices, C9)
-      u0 += 32;
-      load_window(u0);
-    }
-    const int bend = min(e_end, lim);
-    // window slot of the batch's first edge (warp-uniform): the window's row starts are
-    // non-decreasing and wex_0 <= e, so it is the count of row starts <= e, minus one
-    const int j0 = __popc(__ballot_sync(0xffffffffu, wex <= e)) - 1;
-    const int row_end = (j0 < 31) ? __shfl_sync(0xffffffffu, wex, min(j0 + 1, 31)) : lim;
-    int e_next = min(e + KX_GROUPS * 32, bend);
-    if (S3BFS_KX_FAST && row_end >= e_next) {
-      // the whole batch lies in one frontier row (most R-MAT arcs): uniform x and base
-      const int x = j0;
-      const int base = __shfl_sync(0xffffffffu, wb, j0);
-      const int start = base + e;  // col index of the batch's first edge
-      const int a0 = start & ~3;   // 16-byte aligned
-#pragma unroll
-      for (int k = 0; k < KX_GROUPS / 4; ++k) xs[k] = (uint32_t)x * 0x01010101u;
-      if (S3BFS_KX_VEC && P.col_vec && (long long)a0 + KX_GROUPS * 32 <= P.nnz) {
-        // vectorised streaming: lane i loads 16 B at a0 + 4*(i + 32k), i.e. each warp
-        // instruction fetches 512 contiguous bytes of the row; edges outside
-        // [start, row/slice end) are masked.  Next batch starts 16-byte aligned.
-        const int lim_idx = base + bend;
-        if (a0 == start && a0 + KX_GROUPS * 32 <= lim_idx) {
-          // interior batch (aligned, whole): no masking
-#pragma unroll
-          for (int k = 0; k < KX_GROUPS / 4; ++k) {
-            const int4 q = ldg_stream4(col + a0 + 4 * (lane + 32 * k), pol_stream);
-            v[4 * k + 0] = q.x;
-            v[4 * k + 1] = q.y;
-            v[4 * k + 2] = q.z;
-            v[4 * k + 3] = q.w;
-          }
-        } else {
-#pragma unroll
-          for (int k = 0; k < KX_GROUPS / 4; ++k) {
-            const int i0 = a0 + 4 * (lane + 32 * k);
-            const int4 q = ldg_stream4(col + i0, pol_stream);  // in bounds: a0 + 256 <= nnz
-            v[4 * k + 0] = (i0 + 0 >= start && i0 + 0 < lim_idx) ? q.x : vs;
-            v[4 * k + 1] = (i0 + 1 >= start && i0 + 1 < lim_idx) ? q.y : vs;
-            v[4 * k + 2] = (i0 + 2 >= start && i0 + 2 < lim_idx) ? q.z : vs;
-            v[4 * k + 3] = (i0 + 3 >= start && i0 + 3 < lim_idx) ? q.w : vs;
-          }
-        }
-        e_next = min(bend, a0 + KX_GROUPS * 32 - base);
-      } else {
-#pragma unroll
-        for (int g = 0; g < KX_GROUPS; ++g) {  // masked lanes re-load the batch's first edge
-          const int my_e = e + g * 32 + lane;
-          const int t = ldg_stream(col + base + (my_e < bend ? my_e : e), pol_stream);
-          v[g] = (my_e < bend) ? t : vs;
-        }
-      }
-    } else if (S3BFS_KX_RANK && !wzero) {
-      // several rows in the batch: rank mapping.  Window lane j's row starts at edge wex_j;
-      // for group g (edges eg .. eg+31) the row starts strictly inside the group form a
-      // 32-bit mask (one REDUX), and lane i's row is the group's first row plus the number
-      // of row starts at or below edge eg+i (exact while no row of the window is empty)
-      // (row starts in [eg, eg+31] -> mask bit rel; r = row of edge eg-1, so lane i's row is
-      // r + popc(mask & bits 0..i); the batch's first edge lies in row j0)
-      const unsigned le = 0xffffffffu >> (31 - lane);  // bits 0 .. lane
-      const int pfirst = __shfl_sync(0xffffffffu, wb, j0) + e;  // col index of edge e (valid)
-      const int lb = bend - e - lane;  // group g's lane is inside the batch iff 32 g < lb
-      int r = j0;
-#pragma unroll
-      for (int g = 0; g < KX_GROUPS; ++g) {
-        const int eg = e + g * 32;
-        const int rel = wex - eg;  // this window lane's row start relative to the group
-        const unsigned m = __reduce_or_sync(0xffffffffu, shl1(rel));  // starts in [eg, eg+31]
-        if (g == 0) r -= (int)(m & 1u);  // a row starting exactly at e is row j0 itself
-        const int j = r + __popc(m & le);
-        xs[g >> 2] |= (uint32_t)j << (8 * (g & 3));
-        const int pos = __shfl_sync(0xffffffffu, wb, j) + eg + lane;
-        const bool ok = g * 32 < lb;
-        const int t = ldg_stream(col + (ok ? pos : pfirst), pol_stream);  // unconditional
-        v[g] = ok ? t : vs;
-        r += __popc(m);
-      }
-    } else {
-#pragma unroll
-      for (int g = 0; g < KX_GROUPS; ++g) {
-        const int my_e = e + g * 32 + lane;
-        int j = j0;  // largest window slot with excl <= my_e (>= j0)
-#pragma unroll
-        for (int s = 16; s >= 1; s >>= 1) {
-          const int cj = __shfl_sync(0xffffffffu, wex, min(j + s, 31));
-          if (j + s <= 31 && cj <= my_e) j += s;
-        }
-        xs[g >> 2] |= (uint32_t)j << (8 * (g & 3));
-        const int pos = __shfl_sync(0xffffffffu, wb, j) + my_e;
-        const int pf = __shfl_sync(0xffffffffu, wb, j0) + e;
-        const int t = ldg_stream(col + (my_e < bend ? pos : pf), pol_stream);
-        v[g] = (my_e < bend) ? t : vs;
-      }
-    }
-    return e_next;
-  };
-  // Discovery of the batch's groups flagged in discm (Fig1 L18-L22): plain stores -- the tag,
-  // {d, parent}, Owner = the candidate slot, and the candidate itself (benign race, R4).
-  auto discover = [&](const int (&v)[KX_GROUPS], const uint32_t (&xs)[KX_GROUPS / 4],
-                      uint32_t discm, auto with_tags) {
-    const unsigned wdisc = __reduce_or_sync(0xffffffffu, discm);
-    if (!wdisc) return;  // warp-uniform skip: most batches of the heavy levels find nothing
+
+  // Discovery of the flagged arcs (Fig1 L18-L22): one warp scan hands out the candidate slots
+  // of the whole round, then each lane stores its own (plain stores, benign race).
+  // wx = the window's caller ids; r0 / r1 = the window rows of the lane's two chunks
+  auto discover = [&](const int (&v)[KX_GROUPS], int wx, int r0, int r1, uint32_t discm) {
+    if (!__any_sync(0xffffffffu, discm != 0u)) return;  // most rounds of heavy levels
+    const int cnt = __popc(discm);
+    const int inc = warp_incl_scan(cnt);
+    int slot = segbase + wcount + inc - cnt;
+    wcount += __shfl_sync(0xffffffffu, inc, 31);
+    const int par0 = __shfl_sync(0xffffffffu, wx, r0);  // parents: the chunks' frontier
+    const int par1 = __shfl_sync(0xffffffffu, wx, r1);  // vertices (caller ids)
 #pragma unroll
     for (int g = 0; g < KX_GROUPS; ++g) {
-      if (!((wdisc >> g) & 1u)) continue;
-      // parent: the window slot's caller id (the window is unchanged since map_load)
-      const int par = __shfl_sync(0xffffffffu, wx, (xs[g >> 2] >> (8 * (g & 3))) & 31u);
-      const bool disc = (discm >> g) & 1u;
-      const unsigned m = __ballot_sync(0xffffffffu, disc);
-      if (disc) {
-        const int slot = segbase + wcount + __popc(m & lanemask_lt());
-        if constexpr (decltype(with_tags)::value) st_u8(claim + claim_slot(P, v[g]), tag);
+      if ((discm >> g) & 1u) {
+        const int par = g < 4 ? par0 : par1;
+        st_u8(claim + claim_slot(P, v[g]), tag);   // discovered (tag mode's visited test)
         st_weak_v2(lp + v[g], new_level, par);     // d[v] <- l, parent (Fig1 L18)
         st_weak(owner_of(vinfo, v[g]), slot);      // Owner[v] <- i (benign race)
         cand[slot] = v[g];                         // Q[i].Enqueue(v)
+        ++slot;
       }
-      wcount += __popc(m);
     }
   };
+
   // The level's visited test (Fig1 L18 "if d[v] = infinity"), chosen per level by
   // decide_tier from the share of arcs that end at visited vertices:
   //  tag mode (most targets new, the discovery-heavy levels): a hub id (< P.hub) reads its
   //    visited bit (exact at level start; hub words L1-resident) and, if clear, its discovery
   //    tag; any other id reads only its tag (nonzero once discovered, in this or an earlier
-  //    level).  A discoverer stores the tag, so a vertex that many frontier arcs reach in this
-  //    level is enqueued about once, not once per arc;
-  //  bitmap mode (most targets visited, the heavy levels that follow): the visited bit alone,
-  //    the paper's d[v] test on d as it stood at level start.  The few new targets of such a
-  //    level have low degree, so racing discoverers are rare; each enqueues the vertex and
-  //    the Owner check keeps one (R4) -- no second dependent load on the ~98 % of
-  //    batches that meet some new vertex (measured).  No later level reads the
-  //    tags (the share of visited arcs only grows), so none are written.
-  // Masked slots probe the sentinel (its bit is always set), so the tests are branch-free.
-  auto run = [&](auto tag_mode) {
-    constexpr bool TAGS = decltype(tag_mode)::value;
-    int e = e_begin;
-    while (e < e_end) {
-      int v[KX_GROUPS];
-      uint32_t xs[KX_GROUPS / 4];  // window slots of the groups' frontier vertices, a byte each
+  //    level) -- one probe instead of two for the arcs that reach new vertices;
+  //  bitmap mode (most targets visited, the heavy levels): the visited bit, then the tag of
+  //    the few clear ones (round 1's test; a discoverer stores the tag, so a vertex reached by
+  //    several frontier arcs in this level is enqueued about once).
+  // Masked elements probe the sentinel (its bit is always set), so the tests are branch-free.
+  auto probe_round = [&](int (&v)[KX_GROUPS], int wx, int r0, int r1, auto tmode) {
+    constexpr bool TAGS = decltype(tmode)::value;
+    uint32_t needm = 0;  // targets whose discovery tag decides (bit clear at level start)
+    uint32_t discm = 0;  // targets found undiscovered: candidates (Fig1 L19-L22)
+    if constexpr (TAGS) {
 #pragma unroll
-      for (int k = 0; k < KX_GROUPS / 4; ++k) xs[k] = 0;
-      e = map_load(e, v, xs);
-      uint32_t needm = 0;  // targets whose discovery tag decides (bit clear at level start)
-      uint32_t discm = 0;  // targets found undiscovered: candidates (Fig1 L19-L22)
-      if constexpr (TAGS) {
-#pragma unroll
-        for (int g = 0; g < KX_GROUPS; ++g) {
-          const bool via_tag = (uint32_t)(v[g] - hub) < tag_span;
-          uint32_t r;
-          if (via_tag) r = (uint32_t)ld_cg_u8_hint(claim + claim_slot(P, v[g]), pol_status);
-          else r = ldg_status_u32(bm + (v[g] >> 5), pol_status);
-          needm |= (via_tag ? 0u : (~rotr32(r, v[g]) & 1u)) << g;
-          discm |= (via_tag ? (uint32_t)(r == 0u) : 0u) << g;
-        }
-      } else {
-#pragma unroll
-        for (int g = 0; g < KX_GROUPS; ++g) {
-          const uint32_t w = ldg_status_u32(bm + (v[g] >> 5), pol_status);
-          discm |= (~rotr32(w, v[g]) & 1u) << g;  // bit (v mod 32) of w, inverted
-        }
-        discover(v, xs, discm, std::false_type{});
-        continue;
+      for (int g = 0; g < KX_GROUPS; ++g) {
+        const bool via_tag = (uint32_t)(v[g] - hub) < tag_span;
+        uint32_t r;
+        if (via_tag) r = (uint32_t)ld_cg_u8_hint(claim + claim_slot(P, v[g]), pol_status);
+        else r = ldg_status_u32(bm + (v[g] >> 5), pol_status);
+        needm |= (via_tag ? 0u : (~rotr32(r, v[g]) & 1u)) << g;
+        discm |= (via_tag ? (uint32_t)(r == 0u) : 0u) << g;
       }
-      const unsigned wneed = __reduce_or_sync(0xffffffffu, needm);
-      if (wneed) {  // warp-uniform skip
+    } else {
 #pragma unroll
-        for (int h = 0; h < KX_GROUPS; h += 4) {  // 4 tag loads in flight (register budget)
-          int cl[4];
-#pragma unroll
-          for (int g = 0; g < 4; ++g)
-            cl[g] = ((needm >> (h + g)) & 1u) ? ld_cg_u8(claim + claim_slot(P, v[h + g])) : 1;
-#pragma unroll
-          for (int g = 0; g < 4; ++g) discm |= (uint32_t)(cl[g] == 0) << (h + g);
-        }
+      for (int g = 0; g < KX_GROUPS; ++g) {
+        const uint32_t w = ldg_status_u32(bm + (v[g] >> 5), pol_status);
+        needm |= (~rotr32(w, v[g]) & 1u) << g;  // bit (v mod 32) of w, inverted
       }
-      discover(v, xs, discm, std::true_type{});
     }
+    const unsigned wneed = __reduce_or_sync(0xffffffffu, needm);
+    if (wneed) {  // warp-uniform skip
+#pragma unroll
+      for (int h = 0; h < KX_GROUPS; h += 4) {  // 4 tag loads in flight (register budget)
+        if (!((wneed >> h) & 15u)) continue;
+        int cl[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+          cl[g] = ((needm >> (h + g)) & 1u) ? ld_cg_u8(claim + claim_slot(P, v[h + g])) : 1;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) discm |= (uint32_t)(cl[g] == 0) << (h + g);
+      }
+    }
+    discover(v, wx, r0, r1, discm);
   };
-  if (c->probe_tags) run(std::true_type{});
-  else run(std::false_type{});
+
+  if (e_begin < e_end) {
+    int u0 = warp_search(fex, n_l, e_begin);  // Find-StartExpPoint (c)
+    for (;;) {
+      // ---- window: rows u0 .. u0+31, clipped to [e_begin, e_end), non-empty ones compacted
+      const int u = u0 + lane;
+      int fe = 0x7fffffff, rs = 0, x = 0;
+      if (u < n_l) {
+        fe = __ldg(fex + u);
+        rs = __ldg(frs + u);
+        x = __ldg(fx + u);
+      }
+      const int fe_last = __ldg(fex + min(u0 + 32, n_l));  // end of the window's last row
+      int fn = __shfl_down_sync(0xffffffffu, fe, 1);
+      if (lane == 31) fn = fe_last;
+      const int a = max(fe, e_begin), z = min(fn, e_end);
+      int cs = 0, ce = 0, cn = 0;
+      if (u < n_l && a < z) {
+        cs = rs + (a - fe);
+        ce = rs + (z - fe);
+        cn = ((ce + 3) >> 2) - (cs >> 2);
+      }
+      const unsigned nz = __ballot_sync(0xffffffffu, cn > 0);
+      const int nrow = __popc(nz);
+      const int src = lane < nrow ? (int)__fns(nz, 0, lane + 1) : 0;
+      const int wcs = __shfl_sync(0xffffffffu, cs, src);
+      const int wce = __shfl_sync(0xffffffffu, ce, src);
+      const int wx = __shfl_sync(0xffffffffu, x, src);
+      const int wn = lane < nrow ? __shfl_sync(0xffffffffu, cn, src) : 0;
+      const int winc = warp_incl_scan(wn);
+      const int nch = __shfl_sync(0xffffffffu, winc, 31);
+      const int wp = lane < nrow ? winc - wn : 0x7fffffff;  // first chunk of compacted row
+      // ---- rounds of 64 chunks (2 per lane)
+      for (int c0 = 0; c0 < nch; c0 += 64) {
+        int v[KX_GROUPS];
+        int rw[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int cb = c0 + 32 * h;
+          const unsigned m = __reduce_or_sync(0xffffffffu, shl1(wp - cb));  // rows starting
+          const int r0 = __popc(__ballot_sync(0xffffffffu, wp <= cb)) - 1;  // row of chunk cb
+          const int row = max(r0, 0) + __popc(m & le & ~1u);
+          rw[h] = row;
+          const int pj = __shfl_sync(0xffffffffu, wp, row);
+          const int csj = __shfl_sync(0xffffffffu, wcs, row);
+          const int cej = __shfl_sync(0xffffffffu, wce, row);
+          const int ci = cb + lane;
+          const int base = ((csj >> 2) + (ci - pj)) << 2;  // col index of the chunk
+          int4 q = make_int4(vs, vs, vs, vs);
+          if (ci < nch) {
+            if (vec && (long long)base + 4 <= col_cap) {
+              q = ldg_stream4(col + base, pol_stream);
+            } else {  // unaligned caller array / its last chunk: element loads in bounds
+              if (base + 0 >= csj && base + 0 < cej) q.x = ldg_stream(col + base + 0, pol_stream);
+              if (base + 1 >= csj && base + 1 < cej) q.y = ldg_stream(col + base + 1, pol_stream);
+              if (base + 2 >= csj && base + 2 < cej) q.z = ldg_stream(col + base + 2, pol_stream);
+              if (base + 3 >= csj && base + 3 < cej) q.w = ldg_stream(col + base + 3, pol_stream);
+            }
+          }
+          const bool in = ci < nch;
+          v[4 * h + 0] = (in && base + 0 >= csj && base + 0 < cej) ? q.x : vs;
+          v[4 * h + 1] = (in && base + 1 >= csj && base + 1 < cej) ? q.y : vs;
+          v[4 * h + 2] = (in && base + 2 >= csj && base + 2 < cej) ? q.z : vs;
+          v[4 * h + 3] = (in && base + 3 >= csj && base + 3 < cej) ? q.w : vs;
+        }
+        if (tag_mode) probe_round(v, wx, rw[0], rw[1], std::true_type{});
+        else probe_round(v, wx, rw[0], rw[1], std::false_type{});
+      }
+      if (fe_last >= e_end || u0 + 32 >= n_l) break;
+      u0 += 32;
+    }
+  }
   if (lane == 0) P.wcnt[b * KD_WARPS + warp] = wcount;
 }
 
