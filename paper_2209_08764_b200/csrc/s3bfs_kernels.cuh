@@ -659,6 +659,11 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   // Discovery of the flagged arcs (Fig1 L18-L22): one warp scan hands out the candidate slots
   // of the whole round, then each lane stores its own (plain stores, benign race).
   // wx = the window's caller ids; r0 / r1 = the window rows of the lane's two chunks
+#ifdef S3BFS_KX_CHECK
+  auto bad = [&](unsigned long long code, long long val) {
+    atomicCAS(&c->t_dbg[3], 0ull, (code << 56) | ((unsigned long long)val & 0xffffffffffffffull));
+  };
+#endif
   auto discover = [&](const int (&v)[KX_GROUPS], int wx, int r0, int r1, uint32_t discm) {
     if (!__any_sync(0xffffffffu, discm != 0u)) return;  // most rounds of heavy levels
     const int cnt = __popc(discm);
@@ -671,6 +676,10 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
     for (int g = 0; g < KX_GROUPS; ++g) {
       if ((discm >> g) & 1u) {
         const int par = g < 4 ? par0 : par1;
+#ifdef S3BFS_KX_CHECK
+        if (v[g] < 0 || v[g] >= P.n) { bad(1, v[g]); continue; }
+        if (slot < segbase || slot >= segbase + wcap) { bad(2, slot - segbase); continue; }
+#endif
         st_u8(claim + claim_slot(P, v[g]), tag);   // discovered (tag mode's visited test)
         st_weak_v2(lp + v[g], new_level, par);     // d[v] <- l, parent (Fig1 L18)
         st_weak(owner_of(vinfo, v[g]), slot);      // Owner[v] <- i (benign race)
@@ -754,7 +763,8 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
       const int wcs = __shfl_sync(0xffffffffu, cs, src);
       const int wce = __shfl_sync(0xffffffffu, ce, src);
       const int wx = __shfl_sync(0xffffffffu, x, src);
-      const int wn = lane < nrow ? __shfl_sync(0xffffffffu, cn, src) : 0;
+      const int cnv = __shfl_sync(0xffffffffu, cn, src);  // every lane shuffles
+      const int wn = lane < nrow ? cnv : 0;
       const int winc = warp_incl_scan(wn);
       const int nch = __shfl_sync(0xffffffffu, winc, 31);
       const int wp = lane < nrow ? winc - wn : 0x7fffffff;  // first chunk of compacted row
@@ -775,6 +785,10 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
           const int ci = cb + lane;
           const int base = ((csj >> 2) + (ci - pj)) << 2;  // col index of the chunk
           int4 q = make_int4(vs, vs, vs, vs);
+#ifdef S3BFS_KX_CHECK
+          if (ci < nch && (base < 0 || (long long)base >= col_cap)) bad(3, base);
+          if (row < 0 || row >= 32) bad(4, row);
+#endif
           if (ci < nch) {
             if (vec && (long long)base + 4 <= col_cap) {
               q = ldg_stream4(col + base, pol_stream);

@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/r2_gpu_tests.log 2>&1; rc=$?; echo "tests rc=$rc"; tail -5 gpurun_out/r2_gpu_tests.log
+python scripts/dbg_small.py variants/libs3bfs_check.so; timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/r2_gpu_tests.log 2>&1; rc=$?; echo "tests rc=$rc"; tail -5 gpurun_out/r2_gpu_tests.log
 [ $rc -eq 0 ] || exit 1
 L=paper_2209_08764_b200/libs3bfs.so
 R=variants/libs3bfs_r01.so
