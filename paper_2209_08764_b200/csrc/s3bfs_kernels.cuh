@@ -93,9 +93,6 @@ namespace s3bfs {
 #ifndef S3BFS_BU_P
 #define S3BFS_BU_P 2
 #endif
-#ifndef S3BFS_KC_GROUPS
-#define S3BFS_KC_GROUPS 4
-#endif
 #ifndef S3BFS_BU_TILES_PER_CTA
 #define S3BFS_BU_TILES_PER_CTA 4  // bottom-up: about this many tiles per resident CTA
 #endif
@@ -110,7 +107,8 @@ constexpr int KD_MIN_BLOCKS = S3BFS_KD_MINB;    // CTAs per SM the register budg
 constexpr int KD_WARPS = KD_THREADS / 32;
 constexpr int KD_SLACK = 64;                    // candidate-buffer slack per CTA
 constexpr int KX_GROUPS = S3BFS_KX_GROUPS;      // 32-edge groups per batch and warp
-constexpr int KC_GROUPS = S3BFS_KC_GROUPS;      // 32-candidate groups per k_compact round
+constexpr int KC_ITEMS = 4;                      // k_compact: candidates per thread and tile
+constexpr int KC_TILE = KD_THREADS * KC_ITEMS;   // k_compact: candidates per tile
 constexpr int KS_THREADS = 1024;                // k_small CTA size
 constexpr int KS_ECAP = 8192;                   // T0 maximum (edges per tier-0 level)
 constexpr int KS_NCAP = KS_ECAP;                // frontier capacity of tier 0 (kept <= e_l)
@@ -640,9 +638,11 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   const int hub = P.hub;                              // tag mode: ids < hub bitmap first
   const uint32_t tag_span = (uint32_t)(P.n - P.hub);  // tag mode: ids in [hub, n) tag only
 
-  if (tid == 0) {
-    P.status[b] = 0ull;  // reset k_compact's look-back word for this level
-    if (b == 0) c->t_kx_begin = globaltimer();
+  if (warp == 0) {  // reset k_compact's look-back words: at most one tile per KC_TILE arcs
+    const int mt = (c->e_hi - c->e_lo + KC_TILE - 1) / KC_TILE + 1;
+    const int z = (mt + p_l - 1) / p_l;
+    for (int t = b * z + lane; t < min((b + 1) * z, mt); t += 32) P.status[t] = 0ull;
+    if (b == 0 && lane == 0) c->t_kx_begin = globaltimer();
   }
   const int E0 = c->e_lo + b * chunk;
   const int E1 = min(E0 + chunk, c->e_hi);
@@ -839,123 +839,149 @@ __device__ __forceinline__ void bm_publish(uint32_t *bm, bool keep, int v, int l
 }
 
 // ---- (e)+(a)+(b): k_compact -------------------------------------------------------------------
-// CTA b handles the candidate segments its k_explore twin wrote (one per warp).
-// Pass 1 (Fig1 L20-L23): keep cand[k] iff Owner[cand[k]] == k (one 16-byte vertex-record
-// probe gives Owner, row start and degree); publish the kept vertex's visited bit and
-// compact (id, row start, degree) in place -- the degree is Fig1 L13 of the next level.
-// The next frontier holds caller ids (from the same record), the parents k_explore records.
-// A decoupled look-back over CTAs scans the (kept, degree-sum) pairs (Fig1 L24 and L14 of
-// the next level in one pass).  Pass 2 (Fig1 L25-L29): write the next frontier, its row
-// starts and its exclusive degree scan.  The last CTA to finish advances the control block
-// (Fig1 L9-L10, L15-L16).
+// The level's candidates sit in k_explore's per-warp segments (warp s = CTA b's warp w writes
+// cand[s * wcap + 0 .. wcnt[s])).  Every CTA first scans the wcnt[] array into shared memory
+// (one exclusive prefix over the level's P_l x 16 segments), which numbers the candidates
+// densely 0 .. C-1; tiles of KC_TILE consecutive candidate numbers are then taken in CTA start
+// order (an atomic tile counter), so the work is balanced however unevenly the discoveries
+// fell on k_explore's warps.  Per candidate (Fig1 L20-L23): slot k and vertex v = cand[k]; keep
+// iff Owner[v] == k (one 16-byte vertex-record probe also gives the row start, degree and
+// caller id); publish the kept vertex's visited bit.  A decoupled look-back over the tiles
+// scans the (kept, degree-sum) pairs (Fig1 L24, and L12-L15 of the next level in the same
+// pass), and each tile writes its kept vertices straight from registers into the next
+// frontier: caller ids, row starts, exclusive degree scan (Fig1 L25-L29).  The last CTA to
+// finish advances the control block (Fig1 L9-L10, L15-L16).
 __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P) {
   Ctl *c = P.ctl;
   if (c->tier != TIER_LARGE) return;
-  const int p_l = c->p_l;
+  extern __shared__ int32_t s_pre[];  // exclusive prefix of wcnt[0 .. nseg), then the total
   __shared__ int32_t s_k[KD_WARPS], s_d[KD_WARPS];
   __shared__ int s_last, s_tile;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // Surplus CTAs (blockIdx >= P_l) do no work but are still counted by the last-CTA
-  // election below: the control block is rewritten only after EVERY CTA of this launch has
-  // read it (a late-starting surplus CTA would otherwise see the next level's state).
-  const int nxt = c->cur ^ 1;
-  if ((int)blockIdx.x < p_l) {
-  if (tid == 0) s_tile = (int)atomicAdd(&c->tile_ctr, 1u);  // look-back order = start order
-  __syncthreads();
-  const int b = s_tile;  // this CTA handles tile b: the segments of k_explore's CTA b
-  const int4 *__restrict__ vinfo = P.vinfo;
-  int32_t *__restrict__ cand = P.cand;
-  int2 *__restrict__ crd = P.cand_rd;
-  const int seg = (b * KD_WARPS + warp) * c->wcap;
-  const int cnt = P.wcnt[b * KD_WARPS + warp];
+  const int p_l = c->p_l, wcap = c->wcap, nxt = c->cur ^ 1;
+  const int nseg = p_l * KD_WARPS;
   const bool dist = P.dist_size > 1;
-  if (b == 0 && tid == 0) c->t_kx_end = globaltimer();
-
-  int kept = 0, dsum = 0;
-  for (int k0 = 0; k0 < cnt; k0 += 32 * KC_GROUPS) {
-    int v[KC_GROUPS];
-#pragma unroll
-    for (int g = 0; g < KC_GROUPS; ++g) {
-      const int k = k0 + g * 32 + lane;
-      v[g] = (k < cnt) ? cand[seg + k] : -1;
-    }
-    int4 vi[KC_GROUPS];  // {row start, degree, caller id, Owner}: one sector per candidate
-#pragma unroll
-    for (int g = 0; g < KC_GROUPS; ++g)
-      vi[g] = (v[g] >= 0) ? __ldg(vinfo + v[g]) : make_int4(0, 0, 0, -1);
-#pragma unroll
-    for (int g = 0; g < KC_GROUPS; ++g) {
-      const int k = k0 + g * 32 + lane;
-      const bool keep = v[g] >= 0 && vi[g].w == seg + k;  // Fig1 L22: "if Owner[v] = i"
-      const int d = keep ? vi[g].y : 0;
-      bm_publish(P.bm, keep, v[g], lane);  // exact visited bit (R17)
-      const unsigned m = __ballot_sync(0xffffffffu, keep);
-      if (keep) {
-        const int q = seg + kept + __popc(m & lanemask_lt());
-        cand[q] = dist ? v[g] : vi[g].z;  // NEXT-4 keeps the internal id for the record
-        crd[q] = make_int2(vi[g].x, d);
+  if (blockIdx.x == 0 && tid == 0) c->t_kx_end = globaltimer();
+  // ---- the dense numbering: exclusive scan of the segment counts (blocked, ipt per thread)
+  {
+    const int ipt = (nseg + KD_THREADS - 1) / KD_THREADS;
+    const int s0 = tid * ipt;
+    int sum = 0;
+    for (int i = 0; i < ipt; ++i) sum += (s0 + i < nseg) ? __ldcg(P.wcnt + s0 + i) : 0;
+    const int inc = warp_incl_scan(sum);
+    if (lane == 31) s_k[warp] = inc;
+    __syncthreads();
+    const int wt = lane < KD_WARPS ? s_k[lane] : 0;
+    const int wi = warp_incl_scan(wt);
+    int run = __shfl_sync(0xffffffffu, wi - wt, warp) + inc - sum;
+    for (int i = 0; i < ipt; ++i) {
+      if (s0 + i < nseg) {
+        s_pre[s0 + i] = run;
+        run += __ldcg(P.wcnt + s0 + i);
       }
-      kept += __popc(m);
-      dsum += d;
     }
+    const int tot = __shfl_sync(0xffffffffu, wi, 31);  // lanes >= KD_WARPS add nothing
+    if (tid == 0) s_pre[nseg] = tot;
+    __syncthreads();
   }
-  dsum = warp_sum(dsum);
-  if (lane == 0) { s_k[warp] = kept; s_d[warp] = dsum; }
-  if (P.collect_stats) {
-    const int tot = warp_sum(lane == 0 ? cnt : 0);
-    if (lane == 0 && tot) atomicAdd(&c->cand_acc, tot);  // statistics only
-  }
-  __syncthreads();
-  if (warp == 0) {
-    const int kk = lane < KD_WARPS ? s_k[lane] : 0;
-    const int dd = lane < KD_WARPS ? s_d[lane] : 0;
-    const int ik = warp_incl_scan(kk), id = warp_incl_scan(dd);
-    const Pair agg{(uint32_t)__shfl_sync(0xffffffffu, ik, 31),
-                   (uint32_t)__shfl_sync(0xffffffffu, id, 31)};
-    const Pair ex = lookback<true>(P.status, b, agg);
-    if (lane < KD_WARPS) {
-      s_k[lane] = (int)ex.a + ik - kk;
-      s_d[lane] = (int)ex.b + id - dd;
-    }
-    if (b == p_l - 1 && lane == 0) {  // the level's totals: n_{l+1}, e_{l+1} (Fig1 L15)
-      const int n_next = (int)(ex.a + agg.a), e_next = (int)(ex.b + agg.b);
-      c->n_next = n_next;
-      c->e_next = e_next;
-      if (!dist) P.fex[nxt][n_next] = e_next;
-    }
-  }
-  __syncthreads();
-  int koff = s_k[warp], doff = s_d[warp];
+  const int total = s_pre[nseg];
+  const int ntiles = (total + KC_TILE - 1) / KC_TILE;
+  if (P.collect_stats && blockIdx.x == 0 && tid == 0) c->cand_acc = total;  // statistics only
+  const int4 *__restrict__ vinfo = P.vinfo;
+  const int32_t *__restrict__ cand = P.cand;
   int32_t *__restrict__ fn = P.f[nxt];
   int32_t *__restrict__ frsn = P.frs[nxt];
   int32_t *__restrict__ fexn = P.fex[nxt];
-  for (int k0 = 0; k0 < kept; k0 += 32) {
-    const int k = k0 + lane;
-    int v = 0, r0 = 0, d = 0;
-    if (k < kept) {
-      v = cand[seg + k];
-      const int2 rd = crd[seg + k];
-      r0 = rd.x;
-      d = rd.y;
-    }
-    const int inc = warp_incl_scan(d);
-    if (k < kept) {
-      if (dist) {  // NEXT-4: this rank's kept vertex, for the cross-rank merge
-        P.rec[koff + k] = make_int4(v, P.lp[v].y, r0, d);
-      } else {
-        fn[koff + k] = v;
-        frsn[koff + k] = r0;
-        fexn[koff + k] = doff + inc - d;
+  for (;;) {
+    if (tid == 0) s_tile = (int)atomicAdd(&c->tile_ctr, 1u);  // look-back order = start order
+    __syncthreads();
+    const int t = s_tile;
+    if (t >= ntiles) break;
+    // ---- pass over the tile's candidates: item k of thread tid = number t*KC_TILE + k*512 + tid
+    int v[KC_ITEMS], sl[KC_ITEMS];
+#pragma unroll
+    for (int k = 0; k < KC_ITEMS; ++k) {
+      const int i = t * KC_TILE + k * KD_THREADS + tid;
+      v[k] = -1;
+      sl[k] = -1;
+      if (i < total) {
+        int lo = 0, hi = nseg;  // the segment holding number i: last s with s_pre[s] <= i
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (s_pre[mid] <= i) lo = mid; else hi = mid;
+        }
+        sl[k] = lo * wcap + (i - s_pre[lo]);
       }
     }
-    doff += __shfl_sync(0xffffffffu, inc, 31);
+#pragma unroll
+    for (int k = 0; k < KC_ITEMS; ++k) v[k] = sl[k] >= 0 ? __ldcg(cand + sl[k]) : -1;
+    int4 vi[KC_ITEMS];  // {row start, degree, caller id, Owner}: one sector per candidate
+#pragma unroll
+    for (int k = 0; k < KC_ITEMS; ++k)
+      vi[k] = v[k] >= 0 ? __ldg(vinfo + v[k]) : make_int4(0, 0, 0, -1);
+    unsigned km[KC_ITEMS];
+    int kept = 0, dsum = 0;
+#pragma unroll
+    for (int k = 0; k < KC_ITEMS; ++k) {
+      const bool keep = v[k] >= 0 && vi[k].w == sl[k];  // Fig1 L22: "if Owner[v] = i"
+      bm_publish(P.bm, keep, v[k], lane);               // exact visited bit (R17)
+      km[k] = __ballot_sync(0xffffffffu, keep);
+      kept += __popc(km[k]);
+      dsum += keep ? vi[k].y : 0;
+    }
+    dsum = warp_sum(dsum);
+    if (lane == 0) { s_k[warp] = kept; s_d[warp] = dsum; }
+    __syncthreads();
+    if (warp == 0) {
+      const int kk = lane < KD_WARPS ? s_k[lane] : 0;
+      const int dd = lane < KD_WARPS ? s_d[lane] : 0;
+      const int ik = warp_incl_scan(kk), id = warp_incl_scan(dd);
+      const Pair agg{(uint32_t)__shfl_sync(0xffffffffu, ik, 31),
+                     (uint32_t)__shfl_sync(0xffffffffu, id, 31)};
+      const Pair ex = lookback<true>(P.status, t, agg);
+      if (lane < KD_WARPS) {
+        s_k[lane] = (int)ex.a + ik - kk;
+        s_d[lane] = (int)ex.b + id - dd;
+      }
+      if (t == ntiles - 1 && lane == 0) {  // the level's totals: n_{l+1}, e_{l+1} (Fig1 L15)
+        const int n_next = (int)(ex.a + agg.a), e_next = (int)(ex.b + agg.b);
+        c->n_next = n_next;
+        c->e_next = e_next;
+        if (!dist) P.fex[nxt][n_next] = e_next;
+      }
+    }
+    __syncthreads();
+    // ---- the tile's kept vertices into the next frontier, in (warp, item, lane) order
+    int koff = s_k[warp], doff = s_d[warp];
+#pragma unroll
+    for (int k = 0; k < KC_ITEMS; ++k) {
+      const bool keep = (km[k] >> lane) & 1u;
+      const int d = keep ? vi[k].y : 0;
+      const int inc = warp_incl_scan(d);
+      if (keep) {
+        const int pos = koff + __popc(km[k] & lanemask_lt());
+        if (dist) {  // NEXT-4: this rank's kept vertex, for the cross-rank merge
+          P.rec[pos] = make_int4(v[k], P.lp[v[k]].y, vi[k].x, d);
+        } else {
+          fn[pos] = vi[k].z;     // caller id (the parent the next level records)
+          frsn[pos] = vi[k].x;   // internal row start
+          fexn[pos] = doff + inc - d;
+        }
+      }
+      koff += __popc(km[k]);
+      doff += __shfl_sync(0xffffffffu, inc, 31);
+    }
   }
-  }  // active CTA
   // last-CTA election over the whole grid (one atomic per CTA; not the discovery path, R17)
   __threadfence();
   __syncthreads();
   if (tid == 0) s_last = atomicAdd(&c->done_ctr, 1u) == gridDim.x - 1;
   __syncthreads();
+  if (s_last && tid == 0 && ntiles == 0) {  // no candidates: an empty next frontier
+    c->n_next = 0;
+    c->e_next = 0;
+    if (!dist) P.fex[nxt][0] = 0;
+  }
   if (s_last && tid == 0 && P.dist_size > 1) {
     // NEXT-4: the local kept count stays in n_next; the merge advances the level
     c->done_ctr = 0;
