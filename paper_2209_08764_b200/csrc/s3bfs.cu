@@ -57,7 +57,7 @@ struct s3bfs_ctx {
   const int32_t *ro_int = nullptr;  // row offsets of the internal CSR
   size_t ws_bytes = 0;
   int64_t cand_cap = 0;
-  size_t ks_smem = 0, kc_smem = 0, kc_pre_smem = 0;
+  size_t ks_smem = 0, kc_smem = 0;
   int loop_graph = 1;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -335,7 +335,7 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
         r = add((void *)k_cluster, KC_CL, KC_THREADS, h->kc_smem);
       } else if (k == 'T') {
         r = add((void *)k_explore, h->P.p_max, KD_THREADS, 0);
-        if (r == S3BFS_OK) r = add((void *)k_compact, h->P.p_max, KD_THREADS, h->kc_pre_smem);
+        if (r == S3BFS_OK) r = add((void *)k_compact, h->P.p_max, KD_THREADS, 0);
       } else {  // 'B'
         r = add((void *)k_fb_clear, h->num_sms * 4, 256, 0);
         if (r == S3BFS_OK) r = add((void *)k_fb_set, h->num_sms * 4, 256, 0);
@@ -469,17 +469,12 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   int occ_x = 0, occ_c = 0;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_x, k_explore, KD_THREADS, 0)) != cudaSuccess)
     return bail(cuda_fail(h, e, "occupancy(k_explore)"));
-  // k_compact's dynamic shared memory holds the prefix of P_l x 16 segment counts; sized here
-  // for an upper bound of P_max (4 CTAs per SM), then exactly below
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-           &occ_c, k_compact, KD_THREADS, ((size_t)h->num_sms * 4 * KD_WARPS + 1) * 4)) != cudaSuccess)
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, k_compact, KD_THREADS, 0)) != cudaSuccess)
     return bail(cuda_fail(h, e, "occupancy(k_compact)"));
   int occ = occ_x < occ_c ? occ_x : occ_c;
   if (occ < 1) occ = 1;
-  if (occ > 4) occ = 4;
   int p_max = h->num_sms * occ;  // every CTA resident: the look-back never waits on a CTA
   if (h->opt.max_ctas > 0 && h->opt.max_ctas < p_max) p_max = h->opt.max_ctas;
-  h->kc_pre_smem = ((size_t)p_max * KD_WARPS + 1) * 4;
   const int grain = h->opt.edges_per_cta > 0 ? h->opt.edges_per_cta : 2048;
   // cluster tier: T0 < e_l <= tc_max (one 8-CTA cluster); tier 0 keeps the small levels
   int tc_max = h->opt.cluster_max_edges == 0 ? KC_CL * KC_ECTA : h->opt.cluster_max_edges;
@@ -518,7 +513,8 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   const size_t o_cand = take((size_t)h->cand_cap * 4);
   const size_t o_crd = take((size_t)h->cand_cap * 8);
   const size_t bm_bytes = ((size_t)n + 127) / 128 * 16;  // 16 B padded (vector clears)
-  const size_t o_bm = take(bm_bytes + 16);  // + the sentinel block (Params::v_sent)
+  // status pairs {visited word, claim word} per 32 ids + 2 sentinel blocks (Params::v_sent)
+  const size_t o_bm = take(2 * bm_bytes + 32);
   // claim slots: a power of two >= max(n, a floor) (claim_slot's hash is mod 2^k); the floor
   // spreads a small graph's tags over more L2 lines (fewer same-line probes and stores)
   size_t claim_n = 16;
@@ -526,8 +522,7 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   const size_t o_claim = take(claim_n);
   const size_t o_fb0 = take(bm_bytes), o_fb1 = take(bm_bytes);
   const size_t o_wcnt = take((size_t)p_max * KD_WARPS * 4);
-  // look-back words: k_compact's tiles (<= candidates / KC_TILE + 1) and k_explore's CTAs
-  const size_t o_status = take(((size_t)(h->cand_cap / KC_TILE) + 2 + (size_t)p_max) * 8);
+  const size_t o_status = take((size_t)p_max * 8);
   // NEXT-3 bottom-up tiles: width = the power of two >= words / (tiles-per-CTA x P_max), at
   // least 64 words (one BU_W-word round for each of a CTA's 16 warps)
   const long long bu_words = (((long long)n + 127) >> 7) << 2;
@@ -779,7 +774,7 @@ s3bfs_status s3bfs_run(s3bfs_handle h, int32_t source, int32_t *level, int32_t *
     } else {
       k_explore<<<c.p_l, KD_THREADS, 0, stream>>>(h->P);
       if (h->time_kernels) CK(h, cudaEventRecord(h->ev[1], stream));
-      k_compact<<<h->P.p_max, KD_THREADS, h->kc_pre_smem, stream>>>(h->P);
+      k_compact<<<c.p_l, KD_THREADS, 0, stream>>>(h->P);
       if (h->time_kernels) CK(h, cudaEventRecord(h->ev[2], stream));
     }
     CK(h, cudaGetLastError());
@@ -818,7 +813,7 @@ s3bfs_status s3bfs_dist_expand(s3bfs_handle h, s3bfs_stream_t stream_, int32_t *
   *done = c.tier == TIER_DONE ? 1 : 0;
   if (*done) return S3BFS_OK;
   k_explore<<<c.p_l, KD_THREADS, 0, stream>>>(h->P);
-  k_compact<<<h->P.p_max, KD_THREADS, h->kc_pre_smem, stream>>>(h->P);
+  k_compact<<<c.p_l, KD_THREADS, 0, stream>>>(h->P);
   CK(h, cudaGetLastError());
   CK(h, cudaMemcpyAsync(h->h_ctl, h->P.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, stream));
   CK(h, cudaStreamSynchronize(stream));

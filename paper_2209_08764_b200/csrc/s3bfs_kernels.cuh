@@ -107,8 +107,7 @@ constexpr int KD_MIN_BLOCKS = S3BFS_KD_MINB;    // CTAs per SM the register budg
 constexpr int KD_WARPS = KD_THREADS / 32;
 constexpr int KD_SLACK = 64;                    // candidate-buffer slack per CTA
 constexpr int KX_GROUPS = S3BFS_KX_GROUPS;      // 32-edge groups per batch and warp
-constexpr int KC_ITEMS = 4;                      // k_compact: candidates per thread and tile
-constexpr int KC_TILE = KD_THREADS * KC_ITEMS;   // k_compact: candidates per tile
+constexpr int KC_GROUPS = 4;                     // 32-candidate groups per k_compact round
 constexpr int KS_THREADS = 1024;                // k_small CTA size
 constexpr int KS_ECAP = 8192;                   // T0 maximum (edges per tier-0 level)
 constexpr int KS_NCAP = KS_ECAP;                // frontier capacity of tier 0 (kept <= e_l)
@@ -174,7 +173,9 @@ struct Params {
                                     // discoveries), internal row starts, degree scan
   int32_t *cand;                // candidate per slot (k_explore), compacted by k_compact
   int2 *cand_rd;                // (row start, degree) of kept candidates, pass 1 -> pass 2
-  uint32_t *bm;                 // visited bitmap: bit set => visited (exact at level start),
+  uint32_t *bm;                 // status pairs, one per 32 internal ids: word 2w = visited
+                                //  bits of ids 32w..32w+31 (bit set => visited, exact at level
+                                //  start), word 2w+1 = the level's claim bits (k_explore);
                                 //  plus one always-set 16 B sentinel block after the padded end
   unsigned long long pol_first, pol_last;  // L2 createpolicy descriptors (evict-first for the
                                 //  col stream, evict-last for the bitmap), made once at create:
@@ -548,10 +549,12 @@ __global__ void k_init(Params P, int32_t s, int32_t *level, int32_t *parent) {
   const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long gstride = (long long)gridDim.x * blockDim.x;
   const int si = P.o2n ? __ldg(P.o2n + s) : s;  // the source's internal id
-  const long long nw4 = ((long long)n + 127) >> 7;  // bitmap as uint4 (16 B padded)
-  for (long long i = gtid; i <= nw4; i += gstride) {  // block nw4: the all-ones sentinel
-    uint4 w = i == nw4 ? make_uint4(~0u, ~0u, ~0u, ~0u) : make_uint4(0, 0, 0, 0);
-    if (i == (si >> 7)) (&w.x)[(si >> 5) & 3] = 1u << (si & 31);
+  // status pairs as uint4 (two pairs = 64 ids each, padded to 128 ids); the 2 blocks after
+  // the padded end are the all-ones sentinel (Params::v_sent)
+  const long long nw4 = (((long long)n + 127) >> 7) * 2;
+  for (long long i = gtid; i < nw4 + 2; i += gstride) {
+    uint4 w = i >= nw4 ? make_uint4(~0u, ~0u, ~0u, ~0u) : make_uint4(0, 0, 0, 0);
+    if (i == (si >> 6)) (&w.x)[((si >> 5) & 1) * 2] = 1u << (si & 31);
     reinterpret_cast<uint4 *>(P.bm)[i] = w;
   }
   const long long nc = ((long long)P.claim_mask + 16) >> 4;  // claim tags <- 0 (all slots),
@@ -598,22 +601,19 @@ __global__ void k_policies(unsigned long long *out) {
 // CTA b < P_l owns global edges [b*chunk, min((b+1)*chunk, e_l)) of the level, split evenly
 // over its warps: each warp is one of the paper's workers with an (almost) equal share of the
 // level's edges (Fig1 L16-L17).  A warp finds its start vertex with the 32-ary search
-// (c), then streams its edges (Fig1 L18) through a register window of 32 consecutive frontier
-// rows.
-// Streaming unit = an aligned 16-byte col chunk (4 arcs): each window row's slice of the
-// warp's edge range covers [cs, ce) of col, i.e. chunks cs/4 .. (ce-1)/4; the window's rows
-// with a non-empty slice are compacted to the front lanes, and an exclusive scan of their chunk
-// counts numbers the window's chunks.  A round gives every lane 2 chunks (one 16-byte load
-// each, 8 arcs; 256 arcs per warp): lane i's chunk c belongs to the row whose first chunk is
-// the last one <= c -- one REDUX of the rows' first-chunk bits per 32 chunks, then a popc (the
-// compacted rows start at strictly increasing chunks, so the rank is exact).  The first and
-// last chunk of a row mask the elements outside [cs, ce) (they belong to other rows).  No
-// shared memory and no CTA barrier, so warps progress independently.
-// Visited test (the paper's "d[v] = infinity", R1): see run() below.  Discovery
-// (EXPLORE-VERTEX): tag[v] = tag (tag mode), {d, parent}[v] = {l+1, x}, Owner[v] = slot,
-// cand[slot] = v -- plain stores, the paper's benign race, no atomics.  Racing discoverers
-// store the same d and a valid parent and enqueue duplicates; the Owner check keeps exactly
-// one (R4).
+// (c), then walks its edges in batches of KX_GROUPS groups of 32 -- lane i takes edge e+i, so
+// a group reads 32 consecutive col entries (coalesced streaming, Fig1 L18).  Edge -> frontier
+// vertex mapping uses a register window of 32 consecutive frontier vertices (their
+// degree-scan entries, ids and row starts): one warp-uniform shuffle search per batch, and a
+// per-lane search only when the batch spans several rows.  No shared memory, no CTA barrier,
+// so warps progress independently.
+// Visited test (the paper's "d[v] = infinity", R1): the visited bitmap (exact at level start,
+// read-only here) and, for a clear bit, the vertex's 1-byte claim tag, which equals this
+// level's tag once some worker discovered v in this level.
+// Discovery (EXPLORE-VERTEX): claim[v] = tag, {d, parent}[v] = {l+1, x}, Owner[v] =
+// slot, cand[slot] = v -- plain stores, the paper's benign race, no atomics.  Racing
+// discoverers that all saw an old tag store the same d and a valid parent and enqueue
+// duplicates; the Owner check keeps exactly one (R4).
 __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P) {
   Ctl *c = P.ctl;
   if (c->tier != TIER_LARGE) return;
@@ -624,7 +624,6 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   const int n_l = c->n_l, chunk = c->chunk, cur = c->cur, wcap = c->wcap;
   const int new_level = c->level + 1;     // Fig1 L10: discoveries get l+1 (R11)
   const int tag = 1 + (c->level % 255);   // never 0, the per-run initial value
-  const bool tag_mode = c->probe_tags != 0;
   const int32_t *__restrict__ fx = P.f[cur];
   const int32_t *__restrict__ frs = P.frs[cur];
   const int32_t *__restrict__ fex = P.fex[cur];
@@ -634,15 +633,13 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   int32_t *__restrict__ cand = P.cand;
   const uint32_t *__restrict__ bm = P.bm;
   uint8_t *__restrict__ claim = P.claim;
-  const int vs = P.v_sent;  // masked elements' target: its visited bit is always set
-  const int hub = P.hub;                              // tag mode: ids < hub bitmap first
-  const uint32_t tag_span = (uint32_t)(P.n - P.hub);  // tag mode: ids in [hub, n) tag only
+  const int vs = P.v_sent;  // masked lanes' target: its visited bit is always set
+  const int hub = P.hub;                              // ids < hub: bitmap first
+  const uint32_t tag_span = (uint32_t)(P.n - P.hub);  // ids in [hub, n): tag only
 
-  if (warp == 0) {  // reset k_compact's look-back words: at most one tile per KC_TILE arcs
-    const int mt = (c->e_hi - c->e_lo + KC_TILE - 1) / KC_TILE + 1;
-    const int z = (mt + p_l - 1) / p_l;
-    for (int t = b * z + lane; t < min((b + 1) * z, mt); t += 32) P.status[t] = 0ull;
-    if (b == 0 && lane == 0) c->t_kx_begin = globaltimer();
+  if (tid == 0) {
+    P.status[b] = 0ull;  // reset k_compact's look-back word for this level
+    if (b == 0) c->t_kx_begin = globaltimer();
   }
   const int E0 = c->e_lo + b * chunk;
   const int E1 = min(E0 + chunk, c->e_hi);
@@ -651,167 +648,200 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   const int segbase = (b * KD_WARPS + warp) * wcap;
   const unsigned long long pol_stream = P.pol_first;
   const unsigned long long pol_status = P.pol_last;
-  const unsigned le = 0xffffffffu >> (31 - lane);  // bits 0 .. lane
-  const bool vec = P.col_vec != 0;
-  const long long col_cap = P.col_cap;             // readable col elements (>= nnz)
   int wcount = 0;
-
-  // Discovery of the flagged arcs (Fig1 L18-L22): one warp scan hands out the candidate slots
-  // of the whole round, then each lane stores its own (plain stores, benign race).
-  // wx = the window's caller ids; r0 / r1 = the window rows of the lane's two chunks
-#ifdef S3BFS_KX_CHECK
-  auto bad = [&](unsigned long long code, long long val) {
-    atomicCAS(&c->t_dbg[3], 0ull, (code << 56) | ((unsigned long long)val & 0xffffffffffffffull));
+  int u0 = 0, wex = 0, wx = 0, wb = 0, lim = 0;
+  bool wzero = false;  // the window holds an empty row (two equal row starts)
+  auto load_window = [&](int base) {
+    const int u = base + lane;
+    wex = (u < n_l) ? __ldg(fex + u) : 0x7fffffff;
+    wx = (u < n_l) ? __ldg(fx + u) : 0;
+    wb = (u < n_l) ? __ldg(frs + u) - wex : 0;
+    lim = __ldg(fex + min(base + 32, n_l));
+    const int down = __shfl_down_sync(0xffffffffu, wex, 1);  // all lanes shuffle
+    const int nxt_start = (lane < 31) ? down : lim;
+    wzero = __any_sync(0xffffffffu, u < n_l && nxt_start == wex);
   };
-#endif
-  auto discover = [&](const int (&v)[KX_GROUPS], int wx, int r0, int r1, uint32_t discm) {
-    if (!__any_sync(0xffffffffu, discm != 0u)) return;  // most rounds of heavy levels
-    const int cnt = __popc(discm);
-    const int inc = warp_incl_scan(cnt);
-    int slot = segbase + wcount + inc - cnt;
-    wcount += __shfl_sync(0xffffffffu, inc, 31);
-    const int par0 = __shfl_sync(0xffffffffu, wx, r0);  // parents: the chunks' frontier
-    const int par1 = __shfl_sync(0xffffffffu, wx, r1);  // vertices (caller ids)
-#pragma unroll
-    for (int g = 0; g < KX_GROUPS; ++g) {
-      if ((discm >> g) & 1u) {
-        const int par = g < 4 ? par0 : par1;
-#ifdef S3BFS_KX_CHECK
-        if (v[g] < 0 || v[g] >= P.n) { bad(1, v[g]); continue; }
-        if (slot < segbase || slot >= segbase + wcap) { bad(2, slot - segbase); continue; }
-#endif
-        st_u8(claim + claim_slot(P, v[g]), tag);   // discovered (tag mode's visited test)
-        st_weak_v2(lp + v[g], new_level, par);     // d[v] <- l, parent (Fig1 L18)
-        st_weak(owner_of(vinfo, v[g]), slot);      // Owner[v] <- i (benign race)
-        cand[slot] = v[g];                         // Q[i].Enqueue(v)
-        ++slot;
-      }
+  if (e_begin < e_end) {
+    u0 = warp_search(fex, n_l, e_begin);  // Find-StartExpPoint (c)
+    load_window(u0);
+  }
+  // Map the batch of edges [e, e_next) onto lanes and load their targets: v[g] = col entry of
+  // edge e + 32g + lane (-1 outside the batch), byte g of xs = its frontier vertex's window slot
+  // (the caller id is shuffled only on discovery).
+  auto map_load = [&](int e, int (&v)[KX_GROUPS], uint32_t (&xs)[KX_GROUPS / 4]) -> int {
+    while (lim <= e) {  // window exhausted (also skips runs of zero-degree vertices, C9)
+      u0 += 32;
+      load_window(u0);
     }
-  };
-
-  // The level's visited test (Fig1 L18 "if d[v] = infinity"), chosen per level by
-  // decide_tier from the share of arcs that end at visited vertices:
-  //  tag mode (most targets new, the discovery-heavy levels): a hub id (< P.hub) reads its
-  //    visited bit (exact at level start; hub words L1-resident) and, if clear, its discovery
-  //    tag; any other id reads only its tag (nonzero once discovered, in this or an earlier
-  //    level) -- one probe instead of two for the arcs that reach new vertices;
-  //  bitmap mode (most targets visited, the heavy levels): the visited bit, then the tag of
-  //    the few clear ones (round 1's test; a discoverer stores the tag, so a vertex reached by
-  //    several frontier arcs in this level is enqueued about once).
-  // Masked elements probe the sentinel (its bit is always set), so the tests are branch-free.
-  auto probe_round = [&](int (&v)[KX_GROUPS], int wx, int r0, int r1, auto tmode) {
-    constexpr bool TAGS = decltype(tmode)::value;
-    uint32_t needm = 0;  // targets whose discovery tag decides (bit clear at level start)
-    uint32_t discm = 0;  // targets found undiscovered: candidates (Fig1 L19-L22)
-    if constexpr (TAGS) {
+    const int bend = min(e_end, lim);
+    // window slot of the batch's first edge (warp-uniform): the window's row starts are
+    // non-decreasing and wex_0 <= e, so it is the count of row starts <= e, minus one
+    const int j0 = __popc(__ballot_sync(0xffffffffu, wex <= e)) - 1;
+    const int row_end = (j0 < 31) ? __shfl_sync(0xffffffffu, wex, min(j0 + 1, 31)) : lim;
+    int e_next = min(e + KX_GROUPS * 32, bend);
+    if (S3BFS_KX_FAST && row_end >= e_next) {
+      // the whole batch lies in one frontier row (most R-MAT arcs): uniform x and base
+      const int x = j0;
+      const int base = __shfl_sync(0xffffffffu, wb, j0);
+      const int start = base + e;  // col index of the batch's first edge
+      const int a0 = start & ~3;   // 16-byte aligned
+#pragma unroll
+      for (int k = 0; k < KX_GROUPS / 4; ++k) xs[k] = (uint32_t)x * 0x01010101u;
+      if (S3BFS_KX_VEC && P.col_vec && (long long)a0 + KX_GROUPS * 32 <= P.nnz) {
+        // vectorised streaming: lane i loads 16 B at a0 + 4*(i + 32k), i.e. each warp
+        // instruction fetches 512 contiguous bytes of the row; edges outside
+        // [start, row/slice end) are masked.  Next batch starts 16-byte aligned.
+        const int lim_idx = base + bend;
+        if (a0 == start && a0 + KX_GROUPS * 32 <= lim_idx) {
+          // interior batch (aligned, whole): no masking
+#pragma unroll
+          for (int k = 0; k < KX_GROUPS / 4; ++k) {
+            const int4 q = ldg_stream4(col + a0 + 4 * (lane + 32 * k), pol_stream);
+            v[4 * k + 0] = q.x;
+            v[4 * k + 1] = q.y;
+            v[4 * k + 2] = q.z;
+            v[4 * k + 3] = q.w;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < KX_GROUPS / 4; ++k) {
+            const int i0 = a0 + 4 * (lane + 32 * k);
+            const int4 q = ldg_stream4(col + i0, pol_stream);  // in bounds: a0 + 256 <= nnz
+            v[4 * k + 0] = (i0 + 0 >= start && i0 + 0 < lim_idx) ? q.x : vs;
+            v[4 * k + 1] = (i0 + 1 >= start && i0 + 1 < lim_idx) ? q.y : vs;
+            v[4 * k + 2] = (i0 + 2 >= start && i0 + 2 < lim_idx) ? q.z : vs;
+            v[4 * k + 3] = (i0 + 3 >= start && i0 + 3 < lim_idx) ? q.w : vs;
+          }
+        }
+        e_next = min(bend, a0 + KX_GROUPS * 32 - base);
+      } else {
+#pragma unroll
+        for (int g = 0; g < KX_GROUPS; ++g) {  // masked lanes re-load the batch's first edge
+          const int my_e = e + g * 32 + lane;
+          const int t = ldg_stream(col + base + (my_e < bend ? my_e : e), pol_stream);
+          v[g] = (my_e < bend) ? t : vs;
+        }
+      }
+    } else if (S3BFS_KX_RANK && !wzero) {
+      // several rows in the batch: rank mapping.  Window lane j's row starts at edge wex_j;
+      // for group g (edges eg .. eg+31) the row starts strictly inside the group form a
+      // 32-bit mask (one REDUX), and lane i's row is the group's first row plus the number
+      // of row starts at or below edge eg+i (exact while no row of the window is empty)
+      // (row starts in [eg, eg+31] -> mask bit rel; r = row of edge eg-1, so lane i's row is
+      // r + popc(mask & bits 0..i); the batch's first edge lies in row j0)
+      const unsigned le = 0xffffffffu >> (31 - lane);  // bits 0 .. lane
+      const int pfirst = __shfl_sync(0xffffffffu, wb, j0) + e;  // col index of edge e (valid)
+      const int lb = bend - e - lane;  // group g's lane is inside the batch iff 32 g < lb
+      int r = j0;
 #pragma unroll
       for (int g = 0; g < KX_GROUPS; ++g) {
-        const bool via_tag = (uint32_t)(v[g] - hub) < tag_span;
-        uint32_t r;
-        if (via_tag) r = (uint32_t)ld_cg_u8_hint(claim + claim_slot(P, v[g]), pol_status);
-        else r = ldg_status_u32(bm + (v[g] >> 5), pol_status);
-        needm |= (via_tag ? 0u : (~rotr32(r, v[g]) & 1u)) << g;
-        discm |= (via_tag ? (uint32_t)(r == 0u) : 0u) << g;
+        const int eg = e + g * 32;
+        const int rel = wex - eg;  // this window lane's row start relative to the group
+        const unsigned m = __reduce_or_sync(0xffffffffu, shl1(rel));  // starts in [eg, eg+31]
+        if (g == 0) r -= (int)(m & 1u);  // a row starting exactly at e is row j0 itself
+        const int j = r + __popc(m & le);
+        xs[g >> 2] |= (uint32_t)j << (8 * (g & 3));
+        const int pos = __shfl_sync(0xffffffffu, wb, j) + eg + lane;
+        const bool ok = g * 32 < lb;
+        const int t = ldg_stream(col + (ok ? pos : pfirst), pol_stream);  // unconditional
+        v[g] = ok ? t : vs;
+        r += __popc(m);
       }
     } else {
 #pragma unroll
       for (int g = 0; g < KX_GROUPS; ++g) {
-        const uint32_t w = ldg_status_u32(bm + (v[g] >> 5), pol_status);
-        needm |= (~rotr32(w, v[g]) & 1u) << g;  // bit (v mod 32) of w, inverted
-      }
-    }
-    const unsigned wneed = __reduce_or_sync(0xffffffffu, needm);
-    if (wneed) {  // warp-uniform skip
+        const int my_e = e + g * 32 + lane;
+        int j = j0;  // largest window slot with excl <= my_e (>= j0)
 #pragma unroll
-      for (int h = 0; h < KX_GROUPS; h += 4) {  // 4 tag loads in flight (register budget)
-        if (!((wneed >> h) & 15u)) continue;
-        int cl[4];
-#pragma unroll
-        for (int g = 0; g < 4; ++g)
-          cl[g] = ((needm >> (h + g)) & 1u) ? ld_cg_u8(claim + claim_slot(P, v[h + g])) : 1;
-#pragma unroll
-        for (int g = 0; g < 4; ++g) discm |= (uint32_t)(cl[g] == 0) << (h + g);
-      }
-    }
-    discover(v, wx, r0, r1, discm);
-  };
-
-  if (e_begin < e_end) {
-    int u0 = warp_search(fex, n_l, e_begin);  // Find-StartExpPoint (c)
-    for (;;) {
-      // ---- window: rows u0 .. u0+31, clipped to [e_begin, e_end), non-empty ones compacted
-      const int u = u0 + lane;
-      int fe = 0x7fffffff, rs = 0, x = 0;
-      if (u < n_l) {
-        fe = __ldg(fex + u);
-        rs = __ldg(frs + u);
-        x = __ldg(fx + u);
-      }
-      const int fe_last = __ldg(fex + min(u0 + 32, n_l));  // end of the window's last row
-      int fn = __shfl_down_sync(0xffffffffu, fe, 1);
-      if (lane == 31) fn = fe_last;
-      const int a = max(fe, e_begin), z = min(fn, e_end);
-      int cs = 0, ce = 0, cn = 0;
-      if (u < n_l && a < z) {
-        cs = rs + (a - fe);
-        ce = rs + (z - fe);
-        cn = ((ce + 3) >> 2) - (cs >> 2);
-      }
-      const unsigned nz = __ballot_sync(0xffffffffu, cn > 0);
-      const int nrow = __popc(nz);
-      const int src = lane < nrow ? (int)__fns(nz, 0, lane + 1) : 0;
-      const int wcs = __shfl_sync(0xffffffffu, cs, src);
-      const int wce = __shfl_sync(0xffffffffu, ce, src);
-      const int wx = __shfl_sync(0xffffffffu, x, src);
-      const int cnv = __shfl_sync(0xffffffffu, cn, src);  // every lane shuffles
-      const int wn = lane < nrow ? cnv : 0;
-      const int winc = warp_incl_scan(wn);
-      const int nch = __shfl_sync(0xffffffffu, winc, 31);
-      const int wp = lane < nrow ? winc - wn : 0x7fffffff;  // first chunk of compacted row
-      // ---- rounds of 64 chunks (2 per lane)
-      for (int c0 = 0; c0 < nch; c0 += 64) {
-        int v[KX_GROUPS];
-        int rw[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int cb = c0 + 32 * h;
-          const unsigned m = __reduce_or_sync(0xffffffffu, shl1(wp - cb));  // rows starting
-          const int r0 = __popc(__ballot_sync(0xffffffffu, wp <= cb)) - 1;  // row of chunk cb
-          const int row = max(r0, 0) + __popc(m & le & ~1u);
-          rw[h] = row;
-          const int pj = __shfl_sync(0xffffffffu, wp, row);
-          const int csj = __shfl_sync(0xffffffffu, wcs, row);
-          const int cej = __shfl_sync(0xffffffffu, wce, row);
-          const int ci = cb + lane;
-          const int base = ((csj >> 2) + (ci - pj)) << 2;  // col index of the chunk
-          int4 q = make_int4(vs, vs, vs, vs);
-#ifdef S3BFS_KX_CHECK
-          if (ci < nch && (base < 0 || (long long)base >= col_cap)) bad(3, base);
-          if (row < 0 || row >= 32) bad(4, row);
-#endif
-          if (ci < nch) {
-            if (vec && (long long)base + 4 <= col_cap) {
-              q = ldg_stream4(col + base, pol_stream);
-            } else {  // unaligned caller array / its last chunk: element loads in bounds
-              if (base + 0 >= csj && base + 0 < cej) q.x = ldg_stream(col + base + 0, pol_stream);
-              if (base + 1 >= csj && base + 1 < cej) q.y = ldg_stream(col + base + 1, pol_stream);
-              if (base + 2 >= csj && base + 2 < cej) q.z = ldg_stream(col + base + 2, pol_stream);
-              if (base + 3 >= csj && base + 3 < cej) q.w = ldg_stream(col + base + 3, pol_stream);
-            }
-          }
-          const bool in = ci < nch;
-          v[4 * h + 0] = (in && base + 0 >= csj && base + 0 < cej) ? q.x : vs;
-          v[4 * h + 1] = (in && base + 1 >= csj && base + 1 < cej) ? q.y : vs;
-          v[4 * h + 2] = (in && base + 2 >= csj && base + 2 < cej) ? q.z : vs;
-          v[4 * h + 3] = (in && base + 3 >= csj && base + 3 < cej) ? q.w : vs;
+        for (int s = 16; s >= 1; s >>= 1) {
+          const int cj = __shfl_sync(0xffffffffu, wex, min(j + s, 31));
+          if (j + s <= 31 && cj <= my_e) j += s;
         }
-        if (tag_mode) probe_round(v, wx, rw[0], rw[1], std::true_type{});
-        else probe_round(v, wx, rw[0], rw[1], std::false_type{});
+        xs[g >> 2] |= (uint32_t)j << (8 * (g & 3));
+        const int pos = __shfl_sync(0xffffffffu, wb, j) + my_e;
+        const int pf = __shfl_sync(0xffffffffu, wb, j0) + e;
+        const int t = ldg_stream(col + (my_e < bend ? pos : pf), pol_stream);
+        v[g] = (my_e < bend) ? t : vs;
       }
-      if (fe_last >= e_end || u0 + 32 >= n_l) break;
-      u0 += 32;
     }
-  }
+    return e_next;
+  };
+  // Discovery of the batch's groups flagged in discm (Fig1 L18-L22): plain stores -- the tag,
+  // {d, parent}, Owner = the candidate slot, and the candidate itself (benign race, R4).
+  auto discover = [&](const int (&v)[KX_GROUPS], const uint32_t (&xs)[KX_GROUPS / 4],
+                      uint32_t discm) {
+    const unsigned wdisc = __reduce_or_sync(0xffffffffu, discm);
+    if (!wdisc) return;  // warp-uniform skip: most batches of the heavy levels find nothing
+#pragma unroll
+    for (int g = 0; g < KX_GROUPS; ++g) {
+      if (!((wdisc >> g) & 1u)) continue;
+      // parent: the window slot's caller id (the window is unchanged since map_load)
+      const int par = __shfl_sync(0xffffffffu, wx, (xs[g >> 2] >> (8 * (g & 3))) & 31u);
+      const bool disc = (discm >> g) & 1u;
+      const unsigned m = __ballot_sync(0xffffffffu, disc);
+      if (disc) {
+        const int slot = segbase + wcount + __popc(m & lanemask_lt());
+        st_u8(claim + claim_slot(P, v[g]), tag);
+        st_weak_v2(lp + v[g], new_level, par);     // d[v] <- l, parent (Fig1 L18)
+        st_weak(owner_of(vinfo, v[g]), slot);      // Owner[v] <- i (benign race)
+        cand[slot] = v[g];                         // Q[i].Enqueue(v)
+      }
+      wcount += __popc(m);
+    }
+  };
+  // The level's visited test (Fig1 L18 "if d[v] = infinity"), chosen per level by
+  // decide_tier from the share of arcs that end at visited vertices:
+  //  bitmap mode (most targets visited, the heavy levels): every target's visited bit (exact
+  //    at level start; hub words L1-resident), then the discovery tag of the few clear ones;
+  //  tag mode (most targets new, the discovery-heavy levels): a hub id (< P.hub) reads its
+  //    bit first, any other id only its discovery tag (nonzero once discovered) -- one probe
+  //    instead of two for the arcs that reach new vertices.
+  // Masked slots probe the sentinel (its bit is always set), so the tests are branch-free.
+  auto run = [&](auto tag_mode) {
+    constexpr bool TAGS = decltype(tag_mode)::value;
+    int e = e_begin;
+    while (e < e_end) {
+      int v[KX_GROUPS];
+      uint32_t xs[KX_GROUPS / 4];  // window slots of the groups' frontier vertices, a byte each
+#pragma unroll
+      for (int k = 0; k < KX_GROUPS / 4; ++k) xs[k] = 0;
+      e = map_load(e, v, xs);
+      uint32_t needm = 0;  // targets whose discovery tag decides (bit clear at level start)
+      uint32_t discm = 0;  // targets found undiscovered: candidates (Fig1 L19-L22)
+      if constexpr (TAGS) {
+#pragma unroll
+        for (int g = 0; g < KX_GROUPS; ++g) {
+          const bool via_tag = (uint32_t)(v[g] - hub) < tag_span;
+          uint32_t r;
+          if (via_tag) r = (uint32_t)ld_cg_u8_hint(claim + claim_slot(P, v[g]), pol_status);
+          else r = ldg_status_u32(bm + 2 * (v[g] >> 5), pol_status);
+          needm |= (via_tag ? 0u : (~rotr32(r, v[g]) & 1u)) << g;
+          discm |= (via_tag ? (uint32_t)(r == 0u) : 0u) << g;
+        }
+      } else {
+#pragma unroll
+        for (int g = 0; g < KX_GROUPS; ++g) {
+          const uint32_t w = ldg_status_u32(bm + 2 * (v[g] >> 5), pol_status);
+          needm |= (~rotr32(w, v[g]) & 1u) << g;  // bit (v mod 32) of w, inverted
+        }
+      }
+      const unsigned wneed = __reduce_or_sync(0xffffffffu, needm);
+      if (wneed) {  // warp-uniform skip
+#pragma unroll
+        for (int h = 0; h < KX_GROUPS; h += 4) {  // 4 tag loads in flight (register budget)
+          int cl[4];
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            cl[g] = ((needm >> (h + g)) & 1u) ? ld_cg_u8(claim + claim_slot(P, v[h + g])) : 1;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) discm |= (uint32_t)(cl[g] == 0) << (h + g);
+        }
+      }
+      discover(v, xs, discm);
+    }
+  };
+  if (c->probe_tags) run(std::true_type{});
+  else run(std::false_type{});
   if (lane == 0) P.wcnt[b * KD_WARPS + warp] = wcount;
 }
 
@@ -832,156 +862,130 @@ __device__ __forceinline__ void bm_publish(uint32_t *bm, bool keep, int v, int l
     if (lane - s >= run0) acc |= o;
   }
   const bool last = lane == 31 || ((heads >> (lane + 1)) & 1u);
-  if (keep && last) atomicOr(bm + wd, acc);
+  if (keep && last) atomicOr(bm + 2 * wd, acc);
 #else
-  if (keep) atomicOr(bm + (v >> 5), 1u << (v & 31));
+  if (keep) atomicOr(bm + 2 * (v >> 5), 1u << (v & 31));
 #endif
 }
 
 // ---- (e)+(a)+(b): k_compact -------------------------------------------------------------------
-// The level's candidates sit in k_explore's per-warp segments (warp s = CTA b's warp w writes
-// cand[s * wcap + 0 .. wcnt[s])).  Every CTA first scans the wcnt[] array into shared memory
-// (one exclusive prefix over the level's P_l x 16 segments), which numbers the candidates
-// densely 0 .. C-1; tiles of KC_TILE consecutive candidate numbers are then taken in CTA start
-// order (an atomic tile counter), so the work is balanced however unevenly the discoveries
-// fell on k_explore's warps.  Per candidate (Fig1 L20-L23): slot k and vertex v = cand[k]; keep
-// iff Owner[v] == k (one 16-byte vertex-record probe also gives the row start, degree and
-// caller id); publish the kept vertex's visited bit.  A decoupled look-back over the tiles
-// scans the (kept, degree-sum) pairs (Fig1 L24, and L12-L15 of the next level in the same
-// pass), and each tile writes its kept vertices straight from registers into the next
-// frontier: caller ids, row starts, exclusive degree scan (Fig1 L25-L29).  The last CTA to
-// finish advances the control block (Fig1 L9-L10, L15-L16).
+// CTA b handles the candidate segments its k_explore twin wrote (one per warp).
+// Pass 1 (Fig1 L20-L23): keep cand[k] iff Owner[cand[k]] == k (one 16-byte vertex-record
+// probe gives Owner, row start and degree); publish the kept vertex's visited bit and
+// compact (id, row start, degree) in place -- the degree is Fig1 L13 of the next level.
+// The next frontier holds caller ids (from the same record), the parents k_explore records.
+// A decoupled look-back over CTAs scans the (kept, degree-sum) pairs (Fig1 L24 and L14 of
+// the next level in one pass).  Pass 2 (Fig1 L25-L29): write the next frontier, its row
+// starts and its exclusive degree scan.  The last CTA to finish advances the control block
+// (Fig1 L9-L10, L15-L16).
 __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P) {
   Ctl *c = P.ctl;
   if (c->tier != TIER_LARGE) return;
-  extern __shared__ int32_t s_pre[];  // exclusive prefix of wcnt[0 .. nseg), then the total
+  const int p_l = c->p_l;
   __shared__ int32_t s_k[KD_WARPS], s_d[KD_WARPS];
   __shared__ int s_last, s_tile;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int p_l = c->p_l, wcap = c->wcap, nxt = c->cur ^ 1;
-  const int nseg = p_l * KD_WARPS;
-  const bool dist = P.dist_size > 1;
-  if (blockIdx.x == 0 && tid == 0) c->t_kx_end = globaltimer();
-  // ---- the dense numbering: exclusive scan of the segment counts (blocked, ipt per thread)
-  {
-    const int ipt = (nseg + KD_THREADS - 1) / KD_THREADS;
-    const int s0 = tid * ipt;
-    int sum = 0;
-    for (int i = 0; i < ipt; ++i) sum += (s0 + i < nseg) ? __ldcg(P.wcnt + s0 + i) : 0;
-    const int inc = warp_incl_scan(sum);
-    if (lane == 31) s_k[warp] = inc;
-    __syncthreads();
-    const int wt = lane < KD_WARPS ? s_k[lane] : 0;
-    const int wi = warp_incl_scan(wt);
-    int run = __shfl_sync(0xffffffffu, wi - wt, warp) + inc - sum;
-    for (int i = 0; i < ipt; ++i) {
-      if (s0 + i < nseg) {
-        s_pre[s0 + i] = run;
-        run += __ldcg(P.wcnt + s0 + i);
-      }
-    }
-    const int tot = __shfl_sync(0xffffffffu, wi, 31);  // lanes >= KD_WARPS add nothing
-    if (tid == 0) s_pre[nseg] = tot;
-    __syncthreads();
-  }
-  const int total = s_pre[nseg];
-  const int ntiles = (total + KC_TILE - 1) / KC_TILE;
-  if (P.collect_stats && blockIdx.x == 0 && tid == 0) c->cand_acc = total;  // statistics only
+  // Surplus CTAs (blockIdx >= P_l) do no work but are still counted by the last-CTA
+  // election below: the control block is rewritten only after EVERY CTA of this launch has
+  // read it (a late-starting surplus CTA would otherwise see the next level's state).
+  const int nxt = c->cur ^ 1;
+  if ((int)blockIdx.x < p_l) {
+  if (tid == 0) s_tile = (int)atomicAdd(&c->tile_ctr, 1u);  // look-back order = start order
+  __syncthreads();
+  const int b = s_tile;  // this CTA handles tile b: the segments of k_explore's CTA b
   const int4 *__restrict__ vinfo = P.vinfo;
-  const int32_t *__restrict__ cand = P.cand;
+  int32_t *__restrict__ cand = P.cand;
+  int2 *__restrict__ crd = P.cand_rd;
+  const int seg = (b * KD_WARPS + warp) * c->wcap;
+  const int cnt = P.wcnt[b * KD_WARPS + warp];
+  const bool dist = P.dist_size > 1;
+  if (b == 0 && tid == 0) c->t_kx_end = globaltimer();
+
+  int kept = 0, dsum = 0;
+  for (int k0 = 0; k0 < cnt; k0 += 32 * KC_GROUPS) {
+    int v[KC_GROUPS];
+#pragma unroll
+    for (int g = 0; g < KC_GROUPS; ++g) {
+      const int k = k0 + g * 32 + lane;
+      v[g] = (k < cnt) ? cand[seg + k] : -1;
+    }
+    int4 vi[KC_GROUPS];  // {row start, degree, caller id, Owner}: one sector per candidate
+#pragma unroll
+    for (int g = 0; g < KC_GROUPS; ++g)
+      vi[g] = (v[g] >= 0) ? __ldg(vinfo + v[g]) : make_int4(0, 0, 0, -1);
+#pragma unroll
+    for (int g = 0; g < KC_GROUPS; ++g) {
+      const int k = k0 + g * 32 + lane;
+      const bool keep = v[g] >= 0 && vi[g].w == seg + k;  // Fig1 L22: "if Owner[v] = i"
+      const int d = keep ? vi[g].y : 0;
+      bm_publish(P.bm, keep, v[g], lane);  // exact visited bit (R17)
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const int q = seg + kept + __popc(m & lanemask_lt());
+        cand[q] = dist ? v[g] : vi[g].z;  // NEXT-4 keeps the internal id for the record
+        crd[q] = make_int2(vi[g].x, d);
+      }
+      kept += __popc(m);
+      dsum += d;
+    }
+  }
+  dsum = warp_sum(dsum);
+  if (lane == 0) { s_k[warp] = kept; s_d[warp] = dsum; }
+  if (P.collect_stats) {
+    const int tot = warp_sum(lane == 0 ? cnt : 0);
+    if (lane == 0 && tot) atomicAdd(&c->cand_acc, tot);  // statistics only
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int kk = lane < KD_WARPS ? s_k[lane] : 0;
+    const int dd = lane < KD_WARPS ? s_d[lane] : 0;
+    const int ik = warp_incl_scan(kk), id = warp_incl_scan(dd);
+    const Pair agg{(uint32_t)__shfl_sync(0xffffffffu, ik, 31),
+                   (uint32_t)__shfl_sync(0xffffffffu, id, 31)};
+    const Pair ex = lookback<true>(P.status, b, agg);
+    if (lane < KD_WARPS) {
+      s_k[lane] = (int)ex.a + ik - kk;
+      s_d[lane] = (int)ex.b + id - dd;
+    }
+    if (b == p_l - 1 && lane == 0) {  // the level's totals: n_{l+1}, e_{l+1} (Fig1 L15)
+      const int n_next = (int)(ex.a + agg.a), e_next = (int)(ex.b + agg.b);
+      c->n_next = n_next;
+      c->e_next = e_next;
+      if (!dist) P.fex[nxt][n_next] = e_next;
+    }
+  }
+  __syncthreads();
+  int koff = s_k[warp], doff = s_d[warp];
   int32_t *__restrict__ fn = P.f[nxt];
   int32_t *__restrict__ frsn = P.frs[nxt];
   int32_t *__restrict__ fexn = P.fex[nxt];
-  for (;;) {
-    if (tid == 0) s_tile = (int)atomicAdd(&c->tile_ctr, 1u);  // look-back order = start order
-    __syncthreads();
-    const int t = s_tile;
-    if (t >= ntiles) break;
-    // ---- pass over the tile's candidates: item k of thread tid = number t*KC_TILE + k*512 + tid
-    int v[KC_ITEMS], sl[KC_ITEMS];
-#pragma unroll
-    for (int k = 0; k < KC_ITEMS; ++k) {
-      const int i = t * KC_TILE + k * KD_THREADS + tid;
-      v[k] = -1;
-      sl[k] = -1;
-      if (i < total) {
-        int lo = 0, hi = nseg;  // the segment holding number i: last s with s_pre[s] <= i
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (s_pre[mid] <= i) lo = mid; else hi = mid;
-        }
-        sl[k] = lo * wcap + (i - s_pre[lo]);
+  for (int k0 = 0; k0 < kept; k0 += 32) {
+    const int k = k0 + lane;
+    int v = 0, r0 = 0, d = 0;
+    if (k < kept) {
+      v = cand[seg + k];
+      const int2 rd = crd[seg + k];
+      r0 = rd.x;
+      d = rd.y;
+    }
+    const int inc = warp_incl_scan(d);
+    if (k < kept) {
+      if (dist) {  // NEXT-4: this rank's kept vertex, for the cross-rank merge
+        P.rec[koff + k] = make_int4(v, P.lp[v].y, r0, d);
+      } else {
+        fn[koff + k] = v;
+        frsn[koff + k] = r0;
+        fexn[koff + k] = doff + inc - d;
       }
     }
-#pragma unroll
-    for (int k = 0; k < KC_ITEMS; ++k) v[k] = sl[k] >= 0 ? __ldcg(cand + sl[k]) : -1;
-    int4 vi[KC_ITEMS];  // {row start, degree, caller id, Owner}: one sector per candidate
-#pragma unroll
-    for (int k = 0; k < KC_ITEMS; ++k)
-      vi[k] = v[k] >= 0 ? __ldg(vinfo + v[k]) : make_int4(0, 0, 0, -1);
-    unsigned km[KC_ITEMS];
-    int kept = 0, dsum = 0;
-#pragma unroll
-    for (int k = 0; k < KC_ITEMS; ++k) {
-      const bool keep = v[k] >= 0 && vi[k].w == sl[k];  // Fig1 L22: "if Owner[v] = i"
-      bm_publish(P.bm, keep, v[k], lane);               // exact visited bit (R17)
-      km[k] = __ballot_sync(0xffffffffu, keep);
-      kept += __popc(km[k]);
-      dsum += keep ? vi[k].y : 0;
-    }
-    dsum = warp_sum(dsum);
-    if (lane == 0) { s_k[warp] = kept; s_d[warp] = dsum; }
-    __syncthreads();
-    if (warp == 0) {
-      const int kk = lane < KD_WARPS ? s_k[lane] : 0;
-      const int dd = lane < KD_WARPS ? s_d[lane] : 0;
-      const int ik = warp_incl_scan(kk), id = warp_incl_scan(dd);
-      const Pair agg{(uint32_t)__shfl_sync(0xffffffffu, ik, 31),
-                     (uint32_t)__shfl_sync(0xffffffffu, id, 31)};
-      const Pair ex = lookback<true>(P.status, t, agg);
-      if (lane < KD_WARPS) {
-        s_k[lane] = (int)ex.a + ik - kk;
-        s_d[lane] = (int)ex.b + id - dd;
-      }
-      if (t == ntiles - 1 && lane == 0) {  // the level's totals: n_{l+1}, e_{l+1} (Fig1 L15)
-        const int n_next = (int)(ex.a + agg.a), e_next = (int)(ex.b + agg.b);
-        c->n_next = n_next;
-        c->e_next = e_next;
-        if (!dist) P.fex[nxt][n_next] = e_next;
-      }
-    }
-    __syncthreads();
-    // ---- the tile's kept vertices into the next frontier, in (warp, item, lane) order
-    int koff = s_k[warp], doff = s_d[warp];
-#pragma unroll
-    for (int k = 0; k < KC_ITEMS; ++k) {
-      const bool keep = (km[k] >> lane) & 1u;
-      const int d = keep ? vi[k].y : 0;
-      const int inc = warp_incl_scan(d);
-      if (keep) {
-        const int pos = koff + __popc(km[k] & lanemask_lt());
-        if (dist) {  // NEXT-4: this rank's kept vertex, for the cross-rank merge
-          P.rec[pos] = make_int4(v[k], P.lp[v[k]].y, vi[k].x, d);
-        } else {
-          fn[pos] = vi[k].z;     // caller id (the parent the next level records)
-          frsn[pos] = vi[k].x;   // internal row start
-          fexn[pos] = doff + inc - d;
-        }
-      }
-      koff += __popc(km[k]);
-      doff += __shfl_sync(0xffffffffu, inc, 31);
-    }
+    doff += __shfl_sync(0xffffffffu, inc, 31);
   }
+  }  // active CTA
   // last-CTA election over the whole grid (one atomic per CTA; not the discovery path, R17)
   __threadfence();
   __syncthreads();
   if (tid == 0) s_last = atomicAdd(&c->done_ctr, 1u) == gridDim.x - 1;
   __syncthreads();
-  if (s_last && tid == 0 && ntiles == 0) {  // no candidates: an empty next frontier
-    c->n_next = 0;
-    c->e_next = 0;
-    if (!dist) P.fex[nxt][0] = 0;
-  }
   if (s_last && tid == 0 && P.dist_size > 1) {
     // NEXT-4: the local kept count stays in n_next; the merge advances the level
     c->done_ctr = 0;
@@ -1149,7 +1153,7 @@ __device__ void tiny_levels(const Params &P, Ctl *c, int32_t *sf, int32_t *srs, 
     const int pe = __shfl_sync(0xffffffffu, fex, u);
     const bool has = lane < e_l;
     const int v = has ? __ldg(col + pr + (lane - pe)) : 0;
-    const uint32_t w = __ldcg(P.bm + (v >> 5));      // published by atomicOr at L2
+    const uint32_t w = __ldcg(P.bm + 2 * (v >> 5));  // published by atomicOr at L2
     // issued together with the bitmap word; through L2 (ld.global.cg), never the read-only
     // path: k_small's block levels store Owner into the same 16-byte record in this launch
     const int4 vi = __ldcg(P.vinfo + v);
@@ -1164,7 +1168,7 @@ __device__ void tiny_levels(const Params &P, Ctl *c, int32_t *sf, int32_t *srs, 
     const unsigned km = ncand > 1 ? __ballot_sync(0xffffffffu, keep) : fm;
     if (keep) {
       P.lp[v] = make_int2(L + 1, px);                 // d[v] <- l, parent (Fig1 L18)
-      atomicOr(P.bm + (v >> 5), 1u << (v & 31));      // exact visited bit
+      atomicOr(P.bm + 2 * (v >> 5), 1u << (v & 31));  // exact visited bit
       mark_tag(P, v);
     }
     const int d = keep ? vi.y : 0;
@@ -1295,7 +1299,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
     uint32_t wv[KS_IPT];
 #pragma unroll
     for (int i = 0; i < KS_IPT; ++i)  // L1-bypassing: bits are published by atomicOr at L2 in
-      wv[i] = ev[i] >= 0 ? __ldcg(bm + (ev[i] >> 5)) : 0xffffffffu;  // earlier levels (H2)
+      wv[i] = ev[i] >= 0 ? __ldcg(bm + 2 * (ev[i] >> 5)) : 0xffffffffu;  // earlier levels (H2)
 #pragma unroll
     for (int i = 0; i < KS_IPT; ++i) {
       const int e = tid + i * KS_THREADS;
@@ -1335,7 +1339,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
       if (v >= 0 && vis[i].w == e) {
         kv[i] = vis[i].z; kr[i] = vis[i].x; kd[i] = vis[i].y;
         P.lp[v] = make_int2(L + 1, cpv[e]);         // d[v] <- l, parent (Fig1 L18)
-        atomicOr(P.bm + (v >> 5), 1u << (v & 31));  // exact visited bit (not discovery)
+        atomicOr(P.bm + 2 * (v >> 5), 1u << (v & 31));  // exact visited bit (not discovery)
         mark_tag(P, v);
       }
     }
@@ -1491,7 +1495,7 @@ __global__ void __cluster_dims__(KC_CL, 1, 1) __launch_bounds__(KC_THREADS, 1) k
     }
     uint32_t wv[KC_IPT];
 #pragma unroll
-    for (int i = 0; i < KC_IPT; ++i) wv[i] = ev[i] >= 0 ? __ldcg(bm + (ev[i] >> 5)) : 0xffffffffu;
+    for (int i = 0; i < KC_IPT; ++i) wv[i] = ev[i] >= 0 ? __ldcg(bm + 2 * (ev[i] >> 5)) : 0xffffffffu;
 #pragma unroll
     for (int i = 0; i < KC_IPT; ++i) {
       const int k = tid + i * KC_THREADS;
@@ -1535,7 +1539,7 @@ __global__ void __cluster_dims__(KC_CL, 1, 1) __launch_bounds__(KC_THREADS, 1) k
       if (v >= 0 && vis[i].w == lo + k) {
         kv[i] = vis[i].z; kr[i] = vis[i].x; kd[i] = vis[i].y;
         P.lp[v] = make_int2(L + 1, cpv[k]);          // d[v] <- l, parent (Fig1 L18)
-        atomicOr(P.bm + (v >> 5), 1u << (v & 31));   // exact visited bit (not discovery)
+        atomicOr(P.bm + 2 * (v >> 5), 1u << (v & 31));  // exact visited bit (not discovery)
         mark_tag(P, v);
         ++cnt;
         dsum += kd[i];
@@ -1699,7 +1703,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params 
     for (int i = 0; i < BU_W; ++i) {
       const int w = wb + i;
       const int v = (w << 5) + lane;
-      bw[i] = (w < w1) ? bm[w] : 0xffffffffu;
+      bw[i] = (w < w1) ? bm[2 * w] : 0xffffffffu;
       const bool act = w < w1 && v < nscan && !((bw[i] >> lane) & 1u);
       r0[i] = act ? __ldg(P.tro + v) : 0;
       r1[i] = act ? __ldg(P.tro + v + 1) : 0;
@@ -1742,7 +1746,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params 
       }
       const unsigned m = __ballot_sync(0xffffffffu, found);
       if (lane == 0 && w < w1) {
-        if (m) bm[w] = bw[i] | m;  // this warp owns word w
+        if (m) bm[2 * w] = bw[i] | m;  // this warp owns word w
         fbn[w] = m;
       }
       kept += __popc(m);
@@ -1826,7 +1830,7 @@ __global__ void k_finalize(Params P) {
        o += (long long)gridDim.x * blockDim.x) {
     const int i = P.o2n ? __ldg(P.o2n + o) : (int)o;
     int lv = -1, pa = -1;
-    if ((__ldg(P.bm + (i >> 5)) >> (i & 31)) & 1u) {
+    if ((__ldg(P.bm + 2 * (i >> 5)) >> (i & 31)) & 1u) {
       const int2 r = __ldg(P.lp + i);
       lv = r.x;
       pa = r.y;
