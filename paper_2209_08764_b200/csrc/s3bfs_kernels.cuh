@@ -301,6 +301,14 @@ __device__ __forceinline__ int ld_cg_u8_hint(const uint8_t *p, unsigned long lon
   asm volatile("ld.global.cg.L2::cache_hint.u8 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
   return (int)v;
 }
+// an id's status pair {visited word, claim word}: weak 8-byte load (L1-allocating; the claim
+// word is stored by other workers during the level, a stale copy only admits a duplicate)
+__device__ __forceinline__ uint2 ld_pair(const uint32_t *p, unsigned long long pol) {
+  uint2 r;
+  asm volatile("ld.global.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+               : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(pol));
+  return r;
+}
 __device__ __forceinline__ void st_u8(uint8_t *p, int v) {
   asm volatile("st.global.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -631,7 +639,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   int4 *__restrict__ vinfo = P.vinfo;
   int2 *__restrict__ lp = P.lp;
   int32_t *__restrict__ cand = P.cand;
-  const uint32_t *__restrict__ bm = P.bm;
+  uint32_t *__restrict__ bm = P.bm;
   uint8_t *__restrict__ claim = P.claim;
   const int vs = P.v_sent;  // masked lanes' target: its visited bit is always set
   const int hub = P.hub;                              // ids < hub: bitmap first
@@ -768,8 +776,14 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   };
   // Discovery of the batch's groups flagged in discm (Fig1 L18-L22): plain stores -- the tag,
   // {d, parent}, Owner = the candidate slot, and the candidate itself (benign race, R4).
+  // Discovery of the batch's groups flagged in discm (Fig1 L18-L22), plain stores (benign
+  // race): the claim -- the discovery tag (tag mode, non-hub id) or the id's bit in its claim
+  // word (cw | bit, cw = the word as loaded; a racing store may drop another id's bit, which
+  // only lets that id be enqueued twice) --, then {d, parent}, Owner = the candidate slot and
+  // the candidate itself.  The Owner check keeps exactly one copy of any duplicate (R4).
   auto discover = [&](const int (&v)[KX_GROUPS], const uint32_t (&xs)[KX_GROUPS / 4],
-                      uint32_t discm) {
+                      const uint32_t (&cw)[KX_GROUPS], uint32_t discm, auto tag_mode) {
+    constexpr bool TAGS = decltype(tag_mode)::value;
     const unsigned wdisc = __reduce_or_sync(0xffffffffu, discm);
     if (!wdisc) return;  // warp-uniform skip: most batches of the heavy levels find nothing
 #pragma unroll
@@ -781,7 +795,11 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
       const unsigned m = __ballot_sync(0xffffffffu, disc);
       if (disc) {
         const int slot = segbase + wcount + __popc(m & lanemask_lt());
-        st_u8(claim + claim_slot(P, v[g]), tag);
+        if (TAGS && (uint32_t)(v[g] - hub) < tag_span)
+          st_u8(claim + claim_slot(P, v[g]), tag);
+        else
+          st_weak(reinterpret_cast<int32_t *>(bm + 2 * (v[g] >> 5) + 1),
+                  (int)(cw[g] | (1u << (v[g] & 31))));
         st_weak_v2(lp + v[g], new_level, par);     // d[v] <- l, parent (Fig1 L18)
         st_weak(owner_of(vinfo, v[g]), slot);      // Owner[v] <- i (benign race)
         cand[slot] = v[g];                         // Q[i].Enqueue(v)
@@ -789,14 +807,16 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
       wcount += __popc(m);
     }
   };
-  // The level's visited test (Fig1 L18 "if d[v] = infinity"), chosen per level by
-  // decide_tier from the share of arcs that end at visited vertices:
-  //  bitmap mode (most targets visited, the heavy levels): every target's visited bit (exact
-  //    at level start; hub words L1-resident), then the discovery tag of the few clear ones;
-  //  tag mode (most targets new, the discovery-heavy levels): a hub id (< P.hub) reads its
-  //    bit first, any other id only its discovery tag (nonzero once discovered) -- one probe
-  //    instead of two for the arcs that reach new vertices.
-  // Masked slots probe the sentinel (its bit is always set), so the tests are branch-free.
+  // The level's visited test (Fig1 L18 "if d[v] = infinity"), one probe per arc.  An id's
+  // status pair {visited word (exact at level start; the hottest ids' words L1-resident),
+  // claim word (bits of the ids some worker discovered in this level)} is one 8-byte load:
+  // v is new iff both bits are clear -- the d[v] = infinity test on d as this level updates
+  // it, with no second dependent load.  Chosen per level by decide_tier:
+  //  bitmap mode (most targets visited, the heavy levels): every id by its status pair;
+  //  tag mode (most targets new, the discovery-heavy levels): hub ids (< P.hub) by their
+  //    status pair, any other id by its 1-byte discovery tag (nonzero once discovered in
+  //    this or an earlier level): the new ids' pairs are cold, the tags half as wide.
+  // Masked slots probe the sentinel pair (all bits set), so the tests are branch-free.
   auto run = [&](auto tag_mode) {
     constexpr bool TAGS = decltype(tag_mode)::value;
     int e = e_begin;
@@ -806,38 +826,21 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
 #pragma unroll
       for (int k = 0; k < KX_GROUPS / 4; ++k) xs[k] = 0;
       e = map_load(e, v, xs);
-      uint32_t needm = 0;  // targets whose discovery tag decides (bit clear at level start)
       uint32_t discm = 0;  // targets found undiscovered: candidates (Fig1 L19-L22)
-      if constexpr (TAGS) {
+      uint32_t cw[KX_GROUPS];  // claim words as loaded (the discoverer's store value)
 #pragma unroll
-        for (int g = 0; g < KX_GROUPS; ++g) {
-          const bool via_tag = (uint32_t)(v[g] - hub) < tag_span;
-          uint32_t r;
-          if (via_tag) r = (uint32_t)ld_cg_u8_hint(claim + claim_slot(P, v[g]), pol_status);
-          else r = ldg_status_u32(bm + 2 * (v[g] >> 5), pol_status);
-          needm |= (via_tag ? 0u : (~rotr32(r, v[g]) & 1u)) << g;
-          discm |= (via_tag ? (uint32_t)(r == 0u) : 0u) << g;
-        }
-      } else {
-#pragma unroll
-        for (int g = 0; g < KX_GROUPS; ++g) {
-          const uint32_t w = ldg_status_u32(bm + 2 * (v[g] >> 5), pol_status);
-          needm |= (~rotr32(w, v[g]) & 1u) << g;  // bit (v mod 32) of w, inverted
+      for (int g = 0; g < KX_GROUPS; ++g) {
+        if (TAGS && (uint32_t)(v[g] - hub) < tag_span) {
+          const uint32_t t = (uint32_t)ld_cg_u8_hint(claim + claim_slot(P, v[g]), pol_status);
+          cw[g] = 0;
+          discm |= (uint32_t)(t == 0u) << g;
+        } else {
+          const uint2 q = ld_pair(bm + 2 * (v[g] >> 5), pol_status);
+          cw[g] = q.y;
+          discm |= (~rotr32(q.x | q.y, v[g]) & 1u) << g;  // bit (v mod 32) of both, inverted
         }
       }
-      const unsigned wneed = __reduce_or_sync(0xffffffffu, needm);
-      if (wneed) {  // warp-uniform skip
-#pragma unroll
-        for (int h = 0; h < KX_GROUPS; h += 4) {  // 4 tag loads in flight (register budget)
-          int cl[4];
-#pragma unroll
-          for (int g = 0; g < 4; ++g)
-            cl[g] = ((needm >> (h + g)) & 1u) ? ld_cg_u8(claim + claim_slot(P, v[h + g])) : 1;
-#pragma unroll
-          for (int g = 0; g < 4; ++g) discm |= (uint32_t)(cl[g] == 0) << (h + g);
-        }
-      }
-      discover(v, xs, discm);
+      discover(v, xs, cw, discm, tag_mode);
     }
   };
   if (c->probe_tags) run(std::true_type{});
