@@ -513,8 +513,7 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   const size_t o_cand = take((size_t)h->cand_cap * 4);
   const size_t o_crd = take((size_t)h->cand_cap * 8);
   const size_t bm_bytes = ((size_t)n + 127) / 128 * 16;  // 16 B padded (vector clears)
-  // status pairs {visited word, claim word} per 32 ids + 2 sentinel blocks (Params::v_sent)
-  const size_t o_bm = take(2 * bm_bytes + 32);
+  const size_t o_bm = take(bm_bytes + 16);  // + the sentinel block (Params::v_sent)
   // claim slots: a power of two >= max(n, a floor) (claim_slot's hash is mod 2^k); the floor
   // spreads a small graph's tags over more L2 lines (fewer same-line probes and stores)
   size_t claim_n = 16;
@@ -638,9 +637,6 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
     h->ro_int = row_offsets;
   }
   P.col_vec = (((uintptr_t)P.col) & 15) == 0 ? 1 : 0;
-  // the internal copy is allocated with 16 bytes of slack (its last chunk may be read whole);
-  // the caller's array only up to nnz
-  P.col_cap = (share ? share->P.col_cap : (h->opt.reorder >= 0 ? nnz + 4 : nnz));
   if (P.direction && !share) {
     s3bfs_status ts = build_in_adjacency(h, stream);
     if (ts != S3BFS_OK) return bail(ts);

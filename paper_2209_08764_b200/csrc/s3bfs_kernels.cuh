@@ -93,6 +93,9 @@ namespace s3bfs {
 #ifndef S3BFS_BU_P
 #define S3BFS_BU_P 2
 #endif
+#ifndef S3BFS_KC_GROUPS
+#define S3BFS_KC_GROUPS 4
+#endif
 #ifndef S3BFS_BU_TILES_PER_CTA
 #define S3BFS_BU_TILES_PER_CTA 4  // bottom-up: about this many tiles per resident CTA
 #endif
@@ -107,7 +110,7 @@ constexpr int KD_MIN_BLOCKS = S3BFS_KD_MINB;    // CTAs per SM the register budg
 constexpr int KD_WARPS = KD_THREADS / 32;
 constexpr int KD_SLACK = 64;                    // candidate-buffer slack per CTA
 constexpr int KX_GROUPS = S3BFS_KX_GROUPS;      // 32-edge groups per batch and warp
-constexpr int KC_GROUPS = 4;                     // 32-candidate groups per k_compact round
+constexpr int KC_GROUPS = S3BFS_KC_GROUPS;      // 32-candidate groups per k_compact round
 constexpr int KS_THREADS = 1024;                // k_small CTA size
 constexpr int KS_ECAP = 8192;                   // T0 maximum (edges per tier-0 level)
 constexpr int KS_NCAP = KS_ECAP;                // frontier capacity of tier 0 (kept <= e_l)
@@ -173,9 +176,7 @@ struct Params {
                                     // discoveries), internal row starts, degree scan
   int32_t *cand;                // candidate per slot (k_explore), compacted by k_compact
   int2 *cand_rd;                // (row start, degree) of kept candidates, pass 1 -> pass 2
-  uint32_t *bm;                 // status pairs, one per 32 internal ids: word 2w = visited
-                                //  bits of ids 32w..32w+31 (bit set => visited, exact at level
-                                //  start), word 2w+1 = the level's claim bits (k_explore);
+  uint32_t *bm;                 // visited bitmap: bit set => visited (exact at level start),
                                 //  plus one always-set 16 B sentinel block after the padded end
   unsigned long long pol_first, pol_last;  // L2 createpolicy descriptors (evict-first for the
                                 //  col stream, evict-last for the bitmap), made once at create:
@@ -207,7 +208,6 @@ struct Params {
   unsigned long long *m_status; // NEXT-4: merge look-back words
   long long nnz;
   int32_t col_vec;              // col is 16-byte aligned: vectorised loads allowed
-  long long col_cap;            // col elements that may be read (16-byte chunks up to it)
   int32_t use_graph;
   unsigned long long h_while, h_tier;  // cudaGraphConditionalHandle values (WHILE; SWITCH on
                                        // the tier: body 0 tier 0, 1 top-down, 2 bottom-up)
@@ -300,14 +300,6 @@ __device__ __forceinline__ int ld_cg_u8_hint(const uint8_t *p, unsigned long lon
   unsigned v;
   asm volatile("ld.global.cg.L2::cache_hint.u8 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
   return (int)v;
-}
-// an id's status pair {visited word, claim word}: weak 8-byte load (L1-allocating; the claim
-// word is stored by other workers during the level, a stale copy only admits a duplicate)
-__device__ __forceinline__ uint2 ld_pair(const uint32_t *p, unsigned long long pol) {
-  uint2 r;
-  asm volatile("ld.global.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
-               : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(pol));
-  return r;
 }
 __device__ __forceinline__ void st_u8(uint8_t *p, int v) {
   asm volatile("st.global.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -557,12 +549,10 @@ __global__ void k_init(Params P, int32_t s, int32_t *level, int32_t *parent) {
   const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long gstride = (long long)gridDim.x * blockDim.x;
   const int si = P.o2n ? __ldg(P.o2n + s) : s;  // the source's internal id
-  // status pairs as uint4 (two pairs = 64 ids each, padded to 128 ids); the 2 blocks after
-  // the padded end are the all-ones sentinel (Params::v_sent)
-  const long long nw4 = (((long long)n + 127) >> 7) * 2;
-  for (long long i = gtid; i < nw4 + 2; i += gstride) {
-    uint4 w = i >= nw4 ? make_uint4(~0u, ~0u, ~0u, ~0u) : make_uint4(0, 0, 0, 0);
-    if (i == (si >> 6)) (&w.x)[((si >> 5) & 1) * 2] = 1u << (si & 31);
+  const long long nw4 = ((long long)n + 127) >> 7;  // bitmap as uint4 (16 B padded)
+  for (long long i = gtid; i <= nw4; i += gstride) {  // block nw4: the all-ones sentinel
+    uint4 w = i == nw4 ? make_uint4(~0u, ~0u, ~0u, ~0u) : make_uint4(0, 0, 0, 0);
+    if (i == (si >> 7)) (&w.x)[(si >> 5) & 3] = 1u << (si & 31);
     reinterpret_cast<uint4 *>(P.bm)[i] = w;
   }
   const long long nc = ((long long)P.claim_mask + 16) >> 4;  // claim tags <- 0 (all slots),
@@ -639,7 +629,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   int4 *__restrict__ vinfo = P.vinfo;
   int2 *__restrict__ lp = P.lp;
   int32_t *__restrict__ cand = P.cand;
-  uint32_t *__restrict__ bm = P.bm;
+  const uint32_t *__restrict__ bm = P.bm;
   uint8_t *__restrict__ claim = P.claim;
   const int vs = P.v_sent;  // masked lanes' target: its visited bit is always set
   const int hub = P.hub;                              // ids < hub: bitmap first
@@ -776,14 +766,8 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   };
   // Discovery of the batch's groups flagged in discm (Fig1 L18-L22): plain stores -- the tag,
   // {d, parent}, Owner = the candidate slot, and the candidate itself (benign race, R4).
-  // Discovery of the batch's groups flagged in discm (Fig1 L18-L22), plain stores (benign
-  // race): the claim -- the discovery tag (tag mode, non-hub id) or the id's bit in its claim
-  // word (cw | bit, cw = the word as loaded; a racing store may drop another id's bit, which
-  // only lets that id be enqueued twice) --, then {d, parent}, Owner = the candidate slot and
-  // the candidate itself.  The Owner check keeps exactly one copy of any duplicate (R4).
   auto discover = [&](const int (&v)[KX_GROUPS], const uint32_t (&xs)[KX_GROUPS / 4],
-                      const uint32_t (&cw)[KX_GROUPS], uint32_t discm, auto tag_mode) {
-    constexpr bool TAGS = decltype(tag_mode)::value;
+                      uint32_t discm) {
     const unsigned wdisc = __reduce_or_sync(0xffffffffu, discm);
     if (!wdisc) return;  // warp-uniform skip: most batches of the heavy levels find nothing
 #pragma unroll
@@ -795,11 +779,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
       const unsigned m = __ballot_sync(0xffffffffu, disc);
       if (disc) {
         const int slot = segbase + wcount + __popc(m & lanemask_lt());
-        if (TAGS && (uint32_t)(v[g] - hub) < tag_span)
-          st_u8(claim + claim_slot(P, v[g]), tag);
-        else
-          st_weak(reinterpret_cast<int32_t *>(bm + 2 * (v[g] >> 5) + 1),
-                  (int)(cw[g] | (1u << (v[g] & 31))));
+        st_u8(claim + claim_slot(P, v[g]), tag);
         st_weak_v2(lp + v[g], new_level, par);     // d[v] <- l, parent (Fig1 L18)
         st_weak(owner_of(vinfo, v[g]), slot);      // Owner[v] <- i (benign race)
         cand[slot] = v[g];                         // Q[i].Enqueue(v)
@@ -807,16 +787,14 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
       wcount += __popc(m);
     }
   };
-  // The level's visited test (Fig1 L18 "if d[v] = infinity"), one probe per arc.  An id's
-  // status pair {visited word (exact at level start; the hottest ids' words L1-resident),
-  // claim word (bits of the ids some worker discovered in this level)} is one 8-byte load:
-  // v is new iff both bits are clear -- the d[v] = infinity test on d as this level updates
-  // it, with no second dependent load.  Chosen per level by decide_tier:
-  //  bitmap mode (most targets visited, the heavy levels): every id by its status pair;
-  //  tag mode (most targets new, the discovery-heavy levels): hub ids (< P.hub) by their
-  //    status pair, any other id by its 1-byte discovery tag (nonzero once discovered in
-  //    this or an earlier level): the new ids' pairs are cold, the tags half as wide.
-  // Masked slots probe the sentinel pair (all bits set), so the tests are branch-free.
+  // The level's visited test (Fig1 L18 "if d[v] = infinity"), chosen per level by
+  // decide_tier from the share of arcs that end at visited vertices:
+  //  bitmap mode (most targets visited, the heavy levels): every target's visited bit (exact
+  //    at level start; hub words L1-resident), then the discovery tag of the few clear ones;
+  //  tag mode (most targets new, the discovery-heavy levels): a hub id (< P.hub) reads its
+  //    bit first, any other id only its discovery tag (nonzero once discovered) -- one probe
+  //    instead of two for the arcs that reach new vertices.
+  // Masked slots probe the sentinel (its bit is always set), so the tests are branch-free.
   auto run = [&](auto tag_mode) {
     constexpr bool TAGS = decltype(tag_mode)::value;
     int e = e_begin;
@@ -826,21 +804,38 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
 #pragma unroll
       for (int k = 0; k < KX_GROUPS / 4; ++k) xs[k] = 0;
       e = map_load(e, v, xs);
+      uint32_t needm = 0;  // targets whose discovery tag decides (bit clear at level start)
       uint32_t discm = 0;  // targets found undiscovered: candidates (Fig1 L19-L22)
-      uint32_t cw[KX_GROUPS];  // claim words as loaded (the discoverer's store value)
+      if constexpr (TAGS) {
 #pragma unroll
-      for (int g = 0; g < KX_GROUPS; ++g) {
-        if (TAGS && (uint32_t)(v[g] - hub) < tag_span) {
-          const uint32_t t = (uint32_t)ld_cg_u8_hint(claim + claim_slot(P, v[g]), pol_status);
-          cw[g] = 0;
-          discm |= (uint32_t)(t == 0u) << g;
-        } else {
-          const uint2 q = ld_pair(bm + 2 * (v[g] >> 5), pol_status);
-          cw[g] = q.y;
-          discm |= (~rotr32(q.x | q.y, v[g]) & 1u) << g;  // bit (v mod 32) of both, inverted
+        for (int g = 0; g < KX_GROUPS; ++g) {
+          const bool via_tag = (uint32_t)(v[g] - hub) < tag_span;
+          uint32_t r;
+          if (via_tag) r = (uint32_t)ld_cg_u8_hint(claim + claim_slot(P, v[g]), pol_status);
+          else r = ldg_status_u32(bm + (v[g] >> 5), pol_status);
+          needm |= (via_tag ? 0u : (~rotr32(r, v[g]) & 1u)) << g;
+          discm |= (via_tag ? (uint32_t)(r == 0u) : 0u) << g;
+        }
+      } else {
+#pragma unroll
+        for (int g = 0; g < KX_GROUPS; ++g) {
+          const uint32_t w = ldg_status_u32(bm + (v[g] >> 5), pol_status);
+          needm |= (~rotr32(w, v[g]) & 1u) << g;  // bit (v mod 32) of w, inverted
         }
       }
-      discover(v, xs, cw, discm, tag_mode);
+      const unsigned wneed = __reduce_or_sync(0xffffffffu, needm);
+      if (wneed) {  // warp-uniform skip
+#pragma unroll
+        for (int h = 0; h < KX_GROUPS; h += 4) {  // 4 tag loads in flight (register budget)
+          int cl[4];
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            cl[g] = ((needm >> (h + g)) & 1u) ? ld_cg_u8(claim + claim_slot(P, v[h + g])) : 1;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) discm |= (uint32_t)(cl[g] == 0) << (h + g);
+        }
+      }
+      discover(v, xs, discm);
     }
   };
   if (c->probe_tags) run(std::true_type{});
@@ -865,9 +860,9 @@ __device__ __forceinline__ void bm_publish(uint32_t *bm, bool keep, int v, int l
     if (lane - s >= run0) acc |= o;
   }
   const bool last = lane == 31 || ((heads >> (lane + 1)) & 1u);
-  if (keep && last) atomicOr(bm + 2 * wd, acc);
+  if (keep && last) atomicOr(bm + wd, acc);
 #else
-  if (keep) atomicOr(bm + 2 * (v >> 5), 1u << (v & 31));
+  if (keep) atomicOr(bm + (v >> 5), 1u << (v & 31));
 #endif
 }
 
@@ -1156,7 +1151,7 @@ __device__ void tiny_levels(const Params &P, Ctl *c, int32_t *sf, int32_t *srs, 
     const int pe = __shfl_sync(0xffffffffu, fex, u);
     const bool has = lane < e_l;
     const int v = has ? __ldg(col + pr + (lane - pe)) : 0;
-    const uint32_t w = __ldcg(P.bm + 2 * (v >> 5));  // published by atomicOr at L2
+    const uint32_t w = __ldcg(P.bm + (v >> 5));      // published by atomicOr at L2
     // issued together with the bitmap word; through L2 (ld.global.cg), never the read-only
     // path: k_small's block levels store Owner into the same 16-byte record in this launch
     const int4 vi = __ldcg(P.vinfo + v);
@@ -1171,7 +1166,7 @@ __device__ void tiny_levels(const Params &P, Ctl *c, int32_t *sf, int32_t *srs, 
     const unsigned km = ncand > 1 ? __ballot_sync(0xffffffffu, keep) : fm;
     if (keep) {
       P.lp[v] = make_int2(L + 1, px);                 // d[v] <- l, parent (Fig1 L18)
-      atomicOr(P.bm + 2 * (v >> 5), 1u << (v & 31));  // exact visited bit
+      atomicOr(P.bm + (v >> 5), 1u << (v & 31));      // exact visited bit
       mark_tag(P, v);
     }
     const int d = keep ? vi.y : 0;
@@ -1302,7 +1297,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
     uint32_t wv[KS_IPT];
 #pragma unroll
     for (int i = 0; i < KS_IPT; ++i)  // L1-bypassing: bits are published by atomicOr at L2 in
-      wv[i] = ev[i] >= 0 ? __ldcg(bm + 2 * (ev[i] >> 5)) : 0xffffffffu;  // earlier levels (H2)
+      wv[i] = ev[i] >= 0 ? __ldcg(bm + (ev[i] >> 5)) : 0xffffffffu;  // earlier levels (H2)
 #pragma unroll
     for (int i = 0; i < KS_IPT; ++i) {
       const int e = tid + i * KS_THREADS;
@@ -1342,7 +1337,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
       if (v >= 0 && vis[i].w == e) {
         kv[i] = vis[i].z; kr[i] = vis[i].x; kd[i] = vis[i].y;
         P.lp[v] = make_int2(L + 1, cpv[e]);         // d[v] <- l, parent (Fig1 L18)
-        atomicOr(P.bm + 2 * (v >> 5), 1u << (v & 31));  // exact visited bit (not discovery)
+        atomicOr(P.bm + (v >> 5), 1u << (v & 31));  // exact visited bit (not discovery)
         mark_tag(P, v);
       }
     }
@@ -1498,7 +1493,7 @@ __global__ void __cluster_dims__(KC_CL, 1, 1) __launch_bounds__(KC_THREADS, 1) k
     }
     uint32_t wv[KC_IPT];
 #pragma unroll
-    for (int i = 0; i < KC_IPT; ++i) wv[i] = ev[i] >= 0 ? __ldcg(bm + 2 * (ev[i] >> 5)) : 0xffffffffu;
+    for (int i = 0; i < KC_IPT; ++i) wv[i] = ev[i] >= 0 ? __ldcg(bm + (ev[i] >> 5)) : 0xffffffffu;
 #pragma unroll
     for (int i = 0; i < KC_IPT; ++i) {
       const int k = tid + i * KC_THREADS;
@@ -1542,7 +1537,7 @@ __global__ void __cluster_dims__(KC_CL, 1, 1) __launch_bounds__(KC_THREADS, 1) k
       if (v >= 0 && vis[i].w == lo + k) {
         kv[i] = vis[i].z; kr[i] = vis[i].x; kd[i] = vis[i].y;
         P.lp[v] = make_int2(L + 1, cpv[k]);          // d[v] <- l, parent (Fig1 L18)
-        atomicOr(P.bm + 2 * (v >> 5), 1u << (v & 31));  // exact visited bit (not discovery)
+        atomicOr(P.bm + (v >> 5), 1u << (v & 31));   // exact visited bit (not discovery)
         mark_tag(P, v);
         ++cnt;
         dsum += kd[i];
@@ -1706,7 +1701,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params 
     for (int i = 0; i < BU_W; ++i) {
       const int w = wb + i;
       const int v = (w << 5) + lane;
-      bw[i] = (w < w1) ? bm[2 * w] : 0xffffffffu;
+      bw[i] = (w < w1) ? bm[w] : 0xffffffffu;
       const bool act = w < w1 && v < nscan && !((bw[i] >> lane) & 1u);
       r0[i] = act ? __ldg(P.tro + v) : 0;
       r1[i] = act ? __ldg(P.tro + v + 1) : 0;
@@ -1749,7 +1744,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params 
       }
       const unsigned m = __ballot_sync(0xffffffffu, found);
       if (lane == 0 && w < w1) {
-        if (m) bm[2 * w] = bw[i] | m;  // this warp owns word w
+        if (m) bm[w] = bw[i] | m;  // this warp owns word w
         fbn[w] = m;
       }
       kept += __popc(m);
@@ -1833,7 +1828,7 @@ __global__ void k_finalize(Params P) {
        o += (long long)gridDim.x * blockDim.x) {
     const int i = P.o2n ? __ldg(P.o2n + o) : (int)o;
     int lv = -1, pa = -1;
-    if ((__ldg(P.bm + 2 * (i >> 5)) >> (i & 31)) & 1u) {
+    if ((__ldg(P.bm + (i >> 5)) >> (i & 31)) & 1u) {
       const int2 r = __ldg(P.lp + i);
       lv = r.x;
       pa = r.y;
