@@ -9,6 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libs3bfs.so")
+LIB_CHECK = os.path.join(HERE, "libs3bfs_check.so")  # S3BFS_CHECK=1: bounds-checked build
 SOURCES = [os.path.join(CSRC, "s3bfs.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "s3bfs_kernels.cuh"), os.path.join(ROOT, "include", "s3bfs.h")]
 

@@ -589,6 +589,7 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   P.do_beta = h->opt.do_beta != 0 ? h->opt.do_beta : 24;
   P.n_scan = n;
   P.nnz = nnz;
+  P.cand_cap = h->cand_cap;
   P.dist_size = dist_size;
   P.dist_rank = dist_rank;
   P.rec = dist_size > 1 ? (int4 *)(base + o_rec) : nullptr;

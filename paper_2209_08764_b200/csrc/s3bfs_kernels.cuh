@@ -41,6 +41,18 @@
 
 namespace s3bfs {
 
+// Bounds-checked build (S3BFS_CHECK=1, tests/check_suite.py): compute-sanitizer is not
+// available on the GPU pool, so every index the traversal kernels derive from data (frontier
+// slots, col positions, vertex ids, bitmap words, claim slots, candidate slots, shared-memory
+// slots) is checked against its buffer; a violation prints the site and traps.
+#if S3BFS_CHECK
+#define S3_CHK(i, lim) do { if (!((long long)(i) >= 0 && (long long)(i) < (long long)(lim))) { \
+    printf("S3BFS_CHECK %s:%d: %s = %lld not in [0, %lld)\n", __FILE__, __LINE__, #i,      \
+           (long long)(i), (long long)(lim)); __trap(); } } while (0)
+#else
+#define S3_CHK(i, lim) ((void)0)
+#endif
+
 // ---- compile-time geometry (the -D switches exist for scripts/kx_micro.py experiments) -----
 #ifndef S3BFS_KD_THREADS
 #define S3BFS_KD_THREADS 512
@@ -87,6 +99,12 @@ namespace s3bfs {
 #ifndef S3BFS_TAG_MODE_PCT
 #define S3BFS_TAG_MODE_PCT 80  // default of opts.tag_mode_pct
 #endif
+#ifndef S3BFS_KX_QUEUE
+#define S3BFS_KX_QUEUE 1  // k_explore: claim checks + discoveries via a warp-private queue
+#endif
+#ifndef S3BFS_CHECK
+#define S3BFS_CHECK 0  // 1: bounds-checked build (every traversal index checked; trap + message)
+#endif
 #ifndef S3BFS_BU_W
 #define S3BFS_BU_W 4
 #endif
@@ -111,6 +129,7 @@ constexpr int KD_WARPS = KD_THREADS / 32;
 constexpr int KD_SLACK = 64;                    // candidate-buffer slack per CTA
 constexpr int KX_GROUPS = S3BFS_KX_GROUPS;      // 32-edge groups per batch and warp
 constexpr int KC_GROUPS = S3BFS_KC_GROUPS;      // 32-candidate groups per k_compact round
+constexpr int KQ_CAP = 32 + 4 * 32;            // k_explore warp queue (< 32 kept + 4 groups)
 constexpr int KS_THREADS = 1024;                // k_small CTA size
 constexpr int KS_ECAP = 8192;                   // T0 maximum (edges per tier-0 level)
 constexpr int KS_NCAP = KS_ECAP;                // frontier capacity of tier 0 (kept <= e_l)
@@ -207,6 +226,7 @@ struct Params {
   int32_t *minrank;             // NEXT-4: per internal vertex, lowest rank keeping it (INT_MAX)
   unsigned long long *m_status; // NEXT-4: merge look-back words
   long long nnz;
+  long long cand_cap;           // candidate buffer entries (bounds-checked build)
   int32_t col_vec;              // col is 16-byte aligned: vectorised loads allowed
   int32_t use_graph;
   unsigned long long h_while, h_tier;  // cudaGraphConditionalHandle values (WHILE; SWITCH on
@@ -694,6 +714,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
           // interior batch (aligned, whole): no masking
 #pragma unroll
           for (int k = 0; k < KX_GROUPS / 4; ++k) {
+            S3_CHK(a0 + 4 * (lane + 32 * k) + 3, P.nnz);
             const int4 q = ldg_stream4(col + a0 + 4 * (lane + 32 * k), pol_stream);
             v[4 * k + 0] = q.x;
             v[4 * k + 1] = q.y;
@@ -704,6 +725,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
 #pragma unroll
           for (int k = 0; k < KX_GROUPS / 4; ++k) {
             const int i0 = a0 + 4 * (lane + 32 * k);
+            S3_CHK(i0 + 3, P.nnz);
             const int4 q = ldg_stream4(col + i0, pol_stream);  // in bounds: a0 + 256 <= nnz
             v[4 * k + 0] = (i0 + 0 >= start && i0 + 0 < lim_idx) ? q.x : vs;
             v[4 * k + 1] = (i0 + 1 >= start && i0 + 1 < lim_idx) ? q.y : vs;
@@ -716,6 +738,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
 #pragma unroll
         for (int g = 0; g < KX_GROUPS; ++g) {  // masked lanes re-load the batch's first edge
           const int my_e = e + g * 32 + lane;
+          S3_CHK(base + (my_e < bend ? my_e : e), P.nnz);
           const int t = ldg_stream(col + base + (my_e < bend ? my_e : e), pol_stream);
           v[g] = (my_e < bend) ? t : vs;
         }
@@ -741,6 +764,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
         xs[g >> 2] |= (uint32_t)j << (8 * (g & 3));
         const int pos = __shfl_sync(0xffffffffu, wb, j) + eg + lane;
         const bool ok = g * 32 < lb;
+        S3_CHK(ok ? pos : pfirst, P.nnz);
         const int t = ldg_stream(col + (ok ? pos : pfirst), pol_stream);  // unconditional
         v[g] = ok ? t : vs;
         r += __popc(m);
@@ -758,12 +782,14 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
         xs[g >> 2] |= (uint32_t)j << (8 * (g & 3));
         const int pos = __shfl_sync(0xffffffffu, wb, j) + my_e;
         const int pf = __shfl_sync(0xffffffffu, wb, j0) + e;
+        S3_CHK(my_e < bend ? pos : pf, P.nnz);
         const int t = ldg_stream(col + (my_e < bend ? pos : pf), pol_stream);
         v[g] = (my_e < bend) ? t : vs;
       }
     }
     return e_next;
   };
+#if !S3BFS_KX_QUEUE
   // Discovery of the batch's groups flagged in discm (Fig1 L18-L22): plain stores -- the tag,
   // {d, parent}, Owner = the candidate slot, and the candidate itself (benign race, R4).
   auto discover = [&](const int (&v)[KX_GROUPS], const uint32_t (&xs)[KX_GROUPS / 4],
@@ -787,6 +813,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
       wcount += __popc(m);
     }
   };
+#endif
   // The level's visited test (Fig1 L18 "if d[v] = infinity"), chosen per level by
   // decide_tier from the share of arcs that end at visited vertices:
   //  bitmap mode (most targets visited, the heavy levels): every target's visited bit (exact
@@ -795,6 +822,54 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   //    bit first, any other id only its discovery tag (nonzero once discovered) -- one probe
   //    instead of two for the arcs that reach new vertices.
   // Masked slots probe the sentinel (its bit is always set), so the tests are branch-free.
+#if S3BFS_KX_QUEUE
+  // Warp-private queue of the batch's rare items -- targets whose claim tag must be read
+  // (bitmap clear) or that were found undiscovered (tag mode) -- with their parents.  The
+  // items of many batches are resolved 32 at a time, one per lane (claim tag, then the
+  // discovery stores), instead of per group under predication: a heavy level flags about
+  // 2 % of its targets, which otherwise cost every lane the claim and discovery code of
+  // every flagged group (ncu: 45 % of the heavy level's instructions, profiles/).
+  __shared__ int2 s_q[KD_WARPS][KQ_CAP];
+  int2 *const q = s_q[warp];
+  int qn = 0;  // warp-uniform queue length
+  // resolve the first cnt (<= 32) items; the rest (qn - cnt) move to the front
+  auto flush = [&](int cnt) {
+    __syncwarp();
+    const bool valid = lane < cnt;
+    const int2 it = valid ? q[lane] : make_int2(0, 0);
+    const int v = it.x & 0x7fffffff;
+    const uint32_t cs = claim_slot(P, v);
+    int cl = 0;
+    if (valid && it.x < 0) cl = ld_cg_u8(claim + cs);  // Fig1 L18: already claimed this level?
+    const bool disc = valid && cl == 0;
+    const unsigned m = __ballot_sync(0xffffffffu, disc);
+    if (disc) {  // EXPLORE-VERTEX's discovery: plain stores, the benign race (R4)
+      const int slot = segbase + wcount + __popc(m & lanemask_lt());
+      S3_CHK(v, P.n);
+      S3_CHK(slot, (long long)(b * KD_WARPS + warp + 1) * wcap);
+      st_u8(claim + cs, tag);
+      st_weak_v2(lp + v, new_level, it.y);   // d[v] <- l, parent (Fig1 L18)
+      st_weak(owner_of(vinfo, v), slot);     // Owner[v] <- i (benign race)
+      cand[slot] = v;                        // Q[i].Enqueue(v)
+    }
+    wcount += __popc(m);
+    const int rest = qn - cnt;
+    for (int i = 0; i < rest; i += 32) {  // in order: chunk i never reads a slot written before
+      const int2 t = i + lane < rest ? q[cnt + i + lane] : make_int2(0, 0);
+      __syncwarp();
+      if (i + lane < rest) q[i + lane] = t;
+    }
+    __syncwarp();
+    qn = rest;
+  };
+  // enqueue group g's flagged lanes (chk: the claim tag decides)
+  auto enqueue = [&](int g, bool flag, bool chk, int vg, const uint32_t (&xs)[KX_GROUPS / 4]) {
+    const unsigned m = __ballot_sync(0xffffffffu, flag);
+    const int par = __shfl_sync(0xffffffffu, wx, (xs[g >> 2] >> (8 * (g & 3))) & 31u);
+    if (flag) q[qn + __popc(m & lanemask_lt())] = make_int2(vg | (chk ? (int)0x80000000u : 0), par);
+    qn += __popc(m);
+  };
+#endif
   auto run = [&](auto tag_mode) {
     constexpr bool TAGS = decltype(tag_mode)::value;
     int e = e_begin;
@@ -810,6 +885,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
 #pragma unroll
         for (int g = 0; g < KX_GROUPS; ++g) {
           const bool via_tag = (uint32_t)(v[g] - hub) < tag_span;
+          S3_CHK(v[g] >> 5, (P.v_sent >> 5) + 4);
           uint32_t r;
           if (via_tag) r = (uint32_t)ld_cg_u8_hint(claim + claim_slot(P, v[g]), pol_status);
           else r = ldg_status_u32(bm + (v[g] >> 5), pol_status);
@@ -819,10 +895,26 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
       } else {
 #pragma unroll
         for (int g = 0; g < KX_GROUPS; ++g) {
+          S3_CHK(v[g] >> 5, (P.v_sent >> 5) + 4);
           const uint32_t w = ldg_status_u32(bm + (v[g] >> 5), pol_status);
           needm |= (~rotr32(w, v[g]) & 1u) << g;  // bit (v mod 32) of w, inverted
         }
       }
+#if S3BFS_KX_QUEUE
+      const uint32_t itm = needm | discm;
+      const unsigned witm = __reduce_or_sync(0xffffffffu, itm);
+      if (witm) {  // warp-uniform skip; then only the flagged groups
+#pragma unroll
+        for (int g = 0; g < KX_GROUPS; ++g) {
+          if ((witm >> g) & 1u) enqueue(g, (itm >> g) & 1u, (needm >> g) & 1u, v[g], xs);
+          if ((g & 3) == 3) {  // after every 4 groups: at most 32 + 4 * 32 queued
+            while (qn >= 32) flush(32);
+          }
+        }
+      }
+    }
+  };
+#else
       const unsigned wneed = __reduce_or_sync(0xffffffffu, needm);
       if (wneed) {  // warp-uniform skip
 #pragma unroll
@@ -838,8 +930,13 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
       discover(v, xs, discm);
     }
   };
+#endif
   if (c->probe_tags) run(std::true_type{});
   else run(std::false_type{});
+#if S3BFS_KX_QUEUE
+  if (qn > 0) flush(qn);  // warp-uniform: the slice's remaining items
+#endif
+  S3_CHK(segbase + wcount, P.cand_cap);
   if (lane == 0) P.wcnt[b * KD_WARPS + warp] = wcount;
 }
 
@@ -905,7 +1002,9 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
 #pragma unroll
     for (int g = 0; g < KC_GROUPS; ++g) {
       const int k = k0 + g * 32 + lane;
+      if (k < cnt) S3_CHK(seg + k, P.cand_cap);
       v[g] = (k < cnt) ? cand[seg + k] : -1;
+      if (k < cnt) S3_CHK(v[g], P.n);
     }
     int4 vi[KC_GROUPS];  // {row start, degree, caller id, Owner}: one sector per candidate
 #pragma unroll
@@ -920,6 +1019,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       if (keep) {
         const int q = seg + kept + __popc(m & lanemask_lt());
+        S3_CHK(q, P.cand_cap);
         cand[q] = dist ? v[g] : vi[g].z;  // NEXT-4 keeps the internal id for the record
         crd[q] = make_int2(vi[g].x, d);
       }
@@ -971,6 +1071,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
       if (dist) {  // NEXT-4: this rank's kept vertex, for the cross-rank merge
         P.rec[koff + k] = make_int4(v, P.lp[v].y, r0, d);
       } else {
+        S3_CHK(koff + k, P.n);
         fn[koff + k] = v;
         frsn[koff + k] = r0;
         fexn[koff + k] = doff + inc - d;
@@ -1150,7 +1251,9 @@ __device__ void tiny_levels(const Params &P, Ctl *c, int32_t *sf, int32_t *srs, 
     const int pr = __shfl_sync(0xffffffffu, frs, u);
     const int pe = __shfl_sync(0xffffffffu, fex, u);
     const bool has = lane < e_l;
+    if (has) S3_CHK(pr + (lane - pe), P.nnz);
     const int v = has ? __ldg(col + pr + (lane - pe)) : 0;
+    S3_CHK(v, P.n);
     const uint32_t w = __ldcg(P.bm + (v >> 5));      // published by atomicOr at L2
     // issued together with the bitmap word; through L2 (ld.global.cg), never the read-only
     // path: k_small's block levels store Owner into the same 16-byte record in this launch
@@ -1290,8 +1393,11 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
       ev[i] = -1;
       ux[i] = 0;
       if (e < e_l) {
+        S3_CHK(lo[i], n_l);
         ux[i] = sf[lo[i]];
+        S3_CHK(srs[lo[i]] + (e - sex[lo[i]]), P.nnz);
         ev[i] = __ldg(col + srs[lo[i]] + (e - sex[lo[i]]));
+        S3_CHK(ev[i], P.n);
       }
     }
     uint32_t wv[KS_IPT];
@@ -1309,6 +1415,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
           w = v;
           ++ncand;
         }
+        S3_CHK(e, KS_ECAP);
         cv[e] = w;
         cpv[e] = ux[i];
       }
@@ -1384,6 +1491,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
 #pragma unroll
     for (int i = 0; i < KS_IPT; ++i) {
       if (kv[i] >= 0) {
+        S3_CHK(kpos, KS_NCAP);
         sf[kpos] = kv[i];
         srs[kpos] = kr[i];
         sex[kpos] = dpos;
@@ -1487,8 +1595,11 @@ __global__ void __cluster_dims__(KC_CL, 1, 1) __launch_bounds__(KC_THREADS, 1) k
           const int mid = (a + z) >> 1;
           if (sex[mid] <= e) a = mid; else z = mid;
         }
+        S3_CHK(a, n_l);
         ux[i] = sf[a];
+        S3_CHK(srs[a] + (e - sex[a]), P.nnz);
         ev[i] = __ldg(col + srs[a] + (e - sex[a]));
+        S3_CHK(ev[i], P.n);
       }
     }
     uint32_t wv[KC_IPT];
@@ -1505,6 +1616,7 @@ __global__ void __cluster_dims__(KC_CL, 1, 1) __launch_bounds__(KC_THREADS, 1) k
           w = v;
           ++ncand;
         }
+        S3_CHK(k, KC_ECTA);
         cv[k] = w;
         cpv[k] = ux[i];
       }
@@ -1586,6 +1698,7 @@ __global__ void __cluster_dims__(KC_CL, 1, 1) __launch_bounds__(KC_THREADS, 1) k
 #pragma unroll
     for (int i = 0; i < KC_IPT; ++i) {
       if (kv[i] >= 0) {
+        S3_CHK(kpos, stay ? KC_FCAP : P.n);
         if (stay) {  // the next level stays here: write every CTA's frontier copy
 #pragma unroll
           for (int r = 0; r < KC_CL; ++r) {
@@ -1655,7 +1768,9 @@ __global__ void k_fb_set(Params P) {
   for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < n_l;
        u += (long long)gridDim.x * blockDim.x) {
     const int o = f[u];
+    S3_CHK(o, P.n);
     const int i = P.o2n ? __ldg(P.o2n + o) : o;
+    S3_CHK(i, P.n);
     atomicOr(fb + (i >> 5), 1u << (i & 31));  // frontier membership (not the discovery path)
   }
 }
@@ -1719,6 +1834,15 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params 
 #pragma unroll
         for (int j = 0; j < BU_P; ++j)
           u[i][j] = (r0[i] + j < r1[i]) ? __ldg(P.tcol + r0[i] + j) : -1;
+#if S3BFS_CHECK
+#pragma unroll
+      for (int i = 0; i < BU_W; ++i)
+#pragma unroll
+        for (int j = 0; j < BU_P; ++j) {
+          if (r0[i] + j < r1[i]) S3_CHK(r0[i] + j, P.nnz);
+          if (u[i][j] >= 0) S3_CHK(u[i][j], P.n);
+        }
+#endif
       uint32_t fw[BU_W][BU_P];
 #pragma unroll
       for (int i = 0; i < BU_W; ++i)
@@ -1785,6 +1909,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params 
     const int inc = warp_incl_scan(d);
     const int pos = koff + __popc(m & lanemask_lt());
     if (mine) {
+      S3_CHK(pos, P.n);
       P.f[nxt][pos] = vi.z;
       P.frs[nxt][pos] = vi.x;
       P.fex[nxt][pos] = doff + inc - d;
@@ -1827,6 +1952,7 @@ __global__ void k_finalize(Params P) {
   for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < n;
        o += (long long)gridDim.x * blockDim.x) {
     const int i = P.o2n ? __ldg(P.o2n + o) : (int)o;
+    S3_CHK(i, P.n);
     int lv = -1, pa = -1;
     if ((__ldg(P.bm + (i >> 5)) >> (i & 31)) & 1u) {
       const int2 r = __ldg(P.lp + i);

@@ -14,7 +14,9 @@ import numpy as np
 
 from . import build as _build
 
-LIB_PATH = _build.LIB
+# S3BFS_LIB selects another build of the same sources (the bounds-checked build of
+# tests/check_suite.py); the default is the in-tree libs3bfs.so
+LIB_PATH = os.environ.get("S3BFS_LIB", _build.LIB)
 _lib = None
 
 S3BFS_OK = 0

@@ -354,3 +354,20 @@ def test_stats_off(kw):
         for s in srcs:
             check_traversal(g, bfs, s, stats=False)
         bfs.close()
+
+
+def test_bounds_checked_build():
+    """Memory safety without compute-sanitizer (closed on the GPU pool): the S3BFS_CHECK=1
+    build of the same sources checks every data-derived index of the traversal kernels and
+    traps on a violation; tests/check_suite.py runs the tiny suite + R-MAT 14/16 under every
+    setting of this file through it (and against the oracle) in a fresh process."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "paper_2209_08764_b200", "libs3bfs_check.so")
+    assert os.path.exists(lib), "run __graft_entry__.build() (it builds the checked library)"
+    env = dict(os.environ, S3BFS_LIB=lib)
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "check_suite.py"), "--quick"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "no bounds violation" in r.stdout, (r.stdout[-3000:], r.stderr[-3000:])
