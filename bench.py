@@ -575,9 +575,29 @@ def main():
             line["next4_one_traversal_over_ranks"] = next4
         print(json.dumps(line), flush=True)
         if args.detail_out:
+            def d8(stt):
+                # per level, work vs gap (globaltimer stamps of the captured
+                # loop; t_begin = the previous level's end).  Tier 1: gap = until k_explore's
+                # CTA 0 starts, work = k_explore + k_compact; tiers 0 / cluster run inside one
+                # launch, so their whole span is work (gap 0 except the first level).
+                out = []
+                for r in stt:
+                    t0_, t1_ = int(r["t_begin_ns"]), int(r["t_end_ns"])
+                    xb, xe = int(r["t_explore_begin_ns"]), int(r["t_explore_end_ns"])
+                    rec = {"l": int(r["level"]), "n_l": int(r["n_l"]), "e_l": int(r["e_l"]),
+                           "tier": int(r["tier"]), "grid": int(r["grid"]),
+                           "candidates": int(r["candidates"]), "kept": int(r["kept"])}
+                    if int(r["tier"]) in (1, 3) and xb > 0:
+                        rec.update(gap_us=(xb - t0_) / 1e3, work_us=(t1_ - xb) / 1e3,
+                                   explore_us=(xe - xb) / 1e3 if xe > xb else None,
+                                   compact_us=(t1_ - xe) / 1e3 if xe > xb else None)
+                    else:
+                        rec.update(gap_us=0.0, work_us=(t1_ - t0_) / 1e3)
+                    out.append(rec)
+                return out
             detail["per_source"] = {int(s): {"m_c": p["m_c"], "levels": p["levels"],
                                              "launches": p["launches"],
-                                             "per_level": p["stats"].tolist()}
+                                             "per_level": d8(p["stats"])}
                                     for s, p in per.items()}
             detail["step_ms"] = step_ms
             detail["per_step_gteps"] = per_step_gteps

@@ -129,7 +129,7 @@ constexpr int KD_WARPS = KD_THREADS / 32;
 constexpr int KD_SLACK = 64;                    // candidate-buffer slack per CTA
 constexpr int KX_GROUPS = S3BFS_KX_GROUPS;      // 32-edge groups per batch and warp
 constexpr int KC_GROUPS = S3BFS_KC_GROUPS;      // 32-candidate groups per k_compact round
-constexpr int KQ_CAP = 32 + 4 * 32;            // k_explore warp queue (< 32 kept + 4 groups)
+constexpr int KQ_CAP = 32 + 2 * 32;            // k_explore warp queue (< 32 kept + 2 groups)
 constexpr int KS_THREADS = 1024;                // k_small CTA size
 constexpr int KS_ECAP = 8192;                   // T0 maximum (edges per tier-0 level)
 constexpr int KS_NCAP = KS_ECAP;                // frontier capacity of tier 0 (kept <= e_l)
@@ -907,7 +907,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
 #pragma unroll
         for (int g = 0; g < KX_GROUPS; ++g) {
           if ((witm >> g) & 1u) enqueue(g, (itm >> g) & 1u, (needm >> g) & 1u, v[g], xs);
-          if ((g & 3) == 3) {  // after every 4 groups: at most 32 + 4 * 32 queued
+          if ((g & 1) == 1) {  // every 2 groups: at most 32 + 2 * 32 queued
             while (qn >= 32) flush(32);
           }
         }
