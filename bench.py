@@ -53,7 +53,8 @@ def parse():
     ap.add_argument("--grain", type=int, default=0)
     ap.add_argument("--next4", action="store_true",
                     help="multi-GPU nodes: also time ONE traversal split over all ranks (NEXT-4, "
-                         "NCCL all-gathers per level; strong scaling), reported beside the line")
+                         "1-D vertex partition, peer-memory exchange; strong scaling), reported "
+                         "beside the line")
     ap.add_argument("--no-next3", action="store_true",
                     help="skip the extra direction-optimising (NEXT-3) measurement")
     ap.add_argument("--direction", type=int, default=0,
@@ -441,13 +442,17 @@ def main():
     if args.next4 and world > 1:
         import paper_2209_08764_b200.dist as pdist
         dr = pdist.DistRank(ro, col, rank, world)
+        pdist.connect([dr], dist.group.WORLD)  # exchange records; peers opened by CUDA IPC
         n4_steps = min(args.steps, 16)
-        n4_ok = True
+        checked = [s for s in srcs[: args.oracle_sources] if s in oracle_levels]
+        n4_ok = True if checked else None
         for s in srcs[: args.oracle_sources]:  # every rank traverses (collectives); rank 0 checks
             (lv4, _), = pdist.traverse([dr], s, group=dist.group.WORLD)
             torch.cuda.synchronize()
             if s in oracle_levels:
                 n4_ok &= bool(np.array_equal(lv4.cpu().numpy(), oracle_levels[s]))
+        # m_c / 2 per source from the single-GPU traversals (outside the timed region)
+        mc_half = {s: p["m_c"] // 2 for s, p in per.items()}
         for k in range(args.warmup):
             pdist.traverse([dr], srcs[k % len(srcs)], group=dist.group.WORLD)
         torch.cuda.synchronize()
@@ -456,16 +461,18 @@ def main():
         a.record(stream)
         n4_edges = 0
         for k in range(n4_steps):  # every rank runs the SAME source (one traversal)
-            (lv4, _), = pdist.traverse([dr], srcs[k % len(srcs)], group=dist.group.WORLD)
-            n4_edges += int(deg[lv4 >= 0].sum().item()) // 2
+            pdist.traverse([dr], srcs[k % len(srcs)], group=dist.group.WORLD)
+            n4_edges += mc_half[srcs[k % len(srcs)]]
         b.record(stream)
         torch.cuda.synchronize()
         t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dr.close()
-        next4 = {"what": "SURVEY NEXT-4: one traversal over all ranks (replicated graph, each "
-                         "level's edges split over ranks, NCCL all-gather of kept vertices per "
-                         "level, cross-rank merge kernels); same sources, no L2 flush",
+        next4 = {"what": "SURVEY NEXT-4: one traversal over all ranks, 1-D vertex partition "
+                         "(candidates stored into the owners' receive segments by the "
+                         "exploration kernel over NVLink peer memory, owner-side Owner check, "
+                         "replicated bitmap words published by peer stores; NCCL one-element "
+                         "all-reduces order the phases); same sources, no L2 flush",
                  "value": n4_edges / (float(t.item()) / 1e3) / 1e9, "unit": "GTEPS",
                  "ranks": world, "scaling": "strong",
                  "ms_per_traversal": float(t.item()) / n4_steps,

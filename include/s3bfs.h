@@ -80,11 +80,11 @@ typedef struct {
                               top-down when n_l * beta < n (Beamer); 0 = top-down S3BFS only */
   int32_t do_alpha;        /* 0 -> 14 */
   int32_t do_beta;         /* 0 -> 24; < 0 -> never switch back */
-  int32_t dist_size;       /* NEXT-4: 0/1 single GPU; G > 1: this handle is rank dist_rank of
-                              G ranks that each hold the whole graph and explore 1/G of every
-                              level's edges (replicated-graph split); driven by
-                              the s3bfs_dist_* calls below, not s3bfs_run.  Needs loop_mode 2
-                              semantics (set implicitly), tier 0 off (implicit), direction 0 */
+  int32_t dist_size;       /* NEXT-4: 0/1 single GPU; G in [2, 8]: this handle is rank dist_rank
+                              of a 1-D vertex partition over G ranks: it owns the
+                              internal ids v with (v / 32) mod G == dist_rank, their CSR rows and
+                              their state; driven by the s3bfs_dist_* calls below, not s3bfs_run.
+                              Every level runs on tier 1; direction must be 0; no clones */
   int32_t dist_rank;       /* NEXT-4: 0 <= dist_rank < dist_size */
   int32_t cluster_max_edges; /* cluster tier (one 8-CTA thread-block cluster running
                               consecutive levels with T0 < e_l <= this and n_l <= 8192 in one
@@ -181,41 +181,68 @@ s3bfs_status s3bfs_get_kernel_times(s3bfs_handle h, s3bfs_kernel_times *out);
  * out[1] first k_dispatch, out[2] k_small start (0 when not reached).  Synchronises. */
 s3bfs_status s3bfs_debug_timeline(s3bfs_handle h, uint64_t out[4]);
 
-/* ---- NEXT-4: one traversal over G ranks (replicated graph) -------------------
- * Every rank holds the same frontier; rank r explores the level's global edges
- * [r*e_l/G, (r+1)*e_l/G) with the single-GPU kernels (c)(d), deduplicates its discoveries by
- * Owner (e), and leaves its kept vertices as records {internal id, parent (caller id), row
- * start, degree}.  The caller all-gathers the records (the exchange step, e.g. NCCL over
- * NVLink; plumbing outside the library) and hands them to s3bfs_dist_merge, which keeps every
- * vertex once (from the lowest rank that kept it) and builds the identical next frontier on
- * every rank.  Per traversal:
- *   s3bfs_dist_begin; loop { s3bfs_dist_expand -> done? ; all-gather ; s3bfs_dist_merge };
- *   s3bfs_dist_end.
+/* ---- NEXT-4: one traversal over G ranks, 1-D vertex partition -------
+ * Rank r (a handle created with dist_size = G, dist_rank = r, typically one per GPU of a node)
+ * owns the internal ids v with (v / 32) mod G == r (block-cyclic 32-id blocks of the degree
+ * order: one visited-bitmap word per owner, the hubs spread over the ranks), their CSR rows
+ * (a local CSR built at create from the caller's global CSR) and their state (d, parent,
+ * Owner).  The visited bitmap is replicated.  Per level, on every rank:
+ *   s3bfs_dist_explore   (c)(d) over the local frontier; a target with a clear visited bit goes
+ *                        as {v, parent} straight into v's owner's receive segment for this warp
+ *                        (stores into the peer's memory over NVLink / NVSwitch: the exchange
+ *                        is fused into the exploration kernel, no collective carries data)
+ *   -- every rank's explore complete (a stream-ordered barrier across ranks) --
+ *   s3bfs_dist_dedup     (e)(a)(b) on the owner: Owner[v] <- slot for every received
+ *                        candidate, keep iff Owner[v] == slot (the benign race stays on one
+ *                        GPU), d/parent, the next local frontier by the look-back scan; the
+ *                        owner's updated bitmap words and its {n_next, e_next} into every peer
+ *   -- every rank's dedup complete --
+ *   s3bfs_dist_advance   the level's totals over all ranks (Fig1 L9): *done = 1 ends the loop
+ * then s3bfs_dist_end writes level/parent of the rank's own vertices (caller ids); the other
+ * entries keep the -1 s3bfs_dist_begin wrote, so an element-wise max over the ranks' arrays
+ * is the full answer.  Connection: every rank exports its exchange record, the records are
+ * shared (any host channel, e.g. torch.distributed), and every rank connects to all of them:
+ * use_ipc = 1 opens peers' allocations through CUDA IPC (one process per GPU); use_ipc = 0
+ * takes the addresses as they are (several ranks in one process, e.g. a one-GPU loopback).
  * All calls need a handle created with dist_size > 1 (else UNSUPPORTED). */
+typedef struct {
+  uint64_t base;            /* the rank's exchange allocation (device address in its process) */
+  uint64_t recv, rcnt, rmeta, rtot, bm;  /* arrays inside it (same layout on every rank) */
+  uint8_t ipc[64];          /* cudaIpcMemHandle_t of the allocation (valid if ipc_valid) */
+  int32_t ipc_valid;
+  int32_t rank, size;
+  int32_t pad;
+} s3bfs_dist_peer;
 
-/* Start a traversal from `source` (same on every rank); level/parent as in s3bfs_run
- * (written by s3bfs_dist_end).  Enqueued on `stream`. */
+/* This rank's exchange record (host struct, caller-owned). */
+s3bfs_status s3bfs_dist_export(s3bfs_handle h, s3bfs_dist_peer *out);
+
+/* peers: `count` = G records in rank order (this rank's included).  Call once after create
+ * (again to reconnect).  INVALID_ARGUMENT for a wrong count/order; CUDA if an IPC open fails. */
+s3bfs_status s3bfs_dist_connect(s3bfs_handle h, const s3bfs_dist_peer *peers, int32_t count,
+                                int32_t use_ipc);
+
+/* Start a traversal from `source` (caller id, the same on every rank).  level/parent: device,
+ * n int32 each, caller-owned; set to -1 here (enqueued on `stream`) and written for this
+ * rank's vertices by s3bfs_dist_end. */
 s3bfs_status s3bfs_dist_begin(s3bfs_handle h, int32_t source, int32_t *level, int32_t *parent,
                               s3bfs_stream_t stream);
 
-/* Expand this rank's slice of the current level.  Synchronises `stream`.  *done = 1 when the
- * traversal has no further level (then *n_local = 0 and nothing ran); otherwise *n_local =
- * this rank's record count, readable through s3bfs_dist_records. */
-s3bfs_status s3bfs_dist_expand(s3bfs_handle h, s3bfs_stream_t stream, int32_t *n_local,
-                               int32_t *done);
+/* Explore this rank's part of the current level (enqueued on `stream`). */
+s3bfs_status s3bfs_dist_explore(s3bfs_handle h, s3bfs_stream_t stream);
 
-/* Copy this rank's first `count` records (count <= the last *n_local) into dst: device,
- * int32 x 4 per record, caller-owned (e.g. the padded send buffer of the all-gather).
- * Enqueued on `stream`. */
-s3bfs_status s3bfs_dist_records(s3bfs_handle h, void *dst, int32_t count, s3bfs_stream_t stream);
+/* Deduplicate the candidates received this level; publish bitmap words and totals (enqueued
+ * on `stream`; every rank's explore of this level must have completed before it runs). */
+s3bfs_status s3bfs_dist_dedup(s3bfs_handle h, s3bfs_stream_t stream);
 
-/* Merge the all-gathered records: all = device int32 x 4 [G * stride], rank r's n_r records at
- * [r * stride, r * stride + n_r); counts = HOST int32[G] (n_r <= stride).  Advances the level.
- * Enqueued on `stream` (counts are copied before return). */
-s3bfs_status s3bfs_dist_merge(s3bfs_handle h, const void *all, const int32_t *counts,
-                              int32_t stride, s3bfs_stream_t stream);
+/* Advance the level from the totals of all ranks (every rank's dedup of this level must have
+ * completed).  With done / n_next non-NULL it synchronises `stream` and returns *done = 1 when
+ * no rank has a next frontier, *n_next = the next frontier's size over all ranks. */
+s3bfs_status s3bfs_dist_advance(s3bfs_handle h, s3bfs_stream_t stream, int32_t *done,
+                                int64_t *n_next);
 
-/* Write level/parent (caller ids) for the traversal begun by s3bfs_dist_begin. */
+/* Write level/parent (caller ids) of this rank's vertices for the traversal begun by
+ * s3bfs_dist_begin (enqueued on `stream`). */
 s3bfs_status s3bfs_dist_end(s3bfs_handle h, s3bfs_stream_t stream);
 
 /* ---- test-only entry points (same kernels the traversal uses) ------------------------ */

@@ -27,6 +27,7 @@
 #include <string>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 
 #include "s3bfs_kernels.cuh"
@@ -68,7 +69,13 @@ struct s3bfs_ctx {
   bool time_kernels = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   s3bfs_kernel_times kt{};
-  int32_t *d_counts = nullptr;  // NEXT-4: per-rank record counts (device copy)
+  // NEXT-4 (dist_size > 1): the rank's local CSR, the exchange allocation peers write into,
+  // and the peers' exchange allocations opened through CUDA IPC (other processes)
+  void *dgraph = nullptr;
+  void *xws = nullptr;
+  size_t xws_bytes = 0;
+  void *ipc_open[DIST_MAX] = {};
+  int32_t *d_level = nullptr, *d_parent = nullptr;
   std::string err;
 };
 
@@ -187,6 +194,83 @@ s3bfs_status build_reordered(s3bfs_ctx *h, cudaStream_t st) {
   h->P.o2n = o2n;
   h->P.n_scan = h_nz;  // internal ids >= h_nz have degree 0: bottom-up never scans them
   h->ro_int = ro2;
+  return S3BFS_OK;
+}
+
+// NEXT-4 (dist_size > 1): this rank's local CSR (the rows of its block-cyclic vertex slots,
+// targets in global internal ids) and vertex records, and the exchange allocation its peers
+// write into (receive segments, segment counts, per-source {wcap, p_l} and totals, and the
+// replicated visited bitmap).  Every rank computes the same receive layout (block offsets
+// from the arcs each rank owns), so a sender writes at the same offsets on every peer.
+s3bfs_status build_dist(s3bfs_ctx *h, cudaStream_t st, int nloc) {
+  Params &P = h->P;
+  const int G = P.dist_size, r = P.dist_rank, n = h->n;
+  P.nloc = nloc;
+  P.tag_pct = -1;  // the visited test goes through the replicated bitmap: a rank's discovery
+  P.hub = n;       // tags know only its own sends, never another rank's vertices
+  const int32_t *ro = h->ro_int, *col = P.col;
+  const int grid = h->num_sms * 8;
+  AsyncTmp cnt_b(st), deg_b(st), tmp_b(st);
+  CK(h, cnt_b.alloc(8 * DIST_MAX));
+  unsigned long long *d_cnt = cnt_b.as<unsigned long long>();
+  CK(h, cudaMemsetAsync(d_cnt, 0, 8 * DIST_MAX, st));
+  k_dist_rank_arcs<<<grid, 256, 0, st>>>(ro, n, G, d_cnt);
+  unsigned long long h_cnt[DIST_MAX] = {};
+  CK(h, cudaMemcpyAsync(h_cnt, d_cnt, 8 * DIST_MAX, cudaMemcpyDeviceToHost, st));
+  CK(h, cudaStreamSynchronize(st));
+  const long long nnz_l = (long long)h_cnt[r];
+  // local CSR: degrees of the local slots, their exclusive scan, the copied rows
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return o; };
+  const size_t o_ro = take((size_t)(nloc + 1) * 4), o_col = take((size_t)nnz_l * 4 + 16);
+  CK(h, cudaMalloc(&h->dgraph, off));
+  int32_t *ro_l = (int32_t *)((char *)h->dgraph + o_ro);
+  int32_t *col_l = (int32_t *)((char *)h->dgraph + o_col);
+  CK(h, deg_b.alloc((size_t)(nloc + 1) * 4));
+  int32_t *deg_l = deg_b.as<int32_t>();
+  CK(h, cudaMemsetAsync(deg_l + nloc, 0, 4, st));
+  k_dist_local_deg<<<grid, 256, 0, st>>>(P, ro, deg_l);
+  size_t tmp_bytes = 0;
+  CK(h, cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, deg_l, ro_l, nloc + 1, st));
+  CK(h, tmp_b.alloc(tmp_bytes));
+  CK(h, cub::DeviceScan::ExclusiveSum(tmp_b.p, tmp_bytes, deg_l, ro_l, nloc + 1, st));
+  k_dist_copy_rows<<<grid, 256, 0, st>>>(P, ro, col, ro_l, col_l);
+  k_dist_build_vinfo<<<grid, 256, 0, st>>>(P, ro_l, P.n2o, P.vinfo);
+  CK(h, cudaGetLastError());
+  P.col = col_l;
+  P.nnz = nnz_l;
+  // receive layout (identical on every rank) and the exchange allocation
+  long long ofs = 0;
+  for (int t = 0; t < G; ++t) {
+    P.rofs[t] = (int32_t)ofs;
+    ofs += (long long)h_cnt[t] + (long long)P.p_max * (KD_WARPS + 1 + KD_SLACK) + 64;
+    if (ofs >= INT32_MAX)
+      return fail(h, S3BFS_ERR_UNSUPPORTED, "NEXT-4 receive buffer exceeds int32 slots");
+  }
+  P.rofs[G] = (int32_t)ofs;
+  const size_t bm_bytes = ((size_t)n + 127) / 128 * 16;
+  const long long nwmax = (long long)P.p_max * KD_WARPS;
+  off = 0;
+  const size_t o_recv = take((size_t)ofs * 8), o_rcnt = take((size_t)G * nwmax * 4);
+  const size_t o_rmeta = take((size_t)G * 8), o_rtot = take((size_t)G * 8);
+  const size_t o_bm = take(bm_bytes + 16);
+  h->xws_bytes = off;
+  CK(h, cudaMalloc(&h->xws, off));
+  char *x = (char *)h->xws;
+  CK(h, cudaMemsetAsync(x + o_rcnt, 0, off - o_rcnt, st));
+  P.recv = (int2 *)(x + o_recv);
+  P.rcnt = (int32_t *)(x + o_rcnt);
+  P.rmeta = (int2 *)(x + o_rmeta);
+  P.rtot = (int2 *)(x + o_rtot);
+  P.bm = (uint32_t *)(x + o_bm);
+  for (int d = 0; d < DIST_MAX; ++d) {  // until s3bfs_dist_connect: every rank is this one
+    P.p_recv[d] = P.recv;
+    P.p_rcnt[d] = P.rcnt;
+    P.p_rmeta[d] = P.rmeta;
+    P.p_rtot[d] = P.rtot;
+    P.p_bm[d] = P.bm;
+  }
+  CK(h, cudaStreamSynchronize(st));
   return S3BFS_OK;
 }
 
@@ -488,6 +572,9 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   const int dist_size = h->opt.dist_size > 1 ? h->opt.dist_size : 1;
   const int dist_rank = dist_size > 1 ? h->opt.dist_rank : 0;
   if (dist_size > 1) {  // NEXT-4: host-driven per-level protocol, every level on tier 1
+    if (dist_size > DIST_MAX)
+      return bail(fail(h, S3BFS_ERR_UNSUPPORTED, "dist_size > 8 (ranks of one node)"));
+    if (share) return bail(fail(h, S3BFS_ERR_UNSUPPORTED, "clones of a dist_size > 1 handle"));
     if (dist_rank < 0 || dist_rank >= dist_size)
       return bail(fail(h, S3BFS_ERR_INVALID_ARGUMENT, "dist_rank not in [0, dist_size)"));
     if (h->opt.direction == 1)
@@ -503,11 +590,15 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   if (h->cand_cap >= INT32_MAX)
     return bail(fail(h, S3BFS_ERR_UNSUPPORTED, "nnz too large for int32 candidate slots"));
   const int stats_cap = n + 1 < (1 << 16) ? n + 1 : (1 << 16);
-  const size_t nb = (size_t)n * 4, nb1 = (size_t)(n + 1) * 4;
+  // vertex-indexed arrays: n entries, or this rank's local slots with dist_size > 1
+  const long long nblk = ((long long)n + 31) / 32;
+  const long long nloc = dist_size > 1 ? (nblk + dist_size - 1) / dist_size * 32 : n;
+  const long long nv = (nloc > n ? nloc : n) + 32;
+  const size_t nb = (size_t)nv * 4, nb1 = (size_t)(nv + 1) * 4;
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return o; };
-  const size_t o_vinfo = take((size_t)n * 16);
-  const size_t o_lp = take((size_t)n * 8);
+  const size_t o_vinfo = take((size_t)nv * 16);
+  const size_t o_lp = take((size_t)nv * 8);
   size_t o_f[2], o_frs[2], o_fex[2];
   for (int i = 0; i < 2; ++i) { o_f[i] = take(nb); o_frs[i] = take(nb); o_fex[i] = take(nb1 + 16); }
   const size_t o_cand = take((size_t)h->cand_cap * 4);
@@ -521,7 +612,7 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   const size_t o_claim = take(claim_n);
   const size_t o_fb0 = take(bm_bytes), o_fb1 = take(bm_bytes);
   const size_t o_wcnt = take((size_t)p_max * KD_WARPS * 4);
-  const size_t o_status = take((size_t)p_max * 8);
+  const size_t o_status = take((size_t)p_max * (dist_size > 1 ? dist_size : 1) * 8 + 8);
   // NEXT-3 bottom-up tiles: width = the power of two >= words / (tiles-per-CTA x P_max), at
   // least 64 words (one BU_W-word round for each of a CTA's 16 warps)
   const long long bu_words = (((long long)n + 127) >> 7) << 2;
@@ -531,12 +622,8 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   const size_t o_bustatus = take((size_t)(bu_tiles + 1) * 8);
   const size_t o_ctl = take(sizeof(Ctl));
   const size_t o_stats = take((size_t)stats_cap * sizeof(s3bfs_level_stat));
-  // NEXT-4 (dist_size > 1 only): records, per-vertex lowest keeping rank, merge look-back
-  const long long m_tiles = dist_size > 1 ? ((long long)dist_size * n + MG_TILE - 1) / MG_TILE + 1 : 0;
-  const size_t o_rec = take(dist_size > 1 ? (size_t)n * 16 : 0);
-  const size_t o_minrank = take(dist_size > 1 ? (size_t)n * 4 : 0);
-  const size_t o_mstatus = take((size_t)m_tiles * 8);
-  const size_t o_dcounts = take((size_t)dist_size * 4);
+  // NEXT-4 (dist_size > 1 only): internal ids of the kept vertices (publication of bitmap words)
+  const size_t o_kv = take(dist_size > 1 ? (size_t)nv * 4 : 0);
   h->ws_bytes = off;
   if ((e = cudaMalloc(&h->ws, h->ws_bytes)) != cudaSuccess) return bail(cuda_fail(h, e, "cudaMalloc(workspace)"));
   char *base = (char *)h->ws;
@@ -592,12 +679,8 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   P.cand_cap = h->cand_cap;
   P.dist_size = dist_size;
   P.dist_rank = dist_rank;
-  P.rec = dist_size > 1 ? (int4 *)(base + o_rec) : nullptr;
-  P.minrank = dist_size > 1 ? (int32_t *)(base + o_minrank) : nullptr;
-  P.m_status = dist_size > 1 ? (unsigned long long *)(base + o_mstatus) : nullptr;
-  h->d_counts = (int32_t *)(base + o_dcounts);
-  if (dist_size > 1 && (e = cudaMemsetAsync(P.minrank, 0x7f, (size_t)n * 4, stream)) != cudaSuccess)
-    return bail(cuda_fail(h, e, "memset(minrank)"));
+  P.kv = dist_size > 1 ? (int32_t *)(base + o_kv) : nullptr;
+  P.nloc = n;
   if (share) {  // a clone: the prepared graph is the source handle's; vertex records copied
     P.col = share->P.col;
     P.n2o = share->P.n2o;
@@ -637,6 +720,10 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
     if ((e = cudaGetLastError()) != cudaSuccess) return bail(cuda_fail(h, e, "k_build_vinfo"));
     h->ro_int = row_offsets;
   }
+  if (dist_size > 1) {
+    s3bfs_status ds = build_dist(h, stream, (int)nloc);
+    if (ds != S3BFS_OK) return bail(ds);
+  }
   P.col_vec = (((uintptr_t)P.col) & 15) == 0 ? 1 : 0;
   if (P.direction && !share) {
     s3bfs_status ts = build_in_adjacency(h, stream);
@@ -654,14 +741,14 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
     P.pol_last = h_pol[1];
   }
   if ((e = cudaMemsetAsync(P.ctl, 0, sizeof(Ctl), stream)) != cudaSuccess) return bail(cuda_fail(h, e, "memset(ctl)"));
-  if ((e = cudaMemsetAsync(P.status, 0, (size_t)p_max * 8, stream)) != cudaSuccess) return bail(cuda_fail(h, e, "memset(status)"));
+  if ((e = cudaMemsetAsync(P.status, 0, (size_t)p_max * dist_size * 8 + 8, stream)) != cudaSuccess) return bail(cuda_fail(h, e, "memset(status)"));
   if (h->opt.debug_poison) {
     k_poison<<<h->num_sms * 4, 256, 0, stream>>>(P.vinfo, n, (int)h->cand_cap);
     cudaMemsetAsync(P.lp, 0x5a, (size_t)n * 8, stream);  // {d, parent} garbage until written
     if ((e = cudaGetLastError()) != cudaSuccess) return bail(cuda_fail(h, e, "k_poison"));
   }
 
-  h->ks_smem = (size_t)(3 * KS_NCAP + 4 + 2 * KS_ECAP) * 4;
+  h->ks_smem = (size_t)(3 * KS_NCAP + 4 + (S3BFS_KS_ONCHIP ? KS_TAB : 2 * KS_ECAP)) * 4;
   if ((e = cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->ks_smem)) != cudaSuccess)
     return bail(cuda_fail(h, e, "cudaFuncSetAttribute(k_small)"));
   h->kc_smem = (size_t)(3 * KC_FCAP + 4 + 2 * KC_ECTA) * 4;
@@ -780,11 +867,74 @@ s3bfs_status s3bfs_run(s3bfs_handle h, int32_t source, int32_t *level, int32_t *
   return S3BFS_OK;
 }
 
-// ---- NEXT-4: the per-level protocol over G ranks (include/s3bfs.h) ----------------------------
-s3bfs_status s3bfs_dist_begin(s3bfs_handle h, int32_t source, int32_t *level, int32_t *parent,
-                              s3bfs_stream_t stream_) {
+// ---- NEXT-4: one traversal over G ranks, 1-D vertex partition (include/s3bfs.h) ----------------
+static s3bfs_status dist_check(s3bfs_handle h) {
   if (!h) return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "handle is NULL");
   if (h->P.dist_size <= 1) return fail(h, S3BFS_ERR_UNSUPPORTED, "handle has dist_size <= 1");
+  return S3BFS_OK;
+}
+
+s3bfs_status s3bfs_dist_export(s3bfs_handle h, s3bfs_dist_peer *out) {
+  s3bfs_status s = dist_check(h);
+  if (s != S3BFS_OK) return s;
+  if (!out) return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "out is NULL");
+  std::memset(out, 0, sizeof(*out));
+  out->rank = h->P.dist_rank;
+  out->size = h->P.dist_size;
+  out->base = (uint64_t)(uintptr_t)h->xws;
+  out->recv = (uint64_t)(uintptr_t)h->P.recv;
+  out->rcnt = (uint64_t)(uintptr_t)h->P.rcnt;
+  out->rmeta = (uint64_t)(uintptr_t)h->P.rmeta;
+  out->rtot = (uint64_t)(uintptr_t)h->P.rtot;
+  out->bm = (uint64_t)(uintptr_t)h->P.bm;
+  static_assert(sizeof(cudaIpcMemHandle_t) <= sizeof(out->ipc), "IPC handle size");
+  cudaIpcMemHandle_t ih;
+  cudaError_t e = cudaIpcGetMemHandle(&ih, h->xws);
+  if (e == cudaSuccess) std::memcpy(out->ipc, &ih, sizeof(ih));
+  else cudaGetLastError();  // no IPC (e.g. a sandbox): loopback connections still work
+  out->ipc_valid = e == cudaSuccess ? 1 : 0;
+  return S3BFS_OK;
+}
+
+s3bfs_status s3bfs_dist_connect(s3bfs_handle h, const s3bfs_dist_peer *peers, int32_t count,
+                                int32_t use_ipc) {
+  s3bfs_status s = dist_check(h);
+  if (s != S3BFS_OK) return s;
+  const int G = h->P.dist_size, me = h->P.dist_rank;
+  if (!peers || count != G) return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "need one peer record per rank");
+  for (int d = 0; d < G; ++d)
+    if (peers[d].rank != d || peers[d].size != G)
+      return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "peer records must be in rank order, same size");
+  Params &P = h->P;
+  for (int d = 0; d < G; ++d) {
+    const s3bfs_dist_peer &q = peers[d];
+    char *base = (char *)(uintptr_t)q.base;
+    if (d == me) {
+      base = (char *)h->xws;
+    } else if (use_ipc) {
+      if (!q.ipc_valid) return fail(h, S3BFS_ERR_UNSUPPORTED, "peer exported no IPC handle");
+      if (h->ipc_open[d]) { cudaIpcCloseMemHandle(h->ipc_open[d]); h->ipc_open[d] = nullptr; }
+      cudaIpcMemHandle_t ih;
+      std::memcpy(&ih, q.ipc, sizeof(ih));
+      void *p = nullptr;
+      CK(h, cudaIpcOpenMemHandle(&p, ih, cudaIpcMemLazyEnablePeerAccess));
+      h->ipc_open[d] = p;
+      base = (char *)p;
+    }
+    auto map = [&](uint64_t a) { return base + (a - q.base); };  // same layout, rebased
+    P.p_recv[d] = (int2 *)map(q.recv);
+    P.p_rcnt[d] = (int32_t *)map(q.rcnt);
+    P.p_rmeta[d] = (int2 *)map(q.rmeta);
+    P.p_rtot[d] = (int2 *)map(q.rtot);
+    P.p_bm[d] = (uint32_t *)map(q.bm);
+  }
+  return S3BFS_OK;
+}
+
+s3bfs_status s3bfs_dist_begin(s3bfs_handle h, int32_t source, int32_t *level, int32_t *parent,
+                              s3bfs_stream_t stream_) {
+  s3bfs_status s = dist_check(h);
+  if (s != S3BFS_OK) return s;
   if (source < 0 || source >= h->n)
     return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "source " + std::to_string(source) + " not in [0, n)");
   if (!level || !parent || !is_device_ptr(level) || !is_device_ptr(parent))
@@ -792,71 +942,59 @@ s3bfs_status s3bfs_dist_begin(s3bfs_handle h, int32_t source, int32_t *level, in
   cudaStream_t stream = (cudaStream_t)stream_;
   h->last_stream = stream;
   h->ran = true;
-  k_init<<<init_grid(h), 256, 0, stream>>>(h->P, source, level, parent);
+  h->d_level = level;
+  h->d_parent = parent;
+  CK(h, cudaMemsetAsync(level, 0xff, (size_t)h->n * 4, stream));   // -1: not this rank's
+  CK(h, cudaMemsetAsync(parent, 0xff, (size_t)h->n * 4, stream));  //     (or unreached)
+  k_dist_init<<<init_grid(h), 256, 0, stream>>>(h->P, source);
   CK(h, cudaGetLastError());
   return S3BFS_OK;
 }
 
-s3bfs_status s3bfs_dist_expand(s3bfs_handle h, s3bfs_stream_t stream_, int32_t *n_local,
-                               int32_t *done) {
-  if (!h || !n_local || !done) return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "null argument");
-  if (h->P.dist_size <= 1) return fail(h, S3BFS_ERR_UNSUPPORTED, "handle has dist_size <= 1");
+s3bfs_status s3bfs_dist_explore(s3bfs_handle h, s3bfs_stream_t stream_) {
+  s3bfs_status s = dist_check(h);
+  if (s != S3BFS_OK) return s;
+  // P_max CTAs: the level's P_l <= P_max is read on the device (surplus CTAs return at once)
+  k_explore<<<h->P.p_max, KD_THREADS, 0, (cudaStream_t)stream_>>>(h->P);
+  CK(h, cudaGetLastError());
+  return S3BFS_OK;
+}
+
+s3bfs_status s3bfs_dist_dedup(s3bfs_handle h, s3bfs_stream_t stream_) {
+  s3bfs_status s = dist_check(h);
+  if (s != S3BFS_OK) return s;
   cudaStream_t stream = (cudaStream_t)stream_;
+  CK(h, cudaMemsetAsync(h->P.status, 0, (size_t)h->P.p_max * h->P.dist_size * 8, stream));
+  k_dist_owner<<<h->num_sms * 8, 256, 0, stream>>>(h->P);
+  k_dist_keep<<<h->P.p_max * h->P.dist_size, KD_THREADS, 0, stream>>>(h->P);
+  k_dist_publish<<<h->num_sms * 4, 256, 0, stream>>>(h->P);
+  CK(h, cudaGetLastError());
+  return S3BFS_OK;
+}
+
+s3bfs_status s3bfs_dist_advance(s3bfs_handle h, s3bfs_stream_t stream_, int32_t *done,
+                                int64_t *n_next) {
+  s3bfs_status s = dist_check(h);
+  if (s != S3BFS_OK) return s;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  k_dist_advance<<<1, 32, 0, stream>>>(h->P);
+  CK(h, cudaGetLastError());
+  if (!done && !n_next) return S3BFS_OK;
   if (!h->h_ctl) CK(h, cudaMallocHost((void **)&h->h_ctl, sizeof(Ctl)));
   CK(h, cudaMemcpyAsync(h->h_ctl, h->P.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, stream));
   CK(h, cudaStreamSynchronize(stream));
-  const Ctl c = *h->h_ctl;
-  *n_local = 0;
-  *done = c.tier == TIER_DONE ? 1 : 0;
-  if (*done) return S3BFS_OK;
-  k_explore<<<c.p_l, KD_THREADS, 0, stream>>>(h->P);
-  k_compact<<<c.p_l, KD_THREADS, 0, stream>>>(h->P);
-  CK(h, cudaGetLastError());
-  CK(h, cudaMemcpyAsync(h->h_ctl, h->P.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, stream));
-  CK(h, cudaStreamSynchronize(stream));
-  *n_local = h->h_ctl->n_next;
-  return S3BFS_OK;
-}
-
-s3bfs_status s3bfs_dist_records(s3bfs_handle h, void *dst, int32_t count, s3bfs_stream_t stream) {
-  if (!h) return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "handle is NULL");
-  if (h->P.dist_size <= 1) return fail(h, S3BFS_ERR_UNSUPPORTED, "handle has dist_size <= 1");
-  if (count < 0 || count > h->n) return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "count out of [0, n]");
-  if (count == 0) return S3BFS_OK;
-  if (!dst || !is_device_ptr(dst)) return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "dst must be device memory");
-  CK(h, cudaMemcpyAsync(dst, h->P.rec, (size_t)count * 16, cudaMemcpyDeviceToDevice,
-                        (cudaStream_t)stream));
-  return S3BFS_OK;
-}
-
-s3bfs_status s3bfs_dist_merge(s3bfs_handle h, const void *all, const int32_t *counts,
-                              int32_t stride, s3bfs_stream_t stream_) {
-  if (!h || !counts || stride < 0) return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "bad argument");
-  const int G = h->P.dist_size;
-  if (G <= 1) return fail(h, S3BFS_ERR_UNSUPPORTED, "handle has dist_size <= 1");
-  for (int r = 0; r < G; ++r)
-    if (counts[r] < 0 || counts[r] > stride || counts[r] > h->n)
-      return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "record count out of [0, stride]");
-  if (stride > 0 && (!all || !is_device_ptr(all)))
-    return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "records must be device memory");
-  if ((long long)G * stride > (long long)G * h->n)
-    return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "stride > n");
-  cudaStream_t stream = (cudaStream_t)stream_;
-  CK(h, cudaMemcpyAsync(h->d_counts, counts, (size_t)G * 4, cudaMemcpyHostToDevice, stream));
-  long long tiles = ((long long)G * stride + MG_TILE - 1) / MG_TILE;
-  if (tiles < 1) tiles = 1;
-  const int4 *a = (const int4 *)all;
-  k_merge_min<<<h->num_sms * 8, 256, 0, stream>>>(h->P, a, h->d_counts, stride, (int32_t)tiles);
-  k_merge_keep<<<(unsigned)tiles, KD_THREADS, 0, stream>>>(h->P, a, h->d_counts, stride, (int32_t)tiles);
-  CK(h, cudaGetLastError());
-  CK(h, cudaStreamSynchronize(stream));  // counts is the caller's host buffer
+  if (done) *done = h->h_ctl->tier == TIER_DONE ? 1 : 0;
+  if (n_next) *n_next = h->h_ctl->g_n_next;
   return S3BFS_OK;
 }
 
 s3bfs_status s3bfs_dist_end(s3bfs_handle h, s3bfs_stream_t stream_) {
-  if (!h) return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "handle is NULL");
-  if (h->P.dist_size <= 1) return fail(h, S3BFS_ERR_UNSUPPORTED, "handle has dist_size <= 1");
-  k_finalize<<<finalize_grid(h), 256, 0, (cudaStream_t)stream_>>>(h->P);
+  s3bfs_status s = dist_check(h);
+  if (s != S3BFS_OK) return s;
+  if (!h->d_level) return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "no traversal begun");
+  const long long want = ((long long)h->P.nloc + 255) / 256;
+  const int grid = (int)(want < h->num_sms * 8 ? (want < 1 ? 1 : want) : h->num_sms * 8);
+  k_dist_finalize<<<grid, 256, 0, (cudaStream_t)stream_>>>(h->P, h->d_level, h->d_parent);
   CK(h, cudaGetLastError());
   return S3BFS_OK;
 }
@@ -868,6 +1006,10 @@ s3bfs_status s3bfs_destroy(s3bfs_handle h) {
   if (h->exec) cudaGraphExecDestroy(h->exec);
   if (h->graph) cudaGraphDestroy(h->graph);
   if (h->ws) cudaFree(h->ws);
+  for (auto &p : h->ipc_open)
+    if (p) cudaIpcCloseMemHandle(p);
+  if (h->xws) cudaFree(h->xws);
+  if (h->dgraph) cudaFree(h->dgraph);
   if (h->gs && --h->gs->refs == 0) delete h->gs;
   if (h->h_ctl) cudaFreeHost(h->h_ctl);
   for (auto &ev : h->ev)

@@ -102,6 +102,9 @@ namespace s3bfs {
 #ifndef S3BFS_KX_QUEUE
 #define S3BFS_KX_QUEUE 1  // k_explore: claim checks + discoveries via a warp-private queue
 #endif
+#ifndef S3BFS_KS_ONCHIP
+#define S3BFS_KS_ONCHIP 1  // k_small: Owner race in a shared-memory table (no L2 round trip)
+#endif
 #ifndef S3BFS_CHECK
 #define S3BFS_CHECK 0  // 1: bounds-checked build (every traversal index checked; trap + message)
 #endif
@@ -129,9 +132,12 @@ constexpr int KD_WARPS = KD_THREADS / 32;
 constexpr int KD_SLACK = 64;                    // candidate-buffer slack per CTA
 constexpr int KX_GROUPS = S3BFS_KX_GROUPS;      // 32-edge groups per batch and warp
 constexpr int KC_GROUPS = S3BFS_KC_GROUPS;      // 32-candidate groups per k_compact round
+constexpr int DIST_MAX = 8;                     // NEXT-4: ranks per traversal (one node)
 constexpr int KQ_CAP = 32 + 2 * 32;            // k_explore warp queue (< 32 kept + 2 groups)
 constexpr int KS_THREADS = 1024;                // k_small CTA size
-constexpr int KS_ECAP = 8192;                   // T0 maximum (edges per tier-0 level)
+constexpr int KS_ECAP = S3BFS_KS_ONCHIP ? 4096 : 8192;  // T0 maximum (edges per tier-0 level)
+constexpr int KS_TAB_BITS = 14;                 // k_small on-chip Owner table: 2^14 entries
+constexpr int KS_TAB = 1 << KS_TAB_BITS;
 constexpr int KS_NCAP = KS_ECAP;                // frontier capacity of tier 0 (kept <= e_l)
 constexpr int KS_IPT = KS_ECAP / KS_THREADS;    // dedup items per thread
 constexpr int SCAN_THREADS = 512;
@@ -162,8 +168,8 @@ struct Ctl {
   int32_t p_l;        // P_l = CTAs of this level (Fig1 L16)
   int32_t chunk;      // edges per CTA (ceil(e_l / P_l))
   int32_t wcap;       // edges (= candidate capacity) per warp
-  int32_t e_lo, e_hi; // this rank's slice of the level's global edge range (NEXT-4; else 0, e_l)
-  uint32_t m_tile_ctr, m_done_ctr;  // NEXT-4 merge: look-back tile ids / last-CTA election
+  int32_t e_lo, e_hi; // the level's edge range explored here (0, e_l)
+  int32_t g_n_next, g_e_next;  // NEXT-4: the next level's frontier size / edges over all ranks
   int32_t n_next, e_next;   // written by the last k_compact CTA in tile order
   uint32_t done_ctr;        // last-CTA election in k_compact (not the discovery path)
   uint32_t tile_ctr;        // look-back tile ids in start order (forward progress under any
@@ -220,11 +226,25 @@ struct Params {
   int32_t n_scan;               // bottom-up scans internal ids [0, n_scan): the ones with deg > 0
   unsigned long long *bu_status;  // NEXT-3: look-back words of the bottom-up tiles
   int32_t bu_tiles, bu_tile_w;  // NEXT-3: bottom-up tiles and their width (bitmap words)
-  int32_t dist_size, dist_rank; // NEXT-4 (replicated graph, level edges split over ranks); 1, 0
-  int4 *rec;                    // NEXT-4: this rank's kept vertices {internal id, parent, row
-                                //  start, degree}, exchanged by all-gather
-  int32_t *minrank;             // NEXT-4: per internal vertex, lowest rank keeping it (INT_MAX)
-  unsigned long long *m_status; // NEXT-4: merge look-back words
+  // NEXT-4, 1-D vertex partition over G = dist_size ranks: internal id v is
+  // owned by rank (v / 32) mod G (block-cyclic 32-id blocks: one visited-bitmap word per owner,
+  // hubs spread over the ranks); its local slot is (v / 32 / G) * 32 + v mod 32.  vinfo / lp /
+  // the frontier / col are the rank's own (local slots, local CSR rows); bm and claim stay
+  // over global ids (the bitmap is replicated: every owner publishes its words to its peers).
+  int32_t dist_size, dist_rank; // 1, 0 on a single GPU
+  int32_t nloc;                 // local vertex slots of this rank
+  int2 *recv;                   // this rank's receive segments {v, parent}: source s's block
+                                //  at rofs[s], its warp g's segment at rofs[s] + g * wcap_s
+  int32_t *rcnt;                // per (source rank, source warp): candidates in that segment
+  int2 *rmeta;                  // per source rank: {wcap, p_l} of the level
+  int2 *rtot;                   // per source rank: {n_next, e_next} of the level
+  int32_t *kv;                  // internal ids of this rank's kept vertices (frontier order)
+  int32_t rofs[DIST_MAX + 1];   // receive block offsets (identical on every rank)
+  int2 *p_recv[DIST_MAX];       // peers' (and this rank's) arrays, mapped into this process
+  int32_t *p_rcnt[DIST_MAX];
+  int2 *p_rmeta[DIST_MAX];
+  int2 *p_rtot[DIST_MAX];
+  uint32_t *p_bm[DIST_MAX];
   long long nnz;
   long long cand_cap;           // candidate buffer entries (bounds-checked build)
   int32_t col_vec;              // col is 16-byte aligned: vectorised loads allowed
@@ -361,6 +381,15 @@ __device__ __forceinline__ int32_t *owner_of(int4 *vinfo, int v) {
   return reinterpret_cast<int32_t *>(vinfo + v) + 3;
 }
 
+// k_small's on-chip Owner table: round r's bijection of the 32-bit ids (odd multiplies,
+// xor-shifts and an added constant are each invertible)
+__device__ __forceinline__ uint32_t ks_hash(uint32_t v, int r) {
+  uint32_t x = v * 0x9E3779B1u + (uint32_t)r * 0x7F4A7C15u;
+  x ^= x >> 16;
+  x *= 0x85EBCA6Bu;
+  x ^= x >> 13;
+  return x;
+}
 __device__ __forceinline__ int warp_incl_scan(int x) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -538,10 +567,7 @@ __device__ void decide_tier(const Params &P, Ctl *c, int32_t n_l, int32_t e_l) {
     c->p_l = KC_CL;
     return;
   }
-  // NEXT-4: with dist_size ranks, this rank explores edges [e_lo, e_hi) of the level
-  const long long e_lo = (long long)e_l * P.dist_rank / P.dist_size;
-  const long long e_hi = (long long)e_l * (P.dist_rank + 1) / P.dist_size;
-  const long long es = e_hi - e_lo;
+  const long long e_lo = 0, e_hi = e_l, es = e_l;
   long long pt = P.variant ? (long long)P.p_max
                            : min((long long)P.p_max, (es + P.grain - 1) / P.grain);
   if (pt < 1) pt = 1;
@@ -830,6 +856,11 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   // 2 % of its targets, which otherwise cost every lane the claim and discovery code of
   // every flagged group (ncu: 45 % of the heavy level's instructions, profiles/).
   __shared__ int2 s_q[KD_WARPS][KQ_CAP];
+  __shared__ int32_t s_dc[KD_WARPS][DIST_MAX];  // NEXT-4: candidates per destination rank
+  if (P.dist_size > 1) {
+    if (lane < DIST_MAX) s_dc[warp][lane] = 0;
+    __syncwarp();
+  }
   int2 *const q = s_q[warp];
   int qn = 0;  // warp-uniform queue length
   // resolve the first cnt (<= 32) items; the rest (qn - cnt) move to the front
@@ -843,16 +874,36 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
     if (valid && it.x < 0) cl = ld_cg_u8(claim + cs);  // Fig1 L18: already claimed this level?
     const bool disc = valid && cl == 0;
     const unsigned m = __ballot_sync(0xffffffffu, disc);
-    if (disc) {  // EXPLORE-VERTEX's discovery: plain stores, the benign race (R4)
-      const int slot = segbase + wcount + __popc(m & lanemask_lt());
-      S3_CHK(v, P.n);
-      S3_CHK(slot, (long long)(b * KD_WARPS + warp + 1) * wcap);
-      st_u8(claim + cs, tag);
-      st_weak_v2(lp + v, new_level, it.y);   // d[v] <- l, parent (Fig1 L18)
-      st_weak(owner_of(vinfo, v), slot);     // Owner[v] <- i (benign race)
-      cand[slot] = v;                        // Q[i].Enqueue(v)
+    if (P.dist_size == 1) {
+      if (disc) {  // EXPLORE-VERTEX's discovery: plain stores, the benign race (R4)
+        const int slot = segbase + wcount + __popc(m & lanemask_lt());
+        S3_CHK(v, P.n);
+        S3_CHK(slot, (long long)(b * KD_WARPS + warp + 1) * wcap);
+        st_u8(claim + cs, tag);
+        st_weak_v2(lp + v, new_level, it.y);   // d[v] <- l, parent (Fig1 L18)
+        st_weak(owner_of(vinfo, v), slot);     // Owner[v] <- i (benign race)
+        cand[slot] = v;                        // Q[i].Enqueue(v)
+      }
+      wcount += __popc(m);
+    } else {
+      // NEXT-4: the candidate {v, parent} goes straight into the receive segment of this warp
+      // in v's owner rank (a peer store over NVLink, or this rank's own buffer); the owner
+      // runs the Owner check (e).  The tag only filters this rank's repeats.
+      if (disc) st_u8(claim + cs, tag);
+      const int d = disc ? (v >> 5) % P.dist_size : -1;
+      for (int dd = 0; dd < P.dist_size; ++dd) {
+        const unsigned md = __ballot_sync(0xffffffffu, d == dd);
+        if (!md) continue;  // warp-uniform
+        if (d == dd) {
+          const int k = s_dc[warp][dd] + __popc(md & lanemask_lt());
+          S3_CHK(k, wcap);
+          P.p_recv[dd][P.rofs[P.dist_rank] + segbase + k] = make_int2(v, it.y);
+        }
+        __syncwarp();
+        if (lane == 0) s_dc[warp][dd] += __popc(md);
+        __syncwarp();
+      }
     }
-    wcount += __popc(m);
     const int rest = qn - cnt;
     for (int i = 0; i < rest; i += 32) {  // in order: chunk i never reads a slot written before
       const int2 t = i + lane < rest ? q[cnt + i + lane] : make_int2(0, 0);
@@ -938,6 +989,15 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
 #endif
   S3_CHK(segbase + wcount, P.cand_cap);
   if (lane == 0) P.wcnt[b * KD_WARPS + warp] = wcount;
+  if (P.dist_size > 1) {  // NEXT-4: segment counts and the level's {wcap, p_l} to every owner
+    __syncwarp();
+    const int gw = b * KD_WARPS + warp;
+    if (lane < P.dist_size)
+      P.p_rcnt[lane][(long long)P.dist_rank * P.p_max * KD_WARPS + gw] = s_dc[warp][lane];
+    if (b == 0 && tid == 0)
+      for (int d = 0; d < P.dist_size; ++d) P.p_rmeta[d][P.dist_rank] = make_int2(wcap, p_l);
+    __threadfence_system();  // the peer stores are visible before this grid completes
+  }
 }
 
 // Publish the visited bits of a warp's kept candidates: lanes holding the same bitmap word in
@@ -993,7 +1053,6 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
   int2 *__restrict__ crd = P.cand_rd;
   const int seg = (b * KD_WARPS + warp) * c->wcap;
   const int cnt = P.wcnt[b * KD_WARPS + warp];
-  const bool dist = P.dist_size > 1;
   if (b == 0 && tid == 0) c->t_kx_end = globaltimer();
 
   int kept = 0, dsum = 0;
@@ -1020,7 +1079,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
       if (keep) {
         const int q = seg + kept + __popc(m & lanemask_lt());
         S3_CHK(q, P.cand_cap);
-        cand[q] = dist ? v[g] : vi[g].z;  // NEXT-4 keeps the internal id for the record
+        cand[q] = vi[g].z;
         crd[q] = make_int2(vi[g].x, d);
       }
       kept += __popc(m);
@@ -1049,7 +1108,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
       const int n_next = (int)(ex.a + agg.a), e_next = (int)(ex.b + agg.b);
       c->n_next = n_next;
       c->e_next = e_next;
-      if (!dist) P.fex[nxt][n_next] = e_next;
+      P.fex[nxt][n_next] = e_next;
     }
   }
   __syncthreads();
@@ -1068,14 +1127,10 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
     }
     const int inc = warp_incl_scan(d);
     if (k < kept) {
-      if (dist) {  // NEXT-4: this rank's kept vertex, for the cross-rank merge
-        P.rec[koff + k] = make_int4(v, P.lp[v].y, r0, d);
-      } else {
-        S3_CHK(koff + k, P.n);
-        fn[koff + k] = v;
-        frsn[koff + k] = r0;
-        fexn[koff + k] = doff + inc - d;
-      }
+      S3_CHK(koff + k, P.n);
+      fn[koff + k] = v;
+      frsn[koff + k] = r0;
+      fexn[koff + k] = doff + inc - d;
     }
     doff += __shfl_sync(0xffffffffu, inc, 31);
   }
@@ -1085,12 +1140,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
   __syncthreads();
   if (tid == 0) s_last = atomicAdd(&c->done_ctr, 1u) == gridDim.x - 1;
   __syncthreads();
-  if (s_last && tid == 0 && P.dist_size > 1) {
-    // NEXT-4: the local kept count stays in n_next; the merge advances the level
-    c->done_ctr = 0;
-    c->tile_ctr = 0;
-    c->cand_acc = 0;
-  } else if (s_last && tid == 0) {
+  if (s_last && tid == 0) {
     __threadfence();
     const int n_next = ld_volatile(&c->n_next), e_next = ld_volatile(&c->e_next);
     const unsigned long long t = globaltimer();
@@ -1109,116 +1159,297 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
   }
 }
 
-// ---- NEXT-4: cross-rank merge (replicated graph, the level's edges split over ranks) ----------
-// Every rank holds the same frontier and explored 1/G of its edges; k_compact left the rank's
-// kept vertices in rec[].  After an all-gather, all[r * stride + i] (i < counts[r]) holds rank
-// r's records.  A vertex kept by several ranks survives from the lowest rank (atomicMin off the
-// discovery path, then an equality test), so every rank builds the identical next frontier.
-constexpr int MG_TILE = KD_THREADS * 4;  // merge entries per CTA
-__global__ void k_merge_min(Params P, const int4 *__restrict__ all, const int32_t *__restrict__ counts,
-                            int32_t stride, int32_t tiles) {
-  const long long total = (long long)P.dist_size * stride;
-  const long long gs = (long long)gridDim.x * blockDim.x;
-  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < total; j += gs) {
-    const int r = (int)(j / stride), i = (int)(j - (long long)r * stride);
-    if (i < __ldg(counts + r)) atomicMin(P.minrank + __ldg(&all[j].x), r);
+// ---- NEXT-4: one traversal over G ranks, 1-D vertex partition ------------
+// Rank r owns the internal ids v with (v / 32) mod G == r, their CSR rows (a local CSR whose
+// targets stay global ids), and their state (vinfo / lp / Owner in local slots).  Per level:
+//   k_explore (dist mode)  the local frontier's arcs; a target whose visited bit (replicated
+//                          bitmap, exact at level start) is clear goes as {v, parent} straight
+//                          into the receive segment of its owner (peer store over NVLink)
+//   k_dist_owner           Owner[v] <- the candidate's slot for every received candidate (Fig1
+//                          L22 on the owner: the race stays inside one GPU, plain stores)
+//   k_dist_keep            keep a candidate iff Owner[v] is its slot; d/parent, the owner's
+//                          bitmap words, and the next local frontier by the (kept, degree-sum)
+//                          look-back scan over (source rank, CTA) tiles (Fig1 L23-L29, L12-L15)
+//   k_dist_publish         the owner's updated bitmap words into every peer's replica
+//   k_dist_advance         the level's totals over all ranks (each rank published its own into
+//                          every peer's rtot) decide the loop (Fig1 L9) and the local P_l
+// The exchange is peer memory (no collective carries data); the driver only orders the phases
+// across ranks (stream-ordered barriers).
+__device__ __forceinline__ int dist_local(const Params &P, int v) {
+  return ((v >> 5) / P.dist_size) * 32 + (v & 31);
+}
+__device__ __forceinline__ int dist_global(const Params &P, int lv) {
+  return (((lv >> 5) * P.dist_size + P.dist_rank) << 5) + (lv & 31);
+}
+
+__global__ void k_dist_init(Params P, int32_t s) {
+  const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long gstride = (long long)gridDim.x * blockDim.x;
+  const int si = P.o2n ? __ldg(P.o2n + s) : s;
+  const long long nw4 = ((long long)P.n + 127) >> 7;
+  for (long long i = gtid; i <= nw4; i += gstride) {  // every replica: visited = {s} + sentinel
+    uint4 w = i == nw4 ? make_uint4(~0u, ~0u, ~0u, ~0u) : make_uint4(0, 0, 0, 0);
+    if (i == (si >> 7)) (&w.x)[(si >> 5) & 3] = 1u << (si & 31);
+    reinterpret_cast<uint4 *>(P.bm)[i] = w;
   }
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < tiles; t += gs)
-    P.m_status[t] = 0ull;
+  const long long nc = ((long long)P.claim_mask + 16) >> 4;
+  for (long long i = gtid; i < nc; i += gstride)
+    reinterpret_cast<uint4 *>(P.claim)[i] = make_uint4(0, 0, 0, 0);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    P.ctl->m_tile_ctr = 0;
-    P.ctl->m_done_ctr = 0;
+    Ctl *c = P.ctl;
+    int n_l = 0, e_l = 0;
+    if ((si >> 5) % P.dist_size == P.dist_rank) {  // the source's owner seeds its frontier
+      const int ls = dist_local(P, si);
+      const int4 vs = P.vinfo[ls];
+      P.lp[ls] = make_int2(0, s);
+      P.f[0][0] = s;
+      P.frs[0][0] = vs.x;
+      P.fex[0][0] = 0;
+      P.fex[0][1] = vs.y;
+      n_l = 1;
+      e_l = vs.y;
+    } else {
+      P.fex[0][0] = 0;
+    }
+    c->level = 0;
+    c->cur = 0;
+    c->source = s;
+    c->num_levels = 0;
+    c->done_ctr = 0;
+    c->tile_ctr = 0;
+    c->cand_acc = 0;
+    c->t_prev = globaltimer();
+    c->bu = 0;
+    c->fb_valid = 0;
+    c->m_visited = 0;
+    c->g_n_next = 1;
+    c->g_e_next = 0;
+    decide_tier(P, c, n_l, e_l);
+    if (c->tier == TIER_DONE) {  // an empty local frontier still explores (one idle CTA)
+      c->tier = TIER_LARGE;
+      c->p_l = 1;
+      c->chunk = 1;
+      c->wcap = 1;
+      c->e_lo = 0;
+      c->e_hi = 0;
+    }
   }
 }
 
-__global__ void __launch_bounds__(KD_THREADS) k_merge_keep(Params P, const int4 *__restrict__ all,
-                                                           const int32_t *__restrict__ counts,
-                                                           int32_t stride, int32_t tiles) {
+// Fig1 L22 on the owner: Owner[v] <- slot for every candidate received this level
+__global__ void k_dist_owner(Params P) {
+  const int lane = threadIdx.x & 31;
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int nwmax = P.p_max * KD_WARPS;
+  for (int s = 0; s < P.dist_size; ++s) {
+    const int2 m = P.rmeta[s];  // {wcap, p_l} of source s
+    const long long nseg = (long long)m.y * KD_WARPS;
+    for (long long g = gw; g < nseg; g += nw) {
+      const int cnt = P.rcnt[(long long)s * nwmax + g];
+      const long long base = P.rofs[s] + g * m.x;
+      for (int k = lane; k < cnt; k += 32) {
+        const int v = P.recv[base + k].x;
+        S3_CHK(v, P.n);
+        S3_CHK(dist_local(P, v), P.nloc);
+        st_weak(owner_of(P.vinfo, dist_local(P, v)), (int)(base + k));  // benign race
+      }
+    }
+  }
+}
+
+// keep iff Owner[v] == slot (Fig1 L22-L23); tiles = (source rank, source CTA) in start order
+__global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_dist_keep(Params P) {
   Ctl *c = P.ctl;
   __shared__ int32_t s_k[KD_WARPS], s_d[KD_WARPS];
   __shared__ int s_last, s_tile;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nxt = c->cur ^ 1, new_level = c->level + 1;
-  if (tid == 0) s_tile = (int)atomicAdd(&c->m_tile_ctr, 1u);  // look-back order = start order
+  const int nt = P.dist_size * P.p_max;
+  const int nwmax = P.p_max * KD_WARPS;
+  if (tid == 0) s_tile = (int)atomicAdd(&c->tile_ctr, 1u);  // look-back order = start order
   __syncthreads();
-  const int b = s_tile;
-  const long long total = (long long)P.dist_size * stride;
-  // each warp: 4 groups of 32 consecutive entries of this tile
-  int4 rv[4];
-  bool keep[4];
-  int kept = 0, dsum = 0;
-#pragma unroll
-  for (int g = 0; g < 4; ++g) {
-    const long long j = (long long)b * MG_TILE + (warp * 4 + g) * 32 + lane;
-    keep[g] = false;
-    rv[g] = make_int4(0, 0, 0, 0);
-    if (j < total) {
-      const int r = (int)(j / stride), i = (int)(j - (long long)r * stride);
-      if (i < __ldg(counts + r)) {
-        rv[g] = all[j];
-        keep[g] = P.minrank[rv[g].x] == r;
+  const int t = s_tile;
+  if (t < nt) {
+    const int src = t / P.p_max, b = t - src * P.p_max;
+    const int2 m = P.rmeta[src];
+    const int gseg = b * KD_WARPS + warp;
+    const int cnt = b < m.y ? P.rcnt[(long long)src * nwmax + gseg] : 0;
+    const long long base = P.rofs[src] + (long long)gseg * m.x;
+    int kept = 0, dsum = 0;
+    for (int k0 = 0; k0 < cnt; k0 += 32) {
+      const int k = k0 + lane;
+      int2 it = make_int2(-1, 0);
+      int4 vi = make_int4(0, 0, 0, -1);
+      int lv = 0;
+      if (k < cnt) {
+        it = P.recv[base + k];
+        lv = dist_local(P, it.x);
+        vi = ld_weak_v4(P.vinfo + lv);  // written by k_dist_owner (another launch)
+      }
+      const bool keep = k < cnt && vi.w == (int)(base + k);
+      if (keep) P.lp[lv] = make_int2(new_level, it.y);  // d[v] <- l, parent (Fig1 L18)
+      bm_publish(P.bm, keep, it.x, lane);                 // this owner's bitmap words
+      const unsigned mk = __ballot_sync(0xffffffffu, keep);
+      if (keep) P.recv[base + kept + __popc(mk & lanemask_lt())].x = it.x;  // in place
+      kept += __popc(mk);
+      dsum += keep ? vi.y : 0;
+    }
+    dsum = warp_sum(dsum);
+    if (lane == 0) { s_k[warp] = kept; s_d[warp] = dsum; }
+    __syncthreads();
+    if (warp == 0) {
+      const int kk = s_k[lane & (KD_WARPS - 1)] * (lane < KD_WARPS);
+      const int dd = s_d[lane & (KD_WARPS - 1)] * (lane < KD_WARPS);
+      const int ik = warp_incl_scan(kk), id = warp_incl_scan(dd);
+      const Pair agg{(uint32_t)__shfl_sync(0xffffffffu, ik, 31),
+                     (uint32_t)__shfl_sync(0xffffffffu, id, 31)};
+      const Pair ex = lookback<true>(P.status, t, agg);
+      if (lane < KD_WARPS) {
+        s_k[lane] = (int)ex.a + ik - kk;
+        s_d[lane] = (int)ex.b + id - dd;
+      }
+      if (t == nt - 1 && lane == 0) {
+        c->n_next = (int)(ex.a + agg.a);
+        c->e_next = (int)(ex.b + agg.b);
+        P.fex[nxt][c->n_next] = c->e_next;
       }
     }
-    if (keep[g]) {
-      P.minrank[rv[g].x] = 0x7fffffff;  // the unique keeper resets it for the next level
-      P.lp[rv[g].x] = make_int2(new_level, rv[g].y);
-      mark_tag(P, rv[g].x);
+    __syncthreads();
+    int koff = s_k[warp], doff = s_d[warp];
+    for (int k0 = 0; k0 < kept; k0 += 32) {  // pass 2: the next local frontier (Fig1 L25-L29)
+      const int k = k0 + lane;
+      int v = 0;
+      int4 vi = make_int4(0, 0, 0, 0);
+      if (k < kept) {
+        v = P.recv[base + k].x;
+        vi = __ldg(P.vinfo + dist_local(P, v));
+      }
+      const int d = k < kept ? vi.y : 0;
+      const int inc = warp_incl_scan(d);
+      if (k < kept) {
+        S3_CHK(koff + k, P.nloc);
+        P.f[nxt][koff + k] = vi.z;
+        P.frs[nxt][koff + k] = vi.x;
+        P.fex[nxt][koff + k] = doff + inc - d;
+        P.kv[koff + k] = v;
+      }
+      doff += __shfl_sync(0xffffffffu, inc, 31);
     }
-    bm_publish(P.bm, keep[g], rv[g].x, lane);  // ranks that did not keep v learn its bit here
-    kept += __popc(__ballot_sync(0xffffffffu, keep[g]));
-    dsum += keep[g] ? rv[g].w : 0;
-  }
-  dsum = warp_sum(dsum);
-  if (lane == 0) { s_k[warp] = kept; s_d[warp] = dsum; }
-  __syncthreads();
-  if (warp == 0) {
-    const int kk = lane < KD_WARPS ? s_k[lane] : 0;
-    const int dd = lane < KD_WARPS ? s_d[lane] : 0;
-    const int ik = warp_incl_scan(kk), id = warp_incl_scan(dd);
-    const Pair agg{(uint32_t)__shfl_sync(0xffffffffu, ik, 31),
-                   (uint32_t)__shfl_sync(0xffffffffu, id, 31)};
-    const Pair ex = lookback<true>(P.m_status, b, agg);
-    if (lane < KD_WARPS) {
-      s_k[lane] = (int)ex.a + ik - kk;
-      s_d[lane] = (int)ex.b + id - dd;
-    }
-    if (b == tiles - 1 && lane == 0) {
-      const int n_next = (int)(ex.a + agg.a), e_next = (int)(ex.b + agg.b);
-      c->n_next = n_next;
-      c->e_next = e_next;
-      P.fex[nxt][n_next] = e_next;
-    }
-  }
-  __syncthreads();
-  int koff = s_k[warp], doff = s_d[warp];
-#pragma unroll
-  for (int g = 0; g < 4; ++g) {  // next frontier in (tile, warp, group, lane) order
-    const unsigned m = __ballot_sync(0xffffffffu, keep[g]);
-    const int d = keep[g] ? rv[g].w : 0;
-    const int inc = warp_incl_scan(d);
-    if (keep[g]) {
-      const int pos = koff + __popc(m & lanemask_lt());
-      P.f[nxt][pos] = P.n2o ? __ldg(P.n2o + rv[g].x) : rv[g].x;  // caller id
-      P.frs[nxt][pos] = rv[g].z;
-      P.fex[nxt][pos] = doff + inc - d;
-    }
-    koff += __popc(m);
-    doff += __shfl_sync(0xffffffffu, inc, 31);
   }
   __threadfence();
   __syncthreads();
-  if (tid == 0) s_last = atomicAdd(&c->m_done_ctr, 1u) == gridDim.x - 1;
+  if (tid == 0) s_last = atomicAdd(&c->done_ctr, 1u) == gridDim.x - 1;
   __syncthreads();
-  if (s_last && tid == 0) {  // every CTA has read the control block: advance the level
+  if (s_last && tid == 0) {  // every tile is done: this rank's totals to every rank
     __threadfence();
     const int n_next = ld_volatile(&c->n_next), e_next = ld_volatile(&c->e_next);
-    const unsigned long long t = globaltimer();
-    record_stat(P, c, c->level, c->n_l, c->e_l, TIER_LARGE, c->p_l, 0, n_next, c->t_prev, t);
-    c->t_prev = t;
-    c->level = new_level;
-    c->cur = nxt;
-    c->m_visited += e_next;
-    decide(P, c, n_next, e_next);
+    for (int d = 0; d < P.dist_size; ++d) P.p_rtot[d][P.dist_rank] = make_int2(n_next, e_next);
+    c->done_ctr = 0;
+    c->tile_ctr = 0;
+    __threadfence_system();
+  }
+}
+
+// the owner's updated words of the replicated bitmap into every peer (plain stores: only the
+// owner writes a word, after its own atomicOr publications of this level have completed)
+__global__ void k_dist_publish(Params P) {
+  const int n_next = P.ctl->n_next;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n_next;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int w = P.kv[i] >> 5;
+    const uint32_t val = P.bm[w];
+    for (int d = 0; d < P.dist_size; ++d)
+      if (d != P.dist_rank) P.p_bm[d][w] = val;
+  }
+  __threadfence_system();
+}
+
+// Fig1 L9-L11, L15-L16 over all ranks: the global totals end the loop; the local ones size P_l
+__global__ void k_dist_advance(Params P) {
+  if (threadIdx.x != 0) return;
+  Ctl *c = P.ctl;
+  long long gn = 0, ge = 0;
+  for (int s = 0; s < P.dist_size; ++s) {
+    const int32_t *t = reinterpret_cast<const int32_t *>(P.rtot + s);
+    gn += ld_volatile(t);
+    ge += ld_volatile(t + 1);
+  }
+  const unsigned long long tt = globaltimer();
+  record_stat(P, c, c->level, c->n_l, c->e_l, TIER_LARGE, c->p_l, 0, c->n_next, c->t_prev, tt);
+  c->t_prev = tt;
+  c->g_n_next = (int32_t)gn;
+  c->g_e_next = (int32_t)(ge < 0x7fffffff ? ge : 0x7fffffff);
+  c->level = c->level + 1;
+  c->cur ^= 1;
+  if (gn == 0) {
+    c->n_l = 0;
+    c->e_l = 0;
+    c->tier = TIER_DONE;
+    return;
+  }
+  decide_tier(P, c, c->n_next, c->e_next);
+  if (c->tier == TIER_DONE) {  // no local work this level: one idle CTA keeps the protocol
+    c->tier = TIER_LARGE;
+    c->p_l = 1;
+    c->chunk = 1;
+    c->wcap = 1;
+    c->e_lo = 0;
+    c->e_hi = 0;
+  }
+}
+
+// level/parent (caller ids) of this rank's vertices; the others stay as the caller set them
+__global__ void k_dist_finalize(Params P, int32_t *level, int32_t *parent) {
+  for (long long lv = (long long)blockIdx.x * blockDim.x + threadIdx.x; lv < P.nloc;
+       lv += (long long)gridDim.x * blockDim.x) {
+    const int v = dist_global(P, (int)lv);
+    if (v >= P.n) continue;
+    if ((__ldg(P.bm + (v >> 5)) >> (v & 31)) & 1u) {
+      const int o = P.n2o ? __ldg(P.n2o + v) : v;
+      const int2 r = P.lp[lv];
+      level[o] = r.x;
+      parent[o] = r.y;
+    }
+  }
+}
+
+// create time: arcs per owner rank (receive block sizes), the local CSR (rows of this rank's
+// vertices, global target ids) and its vertex records
+__global__ void k_dist_rank_arcs(const int32_t *ro, int n, int G, unsigned long long *cnt) {
+  unsigned long long acc[DIST_MAX] = {};
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (long long)gridDim.x * blockDim.x)
+    acc[(v >> 5) % G] += (unsigned long long)(ro[v + 1] - ro[v]);
+  for (int d = 0; d < G; ++d)
+    if (acc[d]) atomicAdd(cnt + d, acc[d]);
+}
+__global__ void k_dist_local_deg(Params P, const int32_t *ro, int32_t *deg_l) {
+  for (long long lv = (long long)blockIdx.x * blockDim.x + threadIdx.x; lv < P.nloc;
+       lv += (long long)gridDim.x * blockDim.x) {
+    const int v = dist_global(P, (int)lv);
+    deg_l[lv] = v < P.n ? ro[v + 1] - ro[v] : 0;
+  }
+}
+__global__ void k_dist_copy_rows(Params P, const int32_t *ro, const int32_t *col,
+                                 const int32_t *ro_l, int32_t *col_l) {
+  const int lane = threadIdx.x & 31;
+  const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long lv = w0; lv < P.nloc; lv += nw) {
+    const int v = dist_global(P, (int)lv);
+    if (v >= P.n) continue;
+    const int a = ro[v], d = ro[v + 1] - a, o = ro_l[lv];
+    for (int k = lane; k < d; k += 32) col_l[o + k] = col[a + k];
+  }
+}
+__global__ void k_dist_build_vinfo(Params P, const int32_t *ro_l, const int32_t *n2o,
+                                   int4 *vinfo_l) {
+  for (long long lv = (long long)blockIdx.x * blockDim.x + threadIdx.x; lv < P.nloc;
+       lv += (long long)gridDim.x * blockDim.x) {
+    const int v = dist_global(P, (int)lv);
+    const int cid = v < P.n ? (n2o ? n2o[v] : v) : -1;
+    vinfo_l[lv] = make_int4(ro_l[lv], ro_l[lv + 1] - ro_l[lv], cid, -1);
   }
 }
 
@@ -1335,8 +1566,8 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
   int32_t *sf = smem;                 // CurLevelVertices (caller ids)
   int32_t *srs = sf + KS_NCAP;        // internal row starts
   int32_t *sex = srs + KS_NCAP;       // exclusive degree scan, KS_NCAP + 1 entries
-  int32_t *cv = sex + KS_NCAP + 4;    // candidate per level-local edge (or -1)
-  int32_t *cpv = cv + KS_ECAP;        // its discoverer
+  int32_t *cv = sex + KS_NCAP + 4;    // candidate per level-local edge (or -1); with
+  int32_t *cpv = cv + KS_ECAP;        // S3BFS_KS_ONCHIP this space is the Owner table
   __shared__ int32_t s_wk[KS_THREADS / 32], s_wd[KS_THREADS / 32], s_wc[KS_THREADS / 32];
   __shared__ int32_t s_tot[3];
   __shared__ int32_t s_tiny[3];
@@ -1400,6 +1631,68 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
         S3_CHK(ev[i], P.n);
       }
     }
+#if S3BFS_KS_ONCHIP
+    // The visited word and the vertex record of every target in one round trip (both depend
+    // only on the col entry; L1-bypassing: bits are published by atomicOr at L2, H2).
+    uint32_t wv[KS_IPT];
+    int4 rv[KS_IPT];
+#pragma unroll
+    for (int i = 0; i < KS_IPT; ++i) {
+      wv[i] = ev[i] >= 0 ? __ldcg(bm + (ev[i] >> 5)) : 0xffffffffu;
+      rv[i] = ev[i] >= 0 ? __ldcg(vinfo + ev[i]) : make_int4(0, 0, 0, 0);
+    }
+    uint32_t open = 0;  // this thread's candidates (visited bit clear) not yet decided
+#pragma unroll
+    for (int i = 0; i < KS_IPT; ++i)
+      open |= (uint32_t)(ev[i] >= 0 && !((wv[i] >> (ev[i] & 31)) & 1u)) << i;
+    ncand = __popc(open);
+    // (e) Owner race on chip (Fig1 L20-L22; DESIGN R27): the Owner label of v lives in a
+    // 2^14-entry shared table at slot h(v) & (2^14 - 1), stored as {h(v) >> 14, edge index} --
+    // h a bijection of the 32-bit ids, so (slot, tag) names exactly one vertex.  Every copy
+    // of v stores its label (plain stores, the benign race), then reads the slot back: the tag
+    // of v means the race for v is decided (keep iff the label is this copy's); another tag
+    // means another vertex took the slot, and v's copies race again with the next round's
+    // hash.  Every copy of v sees the same slot state, so exactly one copy is kept.
+    int32_t *tab = sex + KS_NCAP + 4;
+    uint32_t km = 0;
+    for (int r = 0;; ++r) {
+#pragma unroll
+      for (int i = 0; i < KS_IPT; ++i)
+        if ((open >> i) & 1u) {
+          const uint32_t h = ks_hash((uint32_t)ev[i], r);
+          tab[h & (KS_TAB - 1)] = (int32_t)((h & ~(uint32_t)(KS_TAB - 1)) | (tid + i * KS_THREADS));
+        }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < KS_IPT; ++i)
+        if ((open >> i) & 1u) {
+          const uint32_t h = ks_hash((uint32_t)ev[i], r);
+          const uint32_t t = (uint32_t)tab[h & (KS_TAB - 1)];
+          if (((t ^ h) & ~(uint32_t)(KS_TAB - 1)) == 0) {  // v's own slot state: decided
+            open &= ~(1u << i);
+            if ((t & (KS_TAB - 1)) == (uint32_t)(tid + i * KS_THREADS)) km |= 1u << i;
+          }
+        }
+      if (!__syncthreads_or(open != 0)) break;  // also orders this round's reads before the
+    }                                            // next round's stores
+    int kv[KS_IPT], kr[KS_IPT], kd[KS_IPT];
+    int cnt = 0, dsum = 0;
+#pragma unroll
+    for (int i = 0; i < KS_IPT; ++i) {
+      kv[i] = -1;
+      kr[i] = 0;
+      kd[i] = 0;
+      if ((km >> i) & 1u) {
+        const int v = ev[i];
+        kv[i] = rv[i].z; kr[i] = rv[i].x; kd[i] = rv[i].y;
+        P.lp[v] = make_int2(L + 1, ux[i]);          // d[v] <- l, parent (Fig1 L18)
+        atomicOr(P.bm + (v >> 5), 1u << (v & 31));  // exact visited bit (not discovery)
+        mark_tag(P, v);
+      }
+      cnt += kv[i] >= 0;
+      dsum += kd[i];
+    }
+#else
     uint32_t wv[KS_IPT];
 #pragma unroll
     for (int i = 0; i < KS_IPT; ++i)  // L1-bypassing: bits are published by atomicOr at L2 in
@@ -1453,6 +1746,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
       cnt += kv[i] >= 0;
       dsum += kd[i];
     }
+#endif
     // block exclusive scan of (cnt, dsum)
     const int ik = warp_incl_scan(cnt), id = warp_incl_scan(dsum);
     const int wc = P.collect_stats ? warp_sum(ncand) : 0;

@@ -1,18 +1,22 @@
 """NEXT-4 ("distributed settings"): one traversal over G ranks.
 
-Replicated-graph split: every rank holds the whole graph and the same frontier, explores
-1/G of each level's edges with the single-GPU kernels, and deduplicates its own discoveries
-(Owner check).  The exchange step of a level is an all-gather of every rank's kept vertices
-(records {internal id, parent, row start, degree}); ``s3bfs_dist_merge`` then keeps each
-vertex once (lowest rank) and builds the identical next frontier on every rank.  All of the
-path's arithmetic runs in the library's kernels; this module is plumbing: the level loop and
-the collectives (``torch.distributed`` all-gathers -- NCCL over NVLink on a multi-GPU node).
+1-D vertex partition: rank r owns the internal ids v with (v / 32) mod G == r, their CSR rows
+and their state (include/s3bfs.h, NEXT-4).  Per level every rank explores its own frontier;
+a target whose visited bit (replicated bitmap) is clear is stored as {v, parent} straight into
+v's owner's receive segment -- peer memory over NVLink, written by the exploration kernel
+itself; the owner deduplicates (Owner check on its own GPU), publishes its new visited words
+and its totals into every peer, and the totals over all ranks end the loop.  All of the path's
+arithmetic and all data movement run in the library's kernels; this module is plumbing: the
+connection (exchange records, CUDA IPC between processes), the phase order and the final
+combination of the ranks' answers.
 
 ``traverse(ranks, source, group)`` drives the protocol for the ranks held by this process:
-one ``DistRank`` per process in a process group, or several ``DistRank`` objects in one
-process with ``group=None`` (loopback: the "all-gather" is a concatenation).  Any object with
-the ``DistRank`` methods can stand in for a rank (the CPU tests use a numpy stand-in to
-check the protocol on a gloo group).
+one ``DistRank`` per process of a process group (``connect(ranks, group)`` first), or several
+``DistRank`` objects in one process with ``group=None`` (a loopback on one GPU: the ranks run
+their phases in turn, so no kernel ever waits for another rank's kernel).  Between the phases
+a process group runs a one-element all-reduce on the current stream: a stream-ordered barrier
+(NCCL on GPUs), no host round trip.  Any object with the ``DistRank`` methods can stand in
+for a rank (the CPU tests use a numpy stand-in on a gloo group).
 """
 from __future__ import annotations
 
@@ -37,21 +41,31 @@ class DistRank:
         self.level = torch.empty(self.n, dtype=torch.int32, device=self.device)
         self.parent = torch.empty(self.n, dtype=torch.int32, device=self.device)
 
-    # -- the five protocol steps (include/s3bfs.h, NEXT-4) --
+    # -- connection --
+    def export(self):
+        return _s.s3bfs_dist_export(self.handle)
+
+    def connect(self, peers, use_ipc: bool) -> None:
+        _s.s3bfs_dist_connect(self.handle, peers, use_ipc)
+
+    # -- the per-level protocol (include/s3bfs.h, NEXT-4) --
     def begin(self, source: int) -> None:
         _s.s3bfs_dist_begin(self.handle, source, self.level, self.parent, self.stream)
 
-    def expand(self) -> tuple[int, bool]:
-        return _s.s3bfs_dist_expand(self.handle, self.stream)
+    def explore(self) -> None:
+        _s.s3bfs_dist_explore(self.handle, self.stream)
 
-    def records(self, n_local: int, stride: int):
-        import torch
-        buf = torch.zeros((max(stride, 1), 4), dtype=torch.int32, device=self.device)
-        _s.s3bfs_dist_records(self.handle, buf, n_local, self.stream)
-        return buf[:stride]
+    def exchange(self, group) -> None:
+        """Nothing to move: the explore kernel stored the candidates in the owners' memory."""
 
-    def merge(self, all_records, counts, stride: int) -> None:
-        _s.s3bfs_dist_merge(self.handle, all_records.contiguous(), counts, stride, self.stream)
+    def dedup(self) -> None:
+        _s.s3bfs_dist_dedup(self.handle, self.stream)
+
+    def publish(self, group) -> None:
+        """Nothing to move: the dedup kernels stored the bitmap words and totals in the peers."""
+
+    def advance(self, group) -> tuple[bool, int]:
+        return _s.s3bfs_dist_advance(self.handle, self.stream)
 
     def end(self):
         _s.s3bfs_dist_end(self.handle, self.stream)
@@ -69,49 +83,87 @@ class DistRank:
             pass
 
 
-def _gather_counts(local: list[int], group, device) -> list[int]:
+def connect(ranks: list, group=None) -> None:
+    """Give every rank the exchange records of all ranks (rank order).  group=None: the ranks
+    are all in this process (addresses used as they are); otherwise one rank per process, the
+    records travel through the group and peers' allocations are opened by CUDA IPC."""
     if group is None:
-        return list(local)
-    import torch
+        peers = [r.export() for r in ranks]
+        if not all(isinstance(p, _s.DistPeer) for p in peers):
+            peers = list(ranks)  # stand-ins (tests) exchange through each other directly
+        for r in ranks:
+            r.connect(peers, use_ipc=False)
+        return
+    import ctypes
+
     import torch.distributed as dist
-    assert len(local) == 1, "one rank per process in a process group"
-    t = torch.tensor(local, dtype=torch.int64, device=device)
-    out = [torch.zeros_like(t) for _ in range(dist.get_world_size(group))]
-    dist.all_gather(out, t, group=group)
-    return [int(x.item()) for x in out]
+    assert len(ranks) == 1, "one rank per process in a process group"
+    mine = ranks[0].export()
+    if isinstance(mine, ctypes.Structure):  # a library record travels as its bytes
+        mine = bytes(mine)
+    allrec = [None] * dist.get_world_size(group)
+    dist.all_gather_object(allrec, mine, group=group)
+    peers = [_s.DistPeer.from_buffer_copy(b) if isinstance(b, (bytes, bytearray)) else b
+             for b in allrec]
+    ranks[0].connect(peers, use_ipc=True)
 
 
-def _gather_records(send: list, group):
-    import torch
+def _barrier(ranks, group) -> None:
+    """Order the phases across ranks.  One process: the ranks' work was enqueued in phase order
+    (same stream), nothing to do.  A group: a one-element all-reduce on the current stream."""
     if group is None:
-        return torch.cat(send, 0)
+        return
+    import torch
     import torch.distributed as dist
-    out = [torch.empty_like(send[0]) for _ in range(dist.get_world_size(group))]
-    dist.all_gather(out, send[0].contiguous(), group=group)
-    return torch.cat(out, 0)
+    t = torch.zeros(1, dtype=torch.int32, device=ranks[0].device)
+    dist.all_reduce(t, group=group)
+
+
+def _combine(outs, group):
+    """Every rank wrote its own vertices and -1 elsewhere: the element-wise max is the answer."""
+    if group is None:
+        import numpy as np
+        lv, pa = outs[0]
+        for a, b in outs[1:]:
+            if isinstance(lv, np.ndarray):
+                lv, pa = np.maximum(lv, a), np.maximum(pa, b)
+            else:
+                import torch
+                lv, pa = torch.maximum(lv, a), torch.maximum(pa, b)
+        return [(lv, pa) for _ in outs]
+    import torch
+    import torch.distributed as dist
+    (lv, pa), = outs
+    lv_t = lv if isinstance(lv, torch.Tensor) else torch.from_numpy(lv)
+    pa_t = pa if isinstance(pa, torch.Tensor) else torch.from_numpy(pa)
+    dist.all_reduce(lv_t, op=dist.ReduceOp.MAX, group=group)
+    dist.all_reduce(pa_t, op=dist.ReduceOp.MAX, group=group)
+    return [(lv_t, pa_t)]
 
 
 def traverse(ranks: list, source: int, group=None) -> list:
-    """Run one traversal from `source`; returns [(level, parent)] of the local ranks.
-
-    Every rank of the job must call this with the same source.  The loop ends on every rank
-    at the same level: the merged frontier, hence the done flag, is identical everywhere."""
+    """Run one traversal from `source`; returns [(level, parent)] (the full answer) for the
+    local ranks.  Every rank of the job must call this with the same source; the loop ends on
+    every rank at the same level (the totals over all ranks decide)."""
     for r in ranks:
         r.begin(source)
     levels = 0
     while True:
-        st = [r.expand() for r in ranks]
-        done = {d for _, d in st}
+        for r in ranks:
+            r.explore()
+        for r in ranks:
+            r.exchange(group)
+        _barrier(ranks, group)
+        for r in ranks:
+            r.dedup()
+        for r in ranks:
+            r.publish(group)
+        _barrier(ranks, group)
+        st = [r.advance(group) for r in ranks]
+        done = {d for d, _ in st}
         if len(done) != 1:
-            raise RuntimeError("ranks disagree on termination (frontiers diverged)")
+            raise RuntimeError("ranks disagree on termination")
+        levels += 1
         if done.pop():
             break
-        local = [nl for nl, _ in st]
-        counts = _gather_counts(local, group, ranks[0].device)
-        stride = max(counts)
-        send = [r.records(nl, stride) for r, nl in zip(ranks, local)]
-        allrec = _gather_records(send, group)
-        for r in ranks:
-            r.merge(allrec, counts, stride)
-        levels += 1
-    return [r.end() for r in ranks]
+    return _combine([r.end() for r in ranks], group)

@@ -26,8 +26,8 @@ STATUS_NAMES = {0: "ok", 1: "invalid argument", 2: "unsupported", 3: "out of mem
 EXPORTED = ("s3bfs_create", "s3bfs_clone", "s3bfs_run", "s3bfs_destroy", "s3bfs_status_string",
             "s3bfs_last_error", "s3bfs_get_level_stats", "s3bfs_get_info", "s3bfs_get_kernel_times",
             "s3bfs_debug_exclusive_scan", "s3bfs_debug_find_start_points", "s3bfs_debug_timeline",
-            "s3bfs_dist_begin", "s3bfs_dist_expand", "s3bfs_dist_records", "s3bfs_dist_merge",
-            "s3bfs_dist_end")
+            "s3bfs_dist_export", "s3bfs_dist_connect", "s3bfs_dist_begin", "s3bfs_dist_explore",
+            "s3bfs_dist_dedup", "s3bfs_dist_advance", "s3bfs_dist_end")
 
 
 class S3BFSError(RuntimeError):
@@ -48,6 +48,14 @@ class Options(ctypes.Structure):
                 ("do_beta", ctypes.c_int32), ("dist_size", ctypes.c_int32),
                 ("dist_rank", ctypes.c_int32), ("cluster_max_edges", ctypes.c_int32),
                 ("hub_vertices", ctypes.c_int32), ("tag_mode_pct", ctypes.c_int32)]
+
+
+class DistPeer(ctypes.Structure):
+    """s3bfs_dist_peer: a rank's exchange record (addresses + CUDA IPC handle)."""
+    _fields_ = [("base", ctypes.c_uint64), ("recv", ctypes.c_uint64), ("rcnt", ctypes.c_uint64),
+                ("rmeta", ctypes.c_uint64), ("rtot", ctypes.c_uint64), ("bm", ctypes.c_uint64),
+                ("ipc", ctypes.c_uint8 * 64), ("ipc_valid", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("size", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
 class LevelStat(ctypes.Structure):
@@ -104,10 +112,12 @@ def load(build_if_missing: bool = True):
     lib.s3bfs_debug_exclusive_scan.argtypes = [vp, vp, i32, vp]
     lib.s3bfs_debug_find_start_points.argtypes = [vp, i32, i32, i32, vp, vp, vp]
     lib.s3bfs_debug_timeline.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64)]
+    lib.s3bfs_dist_export.argtypes = [vp, ctypes.POINTER(DistPeer)]
+    lib.s3bfs_dist_connect.argtypes = [vp, ctypes.POINTER(DistPeer), i32, i32]
     lib.s3bfs_dist_begin.argtypes = [vp, i32, vp, vp, vp]
-    lib.s3bfs_dist_expand.argtypes = [vp, vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]
-    lib.s3bfs_dist_records.argtypes = [vp, vp, i32, vp]
-    lib.s3bfs_dist_merge.argtypes = [vp, vp, ctypes.POINTER(i32), i32, vp]
+    lib.s3bfs_dist_explore.argtypes = [vp, vp]
+    lib.s3bfs_dist_dedup.argtypes = [vp, vp]
+    lib.s3bfs_dist_advance.argtypes = [vp, vp, ctypes.POINTER(i32), ctypes.POINTER(ctypes.c_int64)]
     lib.s3bfs_dist_end.argtypes = [vp, vp]
     for name in EXPORTED:
         if name != "s3bfs_status_string":
@@ -247,31 +257,42 @@ def s3bfs_debug_timeline(handle) -> list:
     return list(out)
 
 
-# ---- NEXT-4: the per-level protocol of a traversal over G ranks (include/s3bfs.h) ----------
+# ---- NEXT-4: one traversal over G ranks, 1-D vertex partition (include/s3bfs.h) ----------
+def s3bfs_dist_export(handle) -> DistPeer:
+    out = DistPeer()
+    _check(load().s3bfs_dist_export(handle, ctypes.byref(out)), "s3bfs_dist_export", handle)
+    return out
+
+
+def s3bfs_dist_connect(handle, peers, use_ipc: bool) -> None:
+    arr = (DistPeer * len(peers))(*peers)
+    _check(load().s3bfs_dist_connect(handle, arr, len(peers), 1 if use_ipc else 0),
+           "s3bfs_dist_connect", handle)
+
+
 def s3bfs_dist_begin(handle, source: int, level, parent, stream=None) -> None:
     _check(load().s3bfs_dist_begin(handle, int(source), _ptr(level), _ptr(parent), _stream(stream)),
            "s3bfs_dist_begin", handle)
 
 
-def s3bfs_dist_expand(handle, stream=None) -> tuple[int, bool]:
-    """Expand this rank's slice of the level: (record count, traversal done)."""
-    n_local, done = ctypes.c_int32(), ctypes.c_int32()
-    _check(load().s3bfs_dist_expand(handle, _stream(stream), ctypes.byref(n_local), ctypes.byref(done)),
-           "s3bfs_dist_expand", handle)
-    return n_local.value, bool(done.value)
+def s3bfs_dist_explore(handle, stream=None) -> None:
+    _check(load().s3bfs_dist_explore(handle, _stream(stream)), "s3bfs_dist_explore", handle)
 
 
-def s3bfs_dist_records(handle, dst, count: int, stream=None) -> None:
-    """Copy the first `count` records into dst (int32 CUDA tensor [>= count, 4])."""
-    _check(load().s3bfs_dist_records(handle, _ptr(dst) if count else 0, int(count), _stream(stream)),
-           "s3bfs_dist_records", handle)
+def s3bfs_dist_dedup(handle, stream=None) -> None:
+    _check(load().s3bfs_dist_dedup(handle, _stream(stream)), "s3bfs_dist_dedup", handle)
 
 
-def s3bfs_dist_merge(handle, all_records, counts, stride: int, stream=None) -> None:
-    """Merge the all-gathered records (int32 CUDA tensor [G * stride, 4]); counts: G ints."""
-    c = (ctypes.c_int32 * len(counts))(*[int(x) for x in counts])
-    _check(load().s3bfs_dist_merge(handle, _ptr(all_records) if stride else 0, c, int(stride),
-                                   _stream(stream)), "s3bfs_dist_merge", handle)
+def s3bfs_dist_advance(handle, stream=None, wait: bool = True):
+    """Advance the level; with wait: (done, next frontier size over all ranks) after a sync."""
+    if not wait:
+        _check(load().s3bfs_dist_advance(handle, _stream(stream), None, None),
+               "s3bfs_dist_advance", handle)
+        return None
+    done, n_next = ctypes.c_int32(), ctypes.c_int64()
+    _check(load().s3bfs_dist_advance(handle, _stream(stream), ctypes.byref(done),
+                                     ctypes.byref(n_next)), "s3bfs_dist_advance", handle)
+    return bool(done.value), int(n_next.value)
 
 
 def s3bfs_dist_end(handle, stream=None) -> None:

@@ -1,11 +1,13 @@
-"""NEXT-4: one traversal over G ranks, the replicated-graph edge split.
+"""NEXT-4: one traversal over G ranks, 1-D vertex partition.
 
-CPU (-m "not gpu"): the real driver (paper_2209_08764_b200.dist.traverse) and the real
-collectives on a world-size-2/3 gloo group, each rank a numpy stand-in with the library's
-per-level semantics (tests/dist_numpy_rank.py) -- the exchange protocol, padding, rank order
-and termination.  GPU (-m gpu): the library's dist kernels (k_explore/k_compact on a rank's
-edge slice, k_merge_min/k_merge_keep) on G handles in one process (loopback exchange), levels
-bit-exact with the oracle and parents valid by the certificate, plus the argument checks.
+CPU (-m "not gpu"): the real driver (paper_2209_08764_b200.dist.traverse / connect) on a
+world-size-2/3 gloo group, each rank a numpy stand-in with the library's per-level semantics
+(tests/dist_numpy_rank.py): phase order, exchange, termination agreement and the final
+combination; and the same stand-ins in one process (loopback).  GPU (-m gpu): the library's
+kernels (k_explore routing candidates into the owners' receive segments, k_dist_owner /
+k_dist_keep / k_dist_publish / k_dist_advance) on G handles in one process (loopback: the
+peers' addresses are plain device pointers, the phases run rank by rank), levels bit-exact
+with the oracle and parents valid by the certificate, plus the argument checks.
 """
 import os
 import socket
@@ -61,9 +63,10 @@ def _worker(rank, world, port, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     res = {}
     for g in _graphs():
+        rk = [NR(g.row_offsets, g.col_indices, rank, world)]
+        pd.connect(rk, dist.group.WORLD)
         for s in sorted({0, g.n // 2, g.n - 1}):
-            (lv, pa), = pd.traverse([NR(g.row_offsets, g.col_indices, rank, world)], s,
-                                    group=dist.group.WORLD)
+            (lv, pa), = pd.traverse(rk, s, group=dist.group.WORLD)
             res[(g.name, s)] = (lv.tolist(), pa.tolist())
     out[rank] = res
     dist.barrier()
@@ -90,10 +93,11 @@ def test_loopback_protocol_numpy():
     import paper_2209_08764_b200.dist as pd
     for g in _graphs():
         for G in (1, 2, 4):
+            rk = [NumpyRank(g.row_offsets, g.col_indices, r, G) for r in range(G)]
+            pd.connect(rk)
             for s in sorted({0, g.n - 1}):
-                outs = pd.traverse([NumpyRank(g.row_offsets, g.col_indices, r, G) for r in range(G)], s)
-                for lv, pa in outs:
-                    _check(g, s, lv, pa)
+                for lv, pa in pd.traverse(rk, s):
+                    _check(g, s, lv.numpy(), pa.numpy())
 
 
 # ---- GPU: the library's dist kernels -----------------------------------------------------
@@ -102,7 +106,10 @@ def _gpu_ranks(g, G, **kw):
     ro = torch.from_numpy(g.row_offsets).cuda()
     col = (torch.from_numpy(g.col_indices).cuda() if g.nnz
            else torch.empty(0, dtype=torch.int32, device="cuda"))
-    return [pkg.DistRank(ro, col, r, G, pkg.Options(**kw)) for r in range(G)]
+    import paper_2209_08764_b200.dist as pd
+    ranks = [pkg.DistRank(ro, col, r, G, pkg.Options(**kw)) for r in range(G)]
+    pd.connect(ranks)
+    return ranks
 
 
 @pytest.mark.gpu
@@ -137,7 +144,7 @@ def test_gpu_loopback_configs(cfg, G, nsrc):
             _check(g, int(s), lvn, pan)
             if ref is None:
                 ref = (lvn, pan)
-            else:  # replicated state: every rank holds the same answer
+            else:  # the combined answer is the same on every rank
                 assert np.array_equal(ref[0], lvn) and np.array_equal(ref[1], pan)
     for r in ranks:
         r.close()
@@ -146,6 +153,7 @@ def test_gpu_loopback_configs(cfg, G, nsrc):
 @pytest.mark.gpu
 def test_gpu_dist_argument_checks():
     pkg = pytest.importorskip("paper_2209_08764_b200")
+    import paper_2209_08764_b200.dist as pd
     g = graphgen.from_edges(3, [(0, 1), (1, 2)])
     ro = torch.from_numpy(g.row_offsets).cuda()
     col = torch.from_numpy(g.col_indices).cuda()
@@ -154,40 +162,58 @@ def test_gpu_dist_argument_checks():
         pkg.DistRank(ro, col, 2, 2)
     with pytest.raises(pkg.S3BFSError, match="unsupported"):
         pkg.DistRank(ro, col, 0, 2, pkg.Options(direction=1))
-    r = pkg.DistRank(ro, col, 0, 2)
     with pytest.raises(pkg.S3BFSError, match="unsupported"):
-        pkg.s3bfs_run(r.handle, 0, lv, lv.clone())
+        pkg.DistRank(ro, col, 0, 9)
+    r0, r1 = pkg.DistRank(ro, col, 0, 2), pkg.DistRank(ro, col, 1, 2)
+    with pytest.raises(pkg.S3BFSError, match="unsupported"):
+        pkg.s3bfs_run(r0.handle, 0, lv, lv.clone())
+    with pytest.raises(pkg.S3BFSError, match="unsupported"):
+        pkg.s3bfs_clone(r0.handle)
     plain = pkg.S3BFS(ro, col)
     with pytest.raises(pkg.S3BFSError, match="unsupported"):
-        pkg.s3bfs.s3bfs_dist_expand(plain.handle)
+        pkg.s3bfs.s3bfs_dist_explore(plain.handle)
+    with pytest.raises(pkg.S3BFSError, match="invalid argument"):  # one record per rank
+        r0.connect([r0.export()], use_ipc=False)
+    with pytest.raises(pkg.S3BFSError, match="invalid argument"):  # rank order
+        r0.connect([r1.export(), r0.export()], use_ipc=False)
+    pd.connect([r0, r1])
     with pytest.raises(pkg.S3BFSError, match="invalid argument"):
-        r.begin(3)
-    r.begin(0)
-    n_local, done = r.expand()
-    assert not done
-    with pytest.raises(pkg.S3BFSError, match="invalid argument"):  # count > stride
-        r.merge(torch.zeros((1, 4), dtype=torch.int32, device="cuda"), [2, 0], 1)
-    r.close()
-    plain.close()
+        r0.begin(3)
+    (a, b), _ = pd.traverse([r0, r1], 0)
+    _check(g, 0, a.cpu().numpy(), b.cpu().numpy())
+    for x in (r0, r1, plain):
+        x.close()
 
 
 @pytest.mark.gpu
-def test_gpu_dist_clone():
-    """A clone of a dist handle (shared prepared graph, own workspace) runs the protocol too."""
+def test_gpu_dist_each_rank_owns_its_vertices():
+    """Before the combination every rank holds exactly its own vertices' answer (block-cyclic
+    32-id blocks of the internal ids; with reorder=-1 internal ids are the caller ids)."""
     pkg = pytest.importorskip("paper_2209_08764_b200")
+    g = graphgen.rmat(12, 16, seed=5)
+    ro = torch.from_numpy(g.row_offsets).cuda()
+    col = torch.from_numpy(g.col_indices).cuda()
     import paper_2209_08764_b200.dist as pd
-    g = _graphs()[4]  # rand-directed
-    ranks = _gpu_ranks(g, 2)
-    clones = []
+    G = 3
+    ranks = [pkg.DistRank(ro, col, r, G, pkg.Options(reorder=-1)) for r in range(G)]
+    pd.connect(ranks)
+    s = int(np.argmax(np.diff(g.row_offsets)))
     for r in ranks:
-        c = pd.DistRank.__new__(pd.DistRank)
-        c.rank, c.size, c.n, c.device, c.stream = r.rank, r.size, r.n, r.device, None
-        c.row_offsets, c.col_indices = r.row_offsets, r.col_indices
-        c.handle = pkg.s3bfs_clone(r.handle)
-        c.level, c.parent = torch.empty_like(r.level), torch.empty_like(r.parent)
-        clones.append(c)
-    for s in (0, g.n - 1):
-        for lv, pa in pd.traverse(clones, s):
-            _check(g, s, lv.cpu().numpy(), pa.cpu().numpy())
-    for c in clones + ranks:
-        c.close()
+        r.begin(s)
+    while True:
+        for r in ranks:
+            r.explore()
+        for r in ranks:
+            r.dedup()
+        if {r.advance(None)[0] for r in ranks} == {True}:
+            break
+    ref, _ = oracle.bfs(g.row_offsets, g.col_indices, s)
+    owner = (np.arange(g.n) // 32) % G
+    for r in ranks:
+        lv, _ = r.end()
+        lv = lv.cpu().numpy()
+        mine = owner == r.rank
+        assert np.array_equal(lv[mine], ref[mine])
+        assert np.all(lv[~mine] == -1)
+    for r in ranks:
+        r.close()
