@@ -207,7 +207,10 @@ s3bfs_status s3bfs_debug_timeline(s3bfs_handle h, uint64_t out[4]);
  * All calls need a handle created with dist_size > 1 (else UNSUPPORTED). */
 typedef struct {
   uint64_t base;            /* the rank's exchange allocation (device address in its process) */
-  uint64_t recv, rcnt, rmeta, rtot, bm;  /* arrays inside it (same layout on every rank) */
+  uint64_t recv, rcnt, rmeta, rtot, bm, vinfo;  /* arrays inside it (same layout on every
+                                               rank): receive segments, their counts, per-source
+                                               {wcap, P_l} and totals, the visited-bitmap
+                                               replica, the vertex records (Owner) */
   uint8_t ipc[64];          /* cudaIpcMemHandle_t of the allocation (valid if ipc_valid) */
   int32_t ipc_valid;
   int32_t rank, size;
@@ -231,8 +234,9 @@ s3bfs_status s3bfs_dist_begin(s3bfs_handle h, int32_t source, int32_t *level, in
 /* Explore this rank's part of the current level (enqueued on `stream`). */
 s3bfs_status s3bfs_dist_explore(s3bfs_handle h, s3bfs_stream_t stream);
 
-/* Deduplicate the candidates received this level; publish bitmap words and totals (enqueued
- * on `stream`; every rank's explore of this level must have completed before it runs). */
+/* Deduplicate the candidates received this level (keep the copy whose slot is Owner[v]);
+ * publish bitmap words (atomicOr into every replica) and totals (enqueued on `stream`; every
+ * rank's explore of this level must have completed before it runs). */
 s3bfs_status s3bfs_dist_dedup(s3bfs_handle h, s3bfs_stream_t stream);
 
 /* Advance the level from the totals of all ranks (every rank's dedup of this level must have
@@ -240,6 +244,11 @@ s3bfs_status s3bfs_dist_dedup(s3bfs_handle h, s3bfs_stream_t stream);
  * no rank has a next frontier, *n_next = the next frontier's size over all ranks. */
 s3bfs_status s3bfs_dist_advance(s3bfs_handle h, s3bfs_stream_t stream, int32_t *done,
                                 int64_t *n_next);
+
+/* Synchronise `stream` and read the last advance: *done = 1 when no rank has a next frontier,
+ * *n_next = the next frontier's size over all ranks (either may be NULL, not both). */
+s3bfs_status s3bfs_dist_status(s3bfs_handle h, s3bfs_stream_t stream, int32_t *done,
+                               int64_t *n_next);
 
 /* Write level/parent (caller ids) of this rank's vertices for the traversal begun by
  * s3bfs_dist_begin (enqueued on `stream`). */

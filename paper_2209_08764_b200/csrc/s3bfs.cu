@@ -235,7 +235,6 @@ s3bfs_status build_dist(s3bfs_ctx *h, cudaStream_t st, int nloc) {
   CK(h, tmp_b.alloc(tmp_bytes));
   CK(h, cub::DeviceScan::ExclusiveSum(tmp_b.p, tmp_bytes, deg_l, ro_l, nloc + 1, st));
   k_dist_copy_rows<<<grid, 256, 0, st>>>(P, ro, col, ro_l, col_l);
-  k_dist_build_vinfo<<<grid, 256, 0, st>>>(P, ro_l, P.n2o, P.vinfo);
   CK(h, cudaGetLastError());
   P.col = col_l;
   P.nnz = nnz_l;
@@ -254,21 +253,26 @@ s3bfs_status build_dist(s3bfs_ctx *h, cudaStream_t st, int nloc) {
   const size_t o_recv = take((size_t)ofs * 8), o_rcnt = take((size_t)G * nwmax * 4);
   const size_t o_rmeta = take((size_t)G * 8), o_rtot = take((size_t)G * 8);
   const size_t o_bm = take(bm_bytes + 16);
+  const size_t o_vinfo = take((size_t)(nloc + 32) * 16);  // the records senders write Owner into
   h->xws_bytes = off;
   CK(h, cudaMalloc(&h->xws, off));
   char *x = (char *)h->xws;
-  CK(h, cudaMemsetAsync(x + o_rcnt, 0, off - o_rcnt, st));
+  CK(h, cudaMemsetAsync(x + o_rcnt, 0, o_bm - o_rcnt, st));
   P.recv = (int2 *)(x + o_recv);
   P.rcnt = (int32_t *)(x + o_rcnt);
   P.rmeta = (int2 *)(x + o_rmeta);
   P.rtot = (int2 *)(x + o_rtot);
   P.bm = (uint32_t *)(x + o_bm);
+  P.vinfo = (int4 *)(x + o_vinfo);
+  k_dist_build_vinfo<<<grid, 256, 0, st>>>(P, ro_l, P.n2o, P.vinfo);
+  CK(h, cudaGetLastError());
   for (int d = 0; d < DIST_MAX; ++d) {  // until s3bfs_dist_connect: every rank is this one
     P.p_recv[d] = P.recv;
     P.p_rcnt[d] = P.rcnt;
     P.p_rmeta[d] = P.rmeta;
     P.p_rtot[d] = P.rtot;
     P.p_bm[d] = P.bm;
+    P.p_vinfo[d] = P.vinfo;
   }
   CK(h, cudaStreamSynchronize(st));
   return S3BFS_OK;
@@ -407,7 +411,21 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
     auto add = [&](void *fn, int grid, int block, size_t smem) -> s3bfs_status {
       cudaGraphNode_t nd;
       cudaKernelNodeParams kp = kparams(fn, grid, block, smem);
-      CK(h, cudaGraphAddKernelNode(&nd, bg, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
+      if (!S3BFS_PDL || !prev) {
+        CK(h, cudaGraphAddKernelNode(&nd, bg, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
+      } else {  // kernel -> kernel: programmatic edge (the kernels' pdl_enter, PTX helpers)
+        cudaGraphNodeParams np = {};
+        np.type = cudaGraphNodeTypeKernel;
+        np.kernel.func = kp.func;
+        np.kernel.gridDim = kp.gridDim;
+        np.kernel.blockDim = kp.blockDim;
+        np.kernel.sharedMemBytes = kp.sharedMemBytes;
+        np.kernel.kernelParams = kp.kernelParams;
+        cudaGraphEdgeData ed = {};
+        ed.from_port = cudaGraphKernelNodePortProgrammatic;
+        ed.type = cudaGraphDependencyTypeProgrammatic;
+        CK(h, cudaGraphAddNode_v2(&nd, bg, &prev, &ed, 1, &np));
+      }
       prev = nd;
       return S3BFS_OK;
     };
@@ -868,6 +886,8 @@ s3bfs_status s3bfs_run(s3bfs_handle h, int32_t source, int32_t *level, int32_t *
 }
 
 // ---- NEXT-4: one traversal over G ranks, 1-D vertex partition (include/s3bfs.h) ----------------
+s3bfs_status s3bfs_dist_status(s3bfs_handle h, s3bfs_stream_t stream_, int32_t *done,
+                               int64_t *n_next);
 static s3bfs_status dist_check(s3bfs_handle h) {
   if (!h) return fail(nullptr, S3BFS_ERR_INVALID_ARGUMENT, "handle is NULL");
   if (h->P.dist_size <= 1) return fail(h, S3BFS_ERR_UNSUPPORTED, "handle has dist_size <= 1");
@@ -887,6 +907,7 @@ s3bfs_status s3bfs_dist_export(s3bfs_handle h, s3bfs_dist_peer *out) {
   out->rmeta = (uint64_t)(uintptr_t)h->P.rmeta;
   out->rtot = (uint64_t)(uintptr_t)h->P.rtot;
   out->bm = (uint64_t)(uintptr_t)h->P.bm;
+  out->vinfo = (uint64_t)(uintptr_t)h->P.vinfo;
   static_assert(sizeof(cudaIpcMemHandle_t) <= sizeof(out->ipc), "IPC handle size");
   cudaIpcMemHandle_t ih;
   cudaError_t e = cudaIpcGetMemHandle(&ih, h->xws);
@@ -927,6 +948,7 @@ s3bfs_status s3bfs_dist_connect(s3bfs_handle h, const s3bfs_dist_peer *peers, in
     P.p_rmeta[d] = (int2 *)map(q.rmeta);
     P.p_rtot[d] = (int2 *)map(q.rtot);
     P.p_bm[d] = (uint32_t *)map(q.bm);
+    P.p_vinfo[d] = (int4 *)map(q.vinfo);
   }
   return S3BFS_OK;
 }
@@ -964,10 +986,7 @@ s3bfs_status s3bfs_dist_dedup(s3bfs_handle h, s3bfs_stream_t stream_) {
   s3bfs_status s = dist_check(h);
   if (s != S3BFS_OK) return s;
   cudaStream_t stream = (cudaStream_t)stream_;
-  CK(h, cudaMemsetAsync(h->P.status, 0, (size_t)h->P.p_max * h->P.dist_size * 8, stream));
-  k_dist_owner<<<h->num_sms * 8, 256, 0, stream>>>(h->P);
   k_dist_keep<<<h->P.p_max * h->P.dist_size, KD_THREADS, 0, stream>>>(h->P);
-  k_dist_publish<<<h->num_sms * 4, 256, 0, stream>>>(h->P);
   CK(h, cudaGetLastError());
   return S3BFS_OK;
 }
@@ -980,6 +999,15 @@ s3bfs_status s3bfs_dist_advance(s3bfs_handle h, s3bfs_stream_t stream_, int32_t 
   k_dist_advance<<<1, 32, 0, stream>>>(h->P);
   CK(h, cudaGetLastError());
   if (!done && !n_next) return S3BFS_OK;
+  return s3bfs_dist_status(h, stream_, done, n_next);
+}
+
+s3bfs_status s3bfs_dist_status(s3bfs_handle h, s3bfs_stream_t stream_, int32_t *done,
+                               int64_t *n_next) {
+  s3bfs_status s = dist_check(h);
+  if (s != S3BFS_OK) return s;
+  if (!done && !n_next) return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "nothing to read");
+  cudaStream_t stream = (cudaStream_t)stream_;
   if (!h->h_ctl) CK(h, cudaMallocHost((void **)&h->h_ctl, sizeof(Ctl)));
   CK(h, cudaMemcpyAsync(h->h_ctl, h->P.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, stream));
   CK(h, cudaStreamSynchronize(stream));

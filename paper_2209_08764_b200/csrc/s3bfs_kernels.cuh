@@ -105,6 +105,9 @@ namespace s3bfs {
 #ifndef S3BFS_KS_ONCHIP
 #define S3BFS_KS_ONCHIP 1  // k_small: Owner race in a shared-memory table (no L2 round trip)
 #endif
+#ifndef S3BFS_PDL
+#define S3BFS_PDL 1  // captured loop: programmatic dependent launch between chained kernels
+#endif
 #ifndef S3BFS_CHECK
 #define S3BFS_CHECK 0  // 1: bounds-checked build (every traversal index checked; trap + message)
 #endif
@@ -245,6 +248,7 @@ struct Params {
   int2 *p_rmeta[DIST_MAX];
   int2 *p_rtot[DIST_MAX];
   uint32_t *p_bm[DIST_MAX];
+  int4 *p_vinfo[DIST_MAX];      // peers' vertex records (the sender stores the Owner label)
   long long nnz;
   long long cand_cap;           // candidate buffer entries (bounds-checked build)
   int32_t col_vec;              // col is 16-byte aligned: vectorised loads allowed
@@ -254,6 +258,18 @@ struct Params {
 };
 
 // ---- PTX helpers ------------------------------------------------------------------------
+// Programmatic dependent launch (captured loop, S3BFS_PDL): every chained kernel lets its
+// successor launch at once (its CTAs become resident and wait), then waits for its own
+// predecessor to complete with memory visible (griddepcontrol.wait) before it reads the
+// control block.  A successor launches only after every CTA of this grid has started, so a
+// waiting grid never holds resources a running one still needs.  Outside a programmatic
+// edge (host loop, plain launches) both are no-ops.
+__device__ __forceinline__ void pdl_enter() {
+#if S3BFS_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -659,10 +675,13 @@ __global__ void k_policies(unsigned long long *out) {
 // discoverers that all saw an old tag store the same d and a valid parent and enqueue
 // duplicates; the Owner check keeps exactly one (R4).
 __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P) {
+  pdl_enter();
   Ctl *c = P.ctl;
   if (c->tier != TIER_LARGE) return;
   const int b = blockIdx.x;
   const int p_l = c->p_l;
+  if (P.dist_size > 1 && threadIdx.x < P.dist_size)  // NEXT-4: k_dist_keep's look-back words
+    P.status[b * P.dist_size + threadIdx.x] = 0ull;  // of this level (gridDim = P_max)
   if (b >= p_l) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n_l = c->n_l, chunk = c->chunk, cur = c->cur, wcap = c->wcap;
@@ -682,7 +701,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   const uint32_t tag_span = (uint32_t)(P.n - P.hub);  // ids in [hub, n): tag only
 
   if (tid == 0) {
-    P.status[b] = 0ull;  // reset k_compact's look-back word for this level
+    if (P.dist_size == 1) P.status[b] = 0ull;  // reset k_compact's look-back word
     if (b == 0) c->t_kx_begin = globaltimer();
   }
   const int E0 = c->e_lo + b * chunk;
@@ -897,7 +916,11 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
         if (d == dd) {
           const int k = s_dc[warp][dd] + __popc(md & lanemask_lt());
           S3_CHK(k, wcap);
-          P.p_recv[dd][P.rofs[P.dist_rank] + segbase + k] = make_int2(v, it.y);
+          const int slot = P.rofs[P.dist_rank] + segbase + k;
+          P.p_recv[dd][slot] = make_int2(v, it.y);
+          // Owner[v] <- slot in the owner's records (Fig1 L22; the benign race, plain stores
+          // from every rank that sends v: one label survives, the owner keeps that copy)
+          st_weak(owner_of(P.p_vinfo[dd], ((v >> 5) / P.dist_size) * 32 + (v & 31)), slot);
         }
         __syncwarp();
         if (lane == 0) s_dc[warp][dd] += __popc(md);
@@ -1034,6 +1057,7 @@ __device__ __forceinline__ void bm_publish(uint32_t *bm, bool keep, int v, int l
 // starts and its exclusive degree scan.  The last CTA to finish advances the control block
 // (Fig1 L9-L10, L15-L16).
 __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P) {
+  pdl_enter();
   Ctl *c = P.ctl;
   if (c->tier != TIER_LARGE) return;
   const int p_l = c->p_l;
@@ -1164,13 +1188,14 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
 // targets stay global ids), and their state (vinfo / lp / Owner in local slots).  Per level:
 //   k_explore (dist mode)  the local frontier's arcs; a target whose visited bit (replicated
 //                          bitmap, exact at level start) is clear goes as {v, parent} straight
-//                          into the receive segment of its owner (peer store over NVLink)
-//   k_dist_owner           Owner[v] <- the candidate's slot for every received candidate (Fig1
-//                          L22 on the owner: the race stays inside one GPU, plain stores)
-//   k_dist_keep            keep a candidate iff Owner[v] is its slot; d/parent, the owner's
-//                          bitmap words, and the next local frontier by the (kept, degree-sum)
-//                          look-back scan over (source rank, CTA) tiles (Fig1 L23-L29, L12-L15)
-//   k_dist_publish         the owner's updated bitmap words into every peer's replica
+//                          into the receive segment of its owner, and the segment slot into
+//                          the owner's Owner[v] (peer stores over NVLink; Fig1 L22's benign race
+//                          now spans the senders: plain stores, one label survives)
+//   k_dist_keep            keep a received candidate iff Owner[v] is its slot; d/parent, the
+//                          owner's bitmap words (atomicOr into its own and every peer's replica,
+//                          off the discovery path), and the next local frontier by the
+//                          (kept, degree-sum) look-back scan over (source rank, CTA) tiles
+//                          (Fig1 L23-L29, L12-L15)
 //   k_dist_advance         the level's totals over all ranks (each rank published its own into
 //                          every peer's rtot) decide the loop (Fig1 L9) and the local P_l
 // The exchange is peer memory (no collective carries data); the driver only orders the phases
@@ -1236,28 +1261,6 @@ __global__ void k_dist_init(Params P, int32_t s) {
   }
 }
 
-// Fig1 L22 on the owner: Owner[v] <- slot for every candidate received this level
-__global__ void k_dist_owner(Params P) {
-  const int lane = threadIdx.x & 31;
-  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  const int nwmax = P.p_max * KD_WARPS;
-  for (int s = 0; s < P.dist_size; ++s) {
-    const int2 m = P.rmeta[s];  // {wcap, p_l} of source s
-    const long long nseg = (long long)m.y * KD_WARPS;
-    for (long long g = gw; g < nseg; g += nw) {
-      const int cnt = P.rcnt[(long long)s * nwmax + g];
-      const long long base = P.rofs[s] + g * m.x;
-      for (int k = lane; k < cnt; k += 32) {
-        const int v = P.recv[base + k].x;
-        S3_CHK(v, P.n);
-        S3_CHK(dist_local(P, v), P.nloc);
-        st_weak(owner_of(P.vinfo, dist_local(P, v)), (int)(base + k));  // benign race
-      }
-    }
-  }
-}
-
 // keep iff Owner[v] == slot (Fig1 L22-L23); tiles = (source rank, source CTA) in start order
 __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_dist_keep(Params P) {
   Ctl *c = P.ctl;
@@ -1285,11 +1288,12 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_dist_keep(Params 
       if (k < cnt) {
         it = P.recv[base + k];
         lv = dist_local(P, it.x);
-        vi = ld_weak_v4(P.vinfo + lv);  // written by k_dist_owner (another launch)
+        vi = ld_weak_v4(P.vinfo + lv);  // Owner written by the senders' k_explore
       }
       const bool keep = k < cnt && vi.w == (int)(base + k);
       if (keep) P.lp[lv] = make_int2(new_level, it.y);  // d[v] <- l, parent (Fig1 L18)
-      bm_publish(P.bm, keep, it.x, lane);                 // this owner's bitmap words
+      for (int d = 0; d < P.dist_size; ++d)             // the owner's bitmap words, in its own
+        bm_publish(P.p_bm[d], keep, it.x, lane);         // replica and every peer's
       const unsigned mk = __ballot_sync(0xffffffffu, keep);
       if (keep) P.recv[base + kept + __popc(mk & lanemask_lt())].x = it.x;  // in place
       kept += __popc(mk);
@@ -1349,20 +1353,6 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_dist_keep(Params 
     c->tile_ctr = 0;
     __threadfence_system();
   }
-}
-
-// the owner's updated words of the replicated bitmap into every peer (plain stores: only the
-// owner writes a word, after its own atomicOr publications of this level have completed)
-__global__ void k_dist_publish(Params P) {
-  const int n_next = P.ctl->n_next;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n_next;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int w = P.kv[i] >> 5;
-    const uint32_t val = P.bm[w];
-    for (int d = 0; d < P.dist_size; ++d)
-      if (d != P.dist_rank) P.p_bm[d][w] = val;
-  }
-  __threadfence_system();
 }
 
 // Fig1 L9-L11, L15-L16 over all ranks: the global totals end the loop; the local ones size P_l
@@ -1560,14 +1550,17 @@ __device__ void tiny_levels(const Params &P, Ctl *c, int32_t *sf, int32_t *srs, 
 // are ordered for its own later reads by the CTA barrier (one SM), so multi-level operation
 // is safe.
 __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
+  pdl_enter();
   Ctl *c = P.ctl;
   if (c->tier != TIER_SMALL) return;
   extern __shared__ int32_t smem[];
   int32_t *sf = smem;                 // CurLevelVertices (caller ids)
   int32_t *srs = sf + KS_NCAP;        // internal row starts
   int32_t *sex = srs + KS_NCAP;       // exclusive degree scan, KS_NCAP + 1 entries
-  int32_t *cv = sex + KS_NCAP + 4;    // candidate per level-local edge (or -1); with
-  int32_t *cpv = cv + KS_ECAP;        // S3BFS_KS_ONCHIP this space is the Owner table
+#if !S3BFS_KS_ONCHIP
+  int32_t *cv = sex + KS_NCAP + 4;    // candidate per level-local edge (or -1)
+  int32_t *cpv = cv + KS_ECAP;        // its discoverer
+#endif                                // (S3BFS_KS_ONCHIP: this space is the Owner table)
   __shared__ int32_t s_wk[KS_THREADS / 32], s_wd[KS_THREADS / 32], s_wc[KS_THREADS / 32];
   __shared__ int32_t s_tot[3];
   __shared__ int32_t s_tiny[3];
@@ -1838,6 +1831,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
 // writes its kept vertices into every CTA's frontier (continuing) or into the global frontier
 // (the level that leaves the tier).  Same per-level contract as k_small / k_explore+k_compact.
 __global__ void __cluster_dims__(KC_CL, 1, 1) __launch_bounds__(KC_THREADS, 1) k_cluster(Params P) {
+  pdl_enter();
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   Ctl *c = P.ctl;
@@ -2043,6 +2037,7 @@ __global__ void __cluster_dims__(KC_CL, 1, 1) __launch_bounds__(KC_THREADS, 1) k
 // neighbour in the current frontier (a bitmap), stopping at the first one.  The frontier
 // bitmap is built from the frontier list when the previous level was top-down.
 __global__ void k_fb_clear(Params P) {
+  pdl_enter();
   Ctl *c = P.ctl;
   if (c->tier != TIER_BU) return;
   const long long gs = (long long)gridDim.x * blockDim.x;
@@ -2054,6 +2049,7 @@ __global__ void k_fb_clear(Params P) {
   for (long long i = g; i < nw4; i += gs) fb[i] = make_uint4(0, 0, 0, 0);
 }
 __global__ void k_fb_set(Params P) {
+  pdl_enter();
   Ctl *c = P.ctl;
   if (c->tier != TIER_BU || c->fb_valid) return;
   const int n_l = c->n_l;
@@ -2074,6 +2070,7 @@ __global__ void k_fb_set(Params P) {
 // words; found vertices are compacted into the next frontier list with the same decoupled
 // look-back (kept, degree-sum) scan as k_compact.
 __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params P) {
+  pdl_enter();
   Ctl *c = P.ctl;
   if (c->tier != TIER_BU) return;
   __shared__ int32_t s_k[KD_WARPS], s_d[KD_WARPS];
@@ -2239,6 +2236,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params 
 // parent[o] = its recorded parent (a caller id, R2).  Reads the internal records in caller
 // order; the caller's arrays are written exactly once, coalesced.
 __global__ void k_finalize(Params P) {
+  pdl_enter();
   const Ctl *c = P.ctl;
   int32_t *__restrict__ level = c->level_out;
   int32_t *__restrict__ parent = c->parent_out;

@@ -64,8 +64,12 @@ class DistRank:
     def publish(self, group) -> None:
         """Nothing to move: the dedup kernels stored the bitmap words and totals in the peers."""
 
-    def advance(self, group) -> tuple[bool, int]:
-        return _s.s3bfs_dist_advance(self.handle, self.stream)
+    def advance(self, group, wait: bool = True):
+        """Advance the level; with wait: (done, next frontier size over all ranks)."""
+        return _s.s3bfs_dist_advance(self.handle, self.stream, wait=wait)
+
+    def status(self) -> tuple[bool, int]:
+        return _s.s3bfs_dist_status(self.handle, self.stream)
 
     def end(self):
         _s.s3bfs_dist_end(self.handle, self.stream)

@@ -27,7 +27,7 @@ EXPORTED = ("s3bfs_create", "s3bfs_clone", "s3bfs_run", "s3bfs_destroy", "s3bfs_
             "s3bfs_last_error", "s3bfs_get_level_stats", "s3bfs_get_info", "s3bfs_get_kernel_times",
             "s3bfs_debug_exclusive_scan", "s3bfs_debug_find_start_points", "s3bfs_debug_timeline",
             "s3bfs_dist_export", "s3bfs_dist_connect", "s3bfs_dist_begin", "s3bfs_dist_explore",
-            "s3bfs_dist_dedup", "s3bfs_dist_advance", "s3bfs_dist_end")
+            "s3bfs_dist_dedup", "s3bfs_dist_advance", "s3bfs_dist_status", "s3bfs_dist_end")
 
 
 class S3BFSError(RuntimeError):
@@ -54,6 +54,7 @@ class DistPeer(ctypes.Structure):
     """s3bfs_dist_peer: a rank's exchange record (addresses + CUDA IPC handle)."""
     _fields_ = [("base", ctypes.c_uint64), ("recv", ctypes.c_uint64), ("rcnt", ctypes.c_uint64),
                 ("rmeta", ctypes.c_uint64), ("rtot", ctypes.c_uint64), ("bm", ctypes.c_uint64),
+                ("vinfo", ctypes.c_uint64),
                 ("ipc", ctypes.c_uint8 * 64), ("ipc_valid", ctypes.c_int32),
                 ("rank", ctypes.c_int32), ("size", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
@@ -118,6 +119,7 @@ def load(build_if_missing: bool = True):
     lib.s3bfs_dist_explore.argtypes = [vp, vp]
     lib.s3bfs_dist_dedup.argtypes = [vp, vp]
     lib.s3bfs_dist_advance.argtypes = [vp, vp, ctypes.POINTER(i32), ctypes.POINTER(ctypes.c_int64)]
+    lib.s3bfs_dist_status.argtypes = [vp, vp, ctypes.POINTER(i32), ctypes.POINTER(ctypes.c_int64)]
     lib.s3bfs_dist_end.argtypes = [vp, vp]
     for name in EXPORTED:
         if name != "s3bfs_status_string":
@@ -292,6 +294,14 @@ def s3bfs_dist_advance(handle, stream=None, wait: bool = True):
     done, n_next = ctypes.c_int32(), ctypes.c_int64()
     _check(load().s3bfs_dist_advance(handle, _stream(stream), ctypes.byref(done),
                                      ctypes.byref(n_next)), "s3bfs_dist_advance", handle)
+    return bool(done.value), int(n_next.value)
+
+
+def s3bfs_dist_status(handle, stream=None):
+    """(done, next frontier size over all ranks) of the last advance; synchronises."""
+    done, n_next = ctypes.c_int32(), ctypes.c_int64()
+    _check(load().s3bfs_dist_status(handle, _stream(stream), ctypes.byref(done),
+                                    ctypes.byref(n_next)), "s3bfs_dist_status", handle)
     return bool(done.value), int(n_next.value)
 
 
