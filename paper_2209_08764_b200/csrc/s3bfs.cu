@@ -206,8 +206,6 @@ s3bfs_status build_dist(s3bfs_ctx *h, cudaStream_t st, int nloc) {
   Params &P = h->P;
   const int G = P.dist_size, r = P.dist_rank, n = h->n;
   P.nloc = nloc;
-  P.tag_pct = -1;  // the visited test goes through the replicated bitmap: a rank's discovery
-  P.hub = n;       // tags know only its own sends, never another rank's vertices
   const int32_t *ro = h->ro_int, *col = P.col;
   const int grid = h->num_sms * 8;
   AsyncTmp cnt_b(st), deg_b(st), tmp_b(st);
@@ -411,21 +409,7 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
     auto add = [&](void *fn, int grid, int block, size_t smem) -> s3bfs_status {
       cudaGraphNode_t nd;
       cudaKernelNodeParams kp = kparams(fn, grid, block, smem);
-      if (!S3BFS_PDL || !prev) {
-        CK(h, cudaGraphAddKernelNode(&nd, bg, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
-      } else {  // kernel -> kernel: programmatic edge (the kernels' pdl_enter, PTX helpers)
-        cudaGraphNodeParams np = {};
-        np.type = cudaGraphNodeTypeKernel;
-        np.kernel.func = kp.func;
-        np.kernel.gridDim = kp.gridDim;
-        np.kernel.blockDim = kp.blockDim;
-        np.kernel.sharedMemBytes = kp.sharedMemBytes;
-        np.kernel.kernelParams = kp.kernelParams;
-        cudaGraphEdgeData ed = {};
-        ed.from_port = cudaGraphKernelNodePortProgrammatic;
-        ed.type = cudaGraphDependencyTypeProgrammatic;
-        CK(h, cudaGraphAddNode_v2(&nd, bg, &prev, &ed, 1, &np));
-      }
+      CK(h, cudaGraphAddKernelNode(&nd, bg, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
       prev = nd;
       return S3BFS_OK;
     };
@@ -640,8 +624,6 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   const size_t o_bustatus = take((size_t)(bu_tiles + 1) * 8);
   const size_t o_ctl = take(sizeof(Ctl));
   const size_t o_stats = take((size_t)stats_cap * sizeof(s3bfs_level_stat));
-  // NEXT-4 (dist_size > 1 only): internal ids of the kept vertices (publication of bitmap words)
-  const size_t o_kv = take(dist_size > 1 ? (size_t)nv * 4 : 0);
   h->ws_bytes = off;
   if ((e = cudaMalloc(&h->ws, h->ws_bytes)) != cudaSuccess) return bail(cuda_fail(h, e, "cudaMalloc(workspace)"));
   char *base = (char *)h->ws;
@@ -694,10 +676,10 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   P.do_beta = h->opt.do_beta != 0 ? h->opt.do_beta : 24;
   P.n_scan = n;
   P.nnz = nnz;
+  P.nnz_all = nnz;
   P.cand_cap = h->cand_cap;
   P.dist_size = dist_size;
   P.dist_rank = dist_rank;
-  P.kv = dist_size > 1 ? (int32_t *)(base + o_kv) : nullptr;
   P.nloc = n;
   if (share) {  // a clone: the prepared graph is the source handle's; vertex records copied
     P.col = share->P.col;
@@ -986,7 +968,7 @@ s3bfs_status s3bfs_dist_dedup(s3bfs_handle h, s3bfs_stream_t stream_) {
   s3bfs_status s = dist_check(h);
   if (s != S3BFS_OK) return s;
   cudaStream_t stream = (cudaStream_t)stream_;
-  k_dist_keep<<<h->P.p_max * h->P.dist_size, KD_THREADS, 0, stream>>>(h->P);
+  k_dist_keep<<<h->P.p_max, KD_THREADS, 0, stream>>>(h->P);
   CK(h, cudaGetLastError());
   return S3BFS_OK;
 }

@@ -105,9 +105,6 @@ namespace s3bfs {
 #ifndef S3BFS_KS_ONCHIP
 #define S3BFS_KS_ONCHIP 1  // k_small: Owner race in a shared-memory table (no L2 round trip)
 #endif
-#ifndef S3BFS_PDL
-#define S3BFS_PDL 1  // captured loop: programmatic dependent launch between chained kernels
-#endif
 #ifndef S3BFS_CHECK
 #define S3BFS_CHECK 0  // 1: bounds-checked build (every traversal index checked; trap + message)
 #endif
@@ -141,6 +138,7 @@ constexpr int KS_THREADS = 1024;                // k_small CTA size
 constexpr int KS_ECAP = S3BFS_KS_ONCHIP ? 4096 : 8192;  // T0 maximum (edges per tier-0 level)
 constexpr int KS_TAB_BITS = 14;                 // k_small on-chip Owner table: 2^14 entries
 constexpr int KS_TAB = 1 << KS_TAB_BITS;
+static_assert(KS_ECAP <= KS_TAB, "k_small Owner-table entries hold a level-local edge index");
 constexpr int KS_NCAP = KS_ECAP;                // frontier capacity of tier 0 (kept <= e_l)
 constexpr int KS_IPT = KS_ECAP / KS_THREADS;    // dedup items per thread
 constexpr int SCAN_THREADS = 512;
@@ -241,7 +239,6 @@ struct Params {
   int32_t *rcnt;                // per (source rank, source warp): candidates in that segment
   int2 *rmeta;                  // per source rank: {wcap, p_l} of the level
   int2 *rtot;                   // per source rank: {n_next, e_next} of the level
-  int32_t *kv;                  // internal ids of this rank's kept vertices (frontier order)
   int32_t rofs[DIST_MAX + 1];   // receive block offsets (identical on every rank)
   int2 *p_recv[DIST_MAX];       // peers' (and this rank's) arrays, mapped into this process
   int32_t *p_rcnt[DIST_MAX];
@@ -251,6 +248,7 @@ struct Params {
   int4 *p_vinfo[DIST_MAX];      // peers' vertex records (the sender stores the Owner label)
   long long nnz;
   long long cand_cap;           // candidate buffer entries (bounds-checked build)
+  long long nnz_all;            // arcs of the whole graph (= nnz on one GPU; NEXT-4: all ranks')
   int32_t col_vec;              // col is 16-byte aligned: vectorised loads allowed
   int32_t use_graph;
   unsigned long long h_while, h_tier;  // cudaGraphConditionalHandle values (WHILE; SWITCH on
@@ -258,18 +256,6 @@ struct Params {
 };
 
 // ---- PTX helpers ------------------------------------------------------------------------
-// Programmatic dependent launch (captured loop, S3BFS_PDL): every chained kernel lets its
-// successor launch at once (its CTAs become resident and wait), then waits for its own
-// predecessor to complete with memory visible (griddepcontrol.wait) before it reads the
-// control block.  A successor launches only after every CTA of this grid has started, so a
-// waiting grid never holds resources a running one still needs.  Outside a programmatic
-// edge (host loop, plain launches) both are no-ops.
-__device__ __forceinline__ void pdl_enter() {
-#if S3BFS_PDL
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-#endif
-}
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -595,7 +581,7 @@ __device__ void decide_tier(const Params &P, Ctl *c, int32_t n_l, int32_t e_l) {
   // k_explore's visited test: tag mode while few arcs end at visited vertices (m_visited =
   // degrees of all visited vertices, the frontier included; arc ends for a symmetric graph)
   c->probe_tags = P.tag_pct >= 0 &&
-                  (double)c->m_visited * 100.0 < (double)P.nnz * (double)P.tag_pct;
+                  (double)c->m_visited * 100.0 < (double)P.nnz_all * (double)P.tag_pct;
   c->tier = TIER_LARGE;
   c->p_l = (int32_t)p_l;
   c->chunk = (int32_t)chunk;
@@ -675,13 +661,12 @@ __global__ void k_policies(unsigned long long *out) {
 // discoverers that all saw an old tag store the same d and a valid parent and enqueue
 // duplicates; the Owner check keeps exactly one (R4).
 __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P) {
-  pdl_enter();
   Ctl *c = P.ctl;
   if (c->tier != TIER_LARGE) return;
   const int b = blockIdx.x;
   const int p_l = c->p_l;
-  if (P.dist_size > 1 && threadIdx.x < P.dist_size)  // NEXT-4: k_dist_keep's look-back words
-    P.status[b * P.dist_size + threadIdx.x] = 0ull;  // of this level (gridDim = P_max)
+  if (P.dist_size > 1 && threadIdx.x == 0)  // NEXT-4: k_dist_keep's look-back word of tile b
+    P.status[b] = 0ull;                      // (gridDim = P_max in dist mode)
   if (b >= p_l) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n_l = c->n_l, chunk = c->chunk, cur = c->cur, wcap = c->wcap;
@@ -1057,7 +1042,6 @@ __device__ __forceinline__ void bm_publish(uint32_t *bm, bool keep, int v, int l
 // starts and its exclusive degree scan.  The last CTA to finish advances the control block
 // (Fig1 L9-L10, L15-L16).
 __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P) {
-  pdl_enter();
   Ctl *c = P.ctl;
   if (c->tier != TIER_LARGE) return;
   const int p_l = c->p_l;
@@ -1261,43 +1245,52 @@ __global__ void k_dist_init(Params P, int32_t s) {
   }
 }
 
-// keep iff Owner[v] == slot (Fig1 L22-L23); tiles = (source rank, source CTA) in start order
+// keep iff Owner[v] == slot (Fig1 L22-L23).  Tile b (start order) = the segments of every source
+// rank's CTA b: warp w handles segment b * 16 + w of each source in turn
 __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_dist_keep(Params P) {
   Ctl *c = P.ctl;
   __shared__ int32_t s_k[KD_WARPS], s_d[KD_WARPS];
+  __shared__ int32_t s_kc[KD_WARPS][DIST_MAX];  // kept per (warp, source), pass 1 -> pass 2
   __shared__ int s_last, s_tile;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nxt = c->cur ^ 1, new_level = c->level + 1;
-  const int nt = P.dist_size * P.p_max;
+  const int nt = P.p_max;
   const int nwmax = P.p_max * KD_WARPS;
   if (tid == 0) s_tile = (int)atomicAdd(&c->tile_ctr, 1u);  // look-back order = start order
   __syncthreads();
   const int t = s_tile;
   if (t < nt) {
-    const int src = t / P.p_max, b = t - src * P.p_max;
-    const int2 m = P.rmeta[src];
-    const int gseg = b * KD_WARPS + warp;
-    const int cnt = b < m.y ? P.rcnt[(long long)src * nwmax + gseg] : 0;
-    const long long base = P.rofs[src] + (long long)gseg * m.x;
+    const int gseg = t * KD_WARPS + warp;
     int kept = 0, dsum = 0;
-    for (int k0 = 0; k0 < cnt; k0 += 32) {
-      const int k = k0 + lane;
-      int2 it = make_int2(-1, 0);
-      int4 vi = make_int4(0, 0, 0, -1);
-      int lv = 0;
-      if (k < cnt) {
-        it = P.recv[base + k];
-        lv = dist_local(P, it.x);
-        vi = ld_weak_v4(P.vinfo + lv);  // Owner written by the senders' k_explore
+    for (int src = 0; src < P.dist_size; ++src) {
+      const int2 m = P.rmeta[src];
+      const int cnt = t < m.y ? P.rcnt[(long long)src * nwmax + gseg] : 0;
+      const long long base = P.rofs[src] + (long long)gseg * m.x;
+      int ks = 0;
+      for (int k0 = 0; k0 < cnt; k0 += 32) {
+        const int k = k0 + lane;
+        int2 it = make_int2(-1, 0);
+        int4 vi = make_int4(0, 0, 0, -1);
+        int lv = 0;
+        if (k < cnt) {
+          it = P.recv[base + k];
+          lv = dist_local(P, it.x);
+          vi = ld_weak_v4(P.vinfo + lv);  // Owner written by the senders' k_explore
+        }
+        // the surviving label's copy, unless v was visited in an earlier level: a sender's tag
+        // mode knows only its own sends, so it may send a vertex another rank found before
+        const bool keep = k < cnt && vi.w == (int)(base + k) &&
+                          !((__ldcg(P.bm + (it.x >> 5)) >> (it.x & 31)) & 1u);
+        if (keep) P.lp[lv] = make_int2(new_level, it.y);  // d[v] <- l, parent (Fig1 L18)
+        for (int d = 0; d < P.dist_size; ++d)             // the owner's bitmap words, in its own
+          bm_publish(P.p_bm[d], keep, it.x, lane);         // replica and every peer's
+        const unsigned mk = __ballot_sync(0xffffffffu, keep);
+        if (keep) P.recv[base + ks + __popc(mk & lanemask_lt())].x = it.x;  // in place
+        ks += __popc(mk);
+        dsum += keep ? vi.y : 0;
       }
-      const bool keep = k < cnt && vi.w == (int)(base + k);
-      if (keep) P.lp[lv] = make_int2(new_level, it.y);  // d[v] <- l, parent (Fig1 L18)
-      for (int d = 0; d < P.dist_size; ++d)             // the owner's bitmap words, in its own
-        bm_publish(P.p_bm[d], keep, it.x, lane);         // replica and every peer's
-      const unsigned mk = __ballot_sync(0xffffffffu, keep);
-      if (keep) P.recv[base + kept + __popc(mk & lanemask_lt())].x = it.x;  // in place
-      kept += __popc(mk);
-      dsum += keep ? vi.y : 0;
+      if (lane == 0) s_kc[warp][src] = ks;
+      kept += ks;
     }
     dsum = warp_sum(dsum);
     if (lane == 0) { s_k[warp] = kept; s_d[warp] = dsum; }
@@ -1321,24 +1314,28 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_dist_keep(Params 
     }
     __syncthreads();
     int koff = s_k[warp], doff = s_d[warp];
-    for (int k0 = 0; k0 < kept; k0 += 32) {  // pass 2: the next local frontier (Fig1 L25-L29)
-      const int k = k0 + lane;
-      int v = 0;
-      int4 vi = make_int4(0, 0, 0, 0);
-      if (k < kept) {
-        v = P.recv[base + k].x;
-        vi = __ldg(P.vinfo + dist_local(P, v));
+    for (int src = 0; src < P.dist_size; ++src) {  // pass 2: the next local frontier (L25-L29)
+      const int ks = s_kc[warp][src];
+      const long long base = P.rofs[src] + (long long)gseg * P.rmeta[src].x;
+      for (int k0 = 0; k0 < ks; k0 += 32) {
+        const int k = k0 + lane;
+        int v = 0;
+        int4 vi = make_int4(0, 0, 0, 0);
+        if (k < ks) {
+          v = P.recv[base + k].x;
+          vi = __ldg(P.vinfo + dist_local(P, v));
+        }
+        const int d = k < ks ? vi.y : 0;
+        const int inc = warp_incl_scan(d);
+        if (k < ks) {
+          S3_CHK(koff + k, P.nloc);
+          P.f[nxt][koff + k] = vi.z;
+          P.frs[nxt][koff + k] = vi.x;
+          P.fex[nxt][koff + k] = doff + inc - d;
+        }
+        doff += __shfl_sync(0xffffffffu, inc, 31);
       }
-      const int d = k < kept ? vi.y : 0;
-      const int inc = warp_incl_scan(d);
-      if (k < kept) {
-        S3_CHK(koff + k, P.nloc);
-        P.f[nxt][koff + k] = vi.z;
-        P.frs[nxt][koff + k] = vi.x;
-        P.fex[nxt][koff + k] = doff + inc - d;
-        P.kv[koff + k] = v;
-      }
-      doff += __shfl_sync(0xffffffffu, inc, 31);
+      koff += ks;
     }
   }
   __threadfence();
@@ -1370,6 +1367,7 @@ __global__ void k_dist_advance(Params P) {
   c->t_prev = tt;
   c->g_n_next = (int32_t)gn;
   c->g_e_next = (int32_t)(ge < 0x7fffffff ? ge : 0x7fffffff);
+  c->m_visited += ge;  // arcs of all visited vertices (all ranks): k_explore's tag-mode rule
   c->level = c->level + 1;
   c->cur ^= 1;
   if (gn == 0) {
@@ -1550,7 +1548,6 @@ __device__ void tiny_levels(const Params &P, Ctl *c, int32_t *sf, int32_t *srs, 
 // are ordered for its own later reads by the CTA barrier (one SM), so multi-level operation
 // is safe.
 __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
-  pdl_enter();
   Ctl *c = P.ctl;
   if (c->tier != TIER_SMALL) return;
   extern __shared__ int32_t smem[];
@@ -1831,7 +1828,6 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
 // writes its kept vertices into every CTA's frontier (continuing) or into the global frontier
 // (the level that leaves the tier).  Same per-level contract as k_small / k_explore+k_compact.
 __global__ void __cluster_dims__(KC_CL, 1, 1) __launch_bounds__(KC_THREADS, 1) k_cluster(Params P) {
-  pdl_enter();
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   Ctl *c = P.ctl;
@@ -2037,7 +2033,6 @@ __global__ void __cluster_dims__(KC_CL, 1, 1) __launch_bounds__(KC_THREADS, 1) k
 // neighbour in the current frontier (a bitmap), stopping at the first one.  The frontier
 // bitmap is built from the frontier list when the previous level was top-down.
 __global__ void k_fb_clear(Params P) {
-  pdl_enter();
   Ctl *c = P.ctl;
   if (c->tier != TIER_BU) return;
   const long long gs = (long long)gridDim.x * blockDim.x;
@@ -2049,7 +2044,6 @@ __global__ void k_fb_clear(Params P) {
   for (long long i = g; i < nw4; i += gs) fb[i] = make_uint4(0, 0, 0, 0);
 }
 __global__ void k_fb_set(Params P) {
-  pdl_enter();
   Ctl *c = P.ctl;
   if (c->tier != TIER_BU || c->fb_valid) return;
   const int n_l = c->n_l;
@@ -2070,7 +2064,6 @@ __global__ void k_fb_set(Params P) {
 // words; found vertices are compacted into the next frontier list with the same decoupled
 // look-back (kept, degree-sum) scan as k_compact.
 __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params P) {
-  pdl_enter();
   Ctl *c = P.ctl;
   if (c->tier != TIER_BU) return;
   __shared__ int32_t s_k[KD_WARPS], s_d[KD_WARPS];
@@ -2236,7 +2229,6 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params 
 // parent[o] = its recorded parent (a caller id, R2).  Reads the internal records in caller
 // order; the caller's arrays are written exactly once, coalesced.
 __global__ void k_finalize(Params P) {
-  pdl_enter();
   const Ctl *c = P.ctl;
   int32_t *__restrict__ level = c->level_out;
   int32_t *__restrict__ parent = c->parent_out;

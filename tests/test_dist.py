@@ -114,8 +114,11 @@ def _gpu_ranks(g, G, **kw):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("G", [2, 3])
-@pytest.mark.parametrize("kw", [dict(), dict(reorder=-1), dict(debug_poison=1, edges_per_cta=1)],
-                         ids=["default", "no-reorder", "poison-grain1"])
+@pytest.mark.parametrize("kw", [dict(), dict(reorder=-1), dict(debug_poison=1, edges_per_cta=1),
+                                dict(hub_vertices=1, tag_mode_pct=101),
+                                dict(hub_vertices=-1, tag_mode_pct=-1)],
+                         ids=["default", "no-reorder", "poison-grain1", "tags-always",
+                              "bitmap-only"])
 def test_gpu_loopback_small(G, kw):
     import paper_2209_08764_b200.dist as pd
     for g in _graphs():
