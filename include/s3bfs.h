@@ -245,6 +245,13 @@ s3bfs_status s3bfs_dist_dedup(s3bfs_handle h, s3bfs_stream_t stream);
 s3bfs_status s3bfs_dist_advance(s3bfs_handle h, s3bfs_stream_t stream, int32_t *done,
                                 int64_t *n_next);
 
+/* Advance without a host round trip: enqueued on `stream`, and the advance writes -1 into
+ * *flag once no rank has a next frontier, else the next frontier's size over all ranks.  flag:
+ * int64 the device can write, e.g. pinned host memory (read it after an event recorded behind
+ * this call).  Calls after the end are no-ops (every s3bfs_dist_* kernel checks the level's
+ * state), so a driver may enqueue a few levels ahead and check the flags late. */
+s3bfs_status s3bfs_dist_advance_flag(s3bfs_handle h, s3bfs_stream_t stream, int64_t *flag);
+
 /* Synchronise `stream` and read the last advance: *done = 1 when no rank has a next frontier,
  * *n_next = the next frontier's size over all ranks (either may be NULL, not both). */
 s3bfs_status s3bfs_dist_status(s3bfs_handle h, s3bfs_stream_t stream, int32_t *done,

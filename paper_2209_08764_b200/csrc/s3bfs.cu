@@ -420,7 +420,7 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
       } else if (k == 'C') {
         r = add((void *)k_cluster, KC_CL, KC_THREADS, h->kc_smem);
       } else if (k == 'T') {
-        r = add((void *)k_explore, h->P.p_max, KD_THREADS, 0);
+        r = add((void *)k_explore<false>, h->P.p_max, KD_THREADS, 0);
         if (r == S3BFS_OK) r = add((void *)k_compact, h->P.p_max, KD_THREADS, 0);
       } else {  // 'B'
         r = add((void *)k_fb_clear, h->num_sms * 4, 256, 0);
@@ -553,7 +553,7 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
 
   // ---- (f) tunables ----
   int occ_x = 0, occ_c = 0;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_x, k_explore, KD_THREADS, 0)) != cudaSuccess)
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_x, k_explore<false>, KD_THREADS, 0)) != cudaSuccess)
     return bail(cuda_fail(h, e, "occupancy(k_explore)"));
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, k_compact, KD_THREADS, 0)) != cudaSuccess)
     return bail(cuda_fail(h, e, "occupancy(k_compact)"));
@@ -856,7 +856,7 @@ s3bfs_status s3bfs_run(s3bfs_handle h, int32_t source, int32_t *level, int32_t *
       k_bottom_up<<<h->P.p_max, KD_THREADS, 0, stream>>>(h->P);
       if (h->time_kernels) CK(h, cudaEventRecord(h->ev[1], stream));
     } else {
-      k_explore<<<c.p_l, KD_THREADS, 0, stream>>>(h->P);
+      k_explore<false><<<c.p_l, KD_THREADS, 0, stream>>>(h->P);
       if (h->time_kernels) CK(h, cudaEventRecord(h->ev[1], stream));
       k_compact<<<c.p_l, KD_THREADS, 0, stream>>>(h->P);
       if (h->time_kernels) CK(h, cudaEventRecord(h->ev[2], stream));
@@ -959,7 +959,7 @@ s3bfs_status s3bfs_dist_explore(s3bfs_handle h, s3bfs_stream_t stream_) {
   s3bfs_status s = dist_check(h);
   if (s != S3BFS_OK) return s;
   // P_max CTAs: the level's P_l <= P_max is read on the device (surplus CTAs return at once)
-  k_explore<<<h->P.p_max, KD_THREADS, 0, (cudaStream_t)stream_>>>(h->P);
+  k_explore<true><<<h->P.p_max, KD_THREADS, 0, (cudaStream_t)stream_>>>(h->P);
   CK(h, cudaGetLastError());
   return S3BFS_OK;
 }
@@ -978,10 +978,19 @@ s3bfs_status s3bfs_dist_advance(s3bfs_handle h, s3bfs_stream_t stream_, int32_t 
   s3bfs_status s = dist_check(h);
   if (s != S3BFS_OK) return s;
   cudaStream_t stream = (cudaStream_t)stream_;
-  k_dist_advance<<<1, 32, 0, stream>>>(h->P);
+  k_dist_advance<<<1, 32, 0, stream>>>(h->P, nullptr);
   CK(h, cudaGetLastError());
   if (!done && !n_next) return S3BFS_OK;
   return s3bfs_dist_status(h, stream_, done, n_next);
+}
+
+s3bfs_status s3bfs_dist_advance_flag(s3bfs_handle h, s3bfs_stream_t stream_, int64_t *flag) {
+  s3bfs_status s = dist_check(h);
+  if (s != S3BFS_OK) return s;
+  if (!flag) return fail(h, S3BFS_ERR_INVALID_ARGUMENT, "flag is NULL");
+  k_dist_advance<<<1, 32, 0, (cudaStream_t)stream_>>>(h->P, (long long *)flag);
+  CK(h, cudaGetLastError());
+  return S3BFS_OK;
 }
 
 s3bfs_status s3bfs_dist_status(s3bfs_handle h, s3bfs_stream_t stream_, int32_t *done,

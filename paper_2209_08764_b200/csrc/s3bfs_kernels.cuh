@@ -660,12 +660,15 @@ __global__ void k_policies(unsigned long long *out) {
 // slot, cand[slot] = v -- plain stores, the paper's benign race, no atomics.  Racing
 // discoverers that all saw an old tag store the same d and a valid parent and enqueue
 // duplicates; the Owner check keeps exactly one (R4).
+// DIST = NEXT-4's rank kernel (candidates routed to owners); the single-GPU kernel is
+// k_explore<false> and carries none of that code
+template <bool DIST>
 __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P) {
   Ctl *c = P.ctl;
   if (c->tier != TIER_LARGE) return;
   const int b = blockIdx.x;
   const int p_l = c->p_l;
-  if (P.dist_size > 1 && threadIdx.x == 0)  // NEXT-4: k_dist_keep's look-back word of tile b
+  if (DIST && threadIdx.x == 0)  // NEXT-4: k_dist_keep's look-back word of tile b
     P.status[b] = 0ull;                      // (gridDim = P_max in dist mode)
   if (b >= p_l) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -686,7 +689,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   const uint32_t tag_span = (uint32_t)(P.n - P.hub);  // ids in [hub, n): tag only
 
   if (tid == 0) {
-    if (P.dist_size == 1) P.status[b] = 0ull;  // reset k_compact's look-back word
+    if (!DIST) P.status[b] = 0ull;  // reset k_compact's look-back word
     if (b == 0) c->t_kx_begin = globaltimer();
   }
   const int E0 = c->e_lo + b * chunk;
@@ -860,8 +863,8 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   // 2 % of its targets, which otherwise cost every lane the claim and discovery code of
   // every flagged group (ncu: 45 % of the heavy level's instructions, profiles/).
   __shared__ int2 s_q[KD_WARPS][KQ_CAP];
-  __shared__ int32_t s_dc[KD_WARPS][DIST_MAX];  // NEXT-4: candidates per destination rank
-  if (P.dist_size > 1) {
+  __shared__ int32_t s_dc[DIST ? KD_WARPS : 1][DIST_MAX];  // NEXT-4: per destination rank
+  if (DIST) {
     if (lane < DIST_MAX) s_dc[warp][lane] = 0;
     __syncwarp();
   }
@@ -878,7 +881,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
     if (valid && it.x < 0) cl = ld_cg_u8(claim + cs);  // Fig1 L18: already claimed this level?
     const bool disc = valid && cl == 0;
     const unsigned m = __ballot_sync(0xffffffffu, disc);
-    if (P.dist_size == 1) {
+    if (!DIST) {
       if (disc) {  // EXPLORE-VERTEX's discovery: plain stores, the benign race (R4)
         const int slot = segbase + wcount + __popc(m & lanemask_lt());
         S3_CHK(v, P.n);
@@ -997,7 +1000,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
 #endif
   S3_CHK(segbase + wcount, P.cand_cap);
   if (lane == 0) P.wcnt[b * KD_WARPS + warp] = wcount;
-  if (P.dist_size > 1) {  // NEXT-4: segment counts and the level's {wcap, p_l} to every owner
+  if (DIST) {  // NEXT-4: segment counts and the level's {wcap, p_l} to every owner
     __syncwarp();
     const int gw = b * KD_WARPS + warp;
     if (lane < P.dist_size)
@@ -1249,6 +1252,7 @@ __global__ void k_dist_init(Params P, int32_t s) {
 // rank's CTA b: warp w handles segment b * 16 + w of each source in turn
 __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_dist_keep(Params P) {
   Ctl *c = P.ctl;
+  if (c->tier != TIER_LARGE) return;  // a level enqueued past the end of the traversal
   __shared__ int32_t s_k[KD_WARPS], s_d[KD_WARPS];
   __shared__ int32_t s_kc[KD_WARPS][DIST_MAX];  // kept per (warp, source), pass 1 -> pass 2
   __shared__ int s_last, s_tile;
@@ -1353,9 +1357,16 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_dist_keep(Params 
 }
 
 // Fig1 L9-L11, L15-L16 over all ranks: the global totals end the loop; the local ones size P_l
-__global__ void k_dist_advance(Params P) {
+// flag (optional, e.g. mapped pinned host memory): -1 once the traversal is done, else the
+// next frontier's size over all ranks -- the driver reads it a few levels late, so levels are
+// enqueued without a host round trip (levels enqueued past the end are no-ops)
+__global__ void k_dist_advance(Params P, long long *flag) {
   if (threadIdx.x != 0) return;
   Ctl *c = P.ctl;
+  if (c->tier == TIER_DONE) {
+    if (flag) *(volatile long long *)flag = -1;
+    return;
+  }
   long long gn = 0, ge = 0;
   for (int s = 0; s < P.dist_size; ++s) {
     const int32_t *t = reinterpret_cast<const int32_t *>(P.rtot + s);
@@ -1374,8 +1385,10 @@ __global__ void k_dist_advance(Params P) {
     c->n_l = 0;
     c->e_l = 0;
     c->tier = TIER_DONE;
+    if (flag) *(volatile long long *)flag = -1;
     return;
   }
+  if (flag) *(volatile long long *)flag = gn;
   decide_tier(P, c, c->n_next, c->e_next);
   if (c->tier == TIER_DONE) {  // no local work this level: one idle CTA keeps the protocol
     c->tier = TIER_LARGE;

@@ -68,6 +68,11 @@ class DistRank:
         """Advance the level; with wait: (done, next frontier size over all ranks)."""
         return _s.s3bfs_dist_advance(self.handle, self.stream, wait=wait)
 
+    def advance_flag(self, flag_ptr: int) -> None:
+        """Advance without a host round trip; the device writes -1 (done) or the next frontier
+        size over all ranks into the int64 at flag_ptr (pinned host memory)."""
+        _s.s3bfs_dist_advance_flag(self.handle, flag_ptr, self.stream)
+
     def status(self) -> tuple[bool, int]:
         return _s.s3bfs_dist_status(self.handle, self.stream)
 
@@ -145,12 +150,21 @@ def _combine(outs, group):
     return [(lv_t, pa_t)]
 
 
-def traverse(ranks: list, source: int, group=None) -> list:
+def traverse(ranks: list, source: int, group=None, lag: int = 2) -> list:
     """Run one traversal from `source`; returns [(level, parent)] (the full answer) for the
     local ranks.  Every rank of the job must call this with the same source; the loop ends on
-    every rank at the same level (the totals over all ranks decide)."""
+    every rank at the same level (the totals over all ranks decide).
+
+    Library ranks: the levels are enqueued without a host round trip -- each level's advance
+    writes its termination flag into pinned host memory and the host reads the flag of the
+    level `lag` levels back (behind a CUDA event), so up to `lag` levels past the end are
+    enqueued; they are no-ops on the device.  Stand-ins without advance_flag advance with
+    a host read per level."""
     for r in ranks:
         r.begin(source)
+    if all(hasattr(r, "advance_flag") for r in ranks):
+        _levels_flagged(ranks, group, max(lag, 0))
+        return _combine([r.end() for r in ranks], group)
     levels = 0
     while True:
         for r in ranks:
@@ -171,3 +185,37 @@ def traverse(ranks: list, source: int, group=None) -> list:
         if done.pop():
             break
     return _combine([r.end() for r in ranks], group)
+
+
+def _levels_flagged(ranks: list, group, lag: int) -> None:
+    import torch
+    slots = torch.zeros((lag + 1, len(ranks)), dtype=torch.int64).pin_memory()
+    pending = []  # (level, event) whose flags are not read yet
+    lv = 0
+    while True:
+        for r in ranks:
+            r.explore()
+        for r in ranks:
+            r.exchange(group)
+        _barrier(ranks, group)
+        for r in ranks:
+            r.dedup()
+        for r in ranks:
+            r.publish(group)
+        _barrier(ranks, group)
+        k = lv % (lag + 1)
+        for i, r in enumerate(ranks):
+            r.advance_flag(slots[k, i].data_ptr())
+        ev = torch.cuda.Event()
+        ev.record()
+        pending.append((lv, ev))
+        lv += 1
+        if len(pending) > lag:
+            old, e = pending.pop(0)
+            e.synchronize()
+            flags = slots[old % (lag + 1)].tolist()
+            done = {f == -1 for f in flags}
+            if len(done) != 1:
+                raise RuntimeError("ranks disagree on termination")
+            if done.pop():
+                return

@@ -27,7 +27,8 @@ EXPORTED = ("s3bfs_create", "s3bfs_clone", "s3bfs_run", "s3bfs_destroy", "s3bfs_
             "s3bfs_last_error", "s3bfs_get_level_stats", "s3bfs_get_info", "s3bfs_get_kernel_times",
             "s3bfs_debug_exclusive_scan", "s3bfs_debug_find_start_points", "s3bfs_debug_timeline",
             "s3bfs_dist_export", "s3bfs_dist_connect", "s3bfs_dist_begin", "s3bfs_dist_explore",
-            "s3bfs_dist_dedup", "s3bfs_dist_advance", "s3bfs_dist_status", "s3bfs_dist_end")
+            "s3bfs_dist_dedup", "s3bfs_dist_advance", "s3bfs_dist_advance_flag", "s3bfs_dist_status",
+            "s3bfs_dist_end")
 
 
 class S3BFSError(RuntimeError):
@@ -119,6 +120,7 @@ def load(build_if_missing: bool = True):
     lib.s3bfs_dist_explore.argtypes = [vp, vp]
     lib.s3bfs_dist_dedup.argtypes = [vp, vp]
     lib.s3bfs_dist_advance.argtypes = [vp, vp, ctypes.POINTER(i32), ctypes.POINTER(ctypes.c_int64)]
+    lib.s3bfs_dist_advance_flag.argtypes = [vp, vp, vp]
     lib.s3bfs_dist_status.argtypes = [vp, vp, ctypes.POINTER(i32), ctypes.POINTER(ctypes.c_int64)]
     lib.s3bfs_dist_end.argtypes = [vp, vp]
     for name in EXPORTED:
@@ -295,6 +297,13 @@ def s3bfs_dist_advance(handle, stream=None, wait: bool = True):
     _check(load().s3bfs_dist_advance(handle, _stream(stream), ctypes.byref(done),
                                      ctypes.byref(n_next)), "s3bfs_dist_advance", handle)
     return bool(done.value), int(n_next.value)
+
+
+def s3bfs_dist_advance_flag(handle, flag_ptr: int, stream=None) -> None:
+    """Enqueue the advance; it writes -1 (done) or the next frontier size into *flag_ptr (an
+    int64 the device can write, e.g. pinned host memory)."""
+    _check(load().s3bfs_dist_advance_flag(handle, _stream(stream), ctypes.c_void_p(int(flag_ptr))),
+           "s3bfs_dist_advance_flag", handle)
 
 
 def s3bfs_dist_status(handle, stream=None):

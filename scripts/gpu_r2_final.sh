@@ -29,3 +29,7 @@ python scripts/prof_run.py > /dev/null 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"k_explore|k_compact" -c 5 \
     -o gpurun_out/r2_prof_final -f python scripts/prof_run.py > gpurun_out/ncu_full.log 2>&1
 echo ncu_rc=$?
+python scripts/prof_run.py --config grid > /dev/null 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"k_small|k_cluster" -c 2 \
+    -o gpurun_out/r2_prof_grid -f python scripts/prof_run.py --config grid > gpurun_out/ncu_grid.log 2>&1
+echo ncu_grid_rc=$?

@@ -14,7 +14,7 @@ extern "C" int kx_micro(const int32_t *col, int n, int n_l, int e_l, int32_t *f,
     int dev, sms, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_explore, KD_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_explore<false>, KD_THREADS, 0);
     p_max = sms * (occ > 0 ? occ : 1);
   }
   Params P{};
@@ -55,7 +55,7 @@ extern "C" int kx_micro(const int32_t *col, int n, int n_l, int e_l, int32_t *f,
     cudaMemset(claim, 0, claim_n);
     cudaDeviceSynchronize();
     cudaEventRecord(a);
-    k_explore<<<h.p_l, KD_THREADS, 0>>>(P);
+    k_explore<false><<<h.p_l, KD_THREADS, 0>>>(P);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms;

@@ -220,3 +220,18 @@ def test_gpu_dist_each_rank_owns_its_vertices():
         assert np.all(lv[~mine] == -1)
     for r in ranks:
         r.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("lag", [0, 1, 5])
+def test_gpu_loopback_lagged_termination(lag):
+    """The driver enqueues levels without a host round trip and reads each level's termination
+    flag `lag` levels late; the levels enqueued past the end are no-ops on the device."""
+    import paper_2209_08764_b200.dist as pd
+    for g in _graphs():
+        ranks = _gpu_ranks(g, 3)
+        for s in sorted({0, g.n - 1}):
+            for lv, pa in pd.traverse(ranks, s, lag=lag):
+                _check(g, s, lv.cpu().numpy(), pa.cpu().numpy())
+        for r in ranks:
+            r.close()
