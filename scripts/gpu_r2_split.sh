@@ -1,0 +1,10 @@
+# one k_explore instance per visited-test mode (both chained per level, the other idles) vs one
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r2_gpu_tests.log 2>&1; rc=$?; echo "tests rc=$rc"; tail -3 gpurun_out/r2_gpu_tests.log
+[ $rc -eq 0 ] || exit 1
+L=paper_2209_08764_b200/libs3bfs.so
+ROUNDS=3 bash scripts/abx.sh rmat24 8 gpurun_out/r2_split_rmat24.log "one|variants/libs3bfs_split0.so|{}" "split|$L|{}"
+ROUNDS=2 bash scripts/abx.sh rmat20 8 gpurun_out/r2_split_rmat20.log "one|variants/libs3bfs_split0.so|{}" "split|$L|{}"
+ROUNDS=3 bash scripts/abx.sh er 8 gpurun_out/r2_split_er.log "one|variants/libs3bfs_split0.so|{}" "split|$L|{}"
+ROUNDS=2 bash scripts/abx.sh tail 4 gpurun_out/r2_split_tail.log "one|variants/libs3bfs_split0.so|{}" "split|$L|{}"
+python scripts/abx_summary.py gpurun_out/r2_split_*.log
