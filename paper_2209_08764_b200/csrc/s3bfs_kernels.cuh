@@ -105,6 +105,9 @@ namespace s3bfs {
 #ifndef S3BFS_KS_ONCHIP
 #define S3BFS_KS_ONCHIP 1  // k_small: Owner race in a shared-memory table (no L2 round trip)
 #endif
+#ifndef S3BFS_LB_WIDE
+#define S3BFS_LB_WIDE 1  // k_compact: CTA-wide one-round-trip prefix over all predecessors
+#endif
 #ifndef S3BFS_CHECK
 #define S3BFS_CHECK 0  // 1: bounds-checked build (every traversal index checked; trap + message)
 #endif
@@ -134,7 +137,10 @@ constexpr int KX_GROUPS = S3BFS_KX_GROUPS;      // 32-edge groups per batch and 
 constexpr int KC_GROUPS = S3BFS_KC_GROUPS;      // 32-candidate groups per k_compact round
 constexpr int DIST_MAX = 8;                     // NEXT-4: ranks per traversal (one node)
 constexpr int KQ_CAP = 32 + 2 * 32;            // k_explore warp queue (< 32 kept + 2 groups)
-constexpr int KS_THREADS = 1024;                // k_small CTA size
+#ifndef S3BFS_KS_THREADS
+#define S3BFS_KS_THREADS 1024
+#endif
+constexpr int KS_THREADS = S3BFS_KS_THREADS;    // k_small CTA size (<= 1024, a multiple of 32)
 constexpr int KS_ECAP = S3BFS_KS_ONCHIP ? 4096 : 8192;  // T0 maximum (edges per tier-0 level)
 constexpr int KS_TAB_BITS = 14;                 // k_small on-chip Owner table: 2^14 entries
 constexpr int KS_TAB = 1 << KS_TAB_BITS;
@@ -153,7 +159,8 @@ constexpr int KC_ECTA = 4096;                    // level edges per CTA (e_l <= 
 constexpr int KC_FCAP = 8192;                    // replicated frontier capacity
 constexpr int KC_IPT = KC_ECTA / KC_THREADS;
 // k_small / k_cluster scan their per-warp totals with warp 0 reading one entry per lane
-static_assert(KS_THREADS == 1024 && KC_THREADS == 1024, "tier-0 / cluster CTAs must have 32 warps");
+static_assert(KC_THREADS == 1024, "cluster CTAs must have 32 warps (warp totals: one per lane)");
+static_assert(KS_THREADS % 32 == 0 && KS_THREADS <= 1024, "k_small: whole warps, <= 32");
 static_assert(KX_GROUPS % 4 == 0, "k_explore packs 4 window slots per register");
 constexpr int BU_W = S3BFS_BU_W;   // bottom-up: bitmap words per warp round
 constexpr int BU_P = S3BFS_BU_P;   // bottom-up: in-neighbours probed per vertex per round
@@ -1049,6 +1056,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
   if (c->tier != TIER_LARGE) return;
   const int p_l = c->p_l;
   __shared__ int32_t s_k[KD_WARPS], s_d[KD_WARPS];
+  __shared__ int32_t s_la[KD_WARPS], s_ld[KD_WARPS];  // S3BFS_LB_WIDE: predecessor sums
   __shared__ int s_last, s_tile;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // Surplus CTAs (blockIdx >= P_l) do no work but are still counted by the last-CTA
@@ -1104,6 +1112,44 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
     if (lane == 0 && tot) atomicAdd(&c->cand_acc, tot);  // statistics only
   }
   __syncthreads();
+#if S3BFS_LB_WIDE
+  // (b) across CTAs in one round trip: CTA b publishes its (kept, degree-sum) aggregate and
+  // every thread reads one predecessor's (P_l <= P_max <= 512 = the CTA size): the exclusive
+  // prefix is their sum, complete once every predecessor has published (tiles are numbered in
+  // start order, so each has started).  A chained look-back needs ~P_l / 32 dependent round
+  // trips for the last tiles; this needs one, plus a CTA reduction.
+  int koff, doff;
+  {
+    const int kk = lane < KD_WARPS ? s_k[lane] : 0;  // every warp scans the warp totals
+    const int dd = lane < KD_WARPS ? s_d[lane] : 0;
+    const int ik = warp_incl_scan(kk), id = warp_incl_scan(dd);
+    const Pair agg{(uint32_t)__shfl_sync(0xffffffffu, ik, 31),
+                   (uint32_t)__shfl_sync(0xffffffffu, id, 31)};
+    if (tid == 0) st_relaxed_u64(P.status + b, FLAG_A | pack<true>(agg));
+    Pair ex{0, 0};
+    for (unsigned ns = 32;;) {
+      const unsigned long long sv = tid < b ? ld_relaxed_u64(P.status + tid) : FLAG_A;
+      const Pair v = unpack<true>(sv);
+      const int sa = warp_sum((int)v.a), sd = warp_sum((int)v.b);
+      if (lane == 0) { s_la[warp] = sa; s_ld[warp] = sd; }
+      if (!__syncthreads_or((sv >> 62) == 0)) {  // (also the barrier before the reads below)
+        ex.a = (uint32_t)warp_sum(lane < KD_WARPS ? s_la[lane] : 0);
+        ex.b = (uint32_t)warp_sum(lane < KD_WARPS ? s_ld[lane] : 0);
+        break;
+      }
+      __nanosleep(ns);
+      if (ns < S3BFS_LB_MAX_NS) ns <<= 1;
+    }
+    koff = (int)ex.a + __shfl_sync(0xffffffffu, ik - kk, warp);
+    doff = (int)ex.b + __shfl_sync(0xffffffffu, id - dd, warp);
+    if (b == p_l - 1 && tid == 0) {  // the level's totals: n_{l+1}, e_{l+1} (Fig1 L15)
+      const int n_next = (int)(ex.a + agg.a), e_next = (int)(ex.b + agg.b);
+      c->n_next = n_next;
+      c->e_next = e_next;
+      P.fex[nxt][n_next] = e_next;
+    }
+  }
+#else
   if (warp == 0) {
     const int kk = lane < KD_WARPS ? s_k[lane] : 0;
     const int dd = lane < KD_WARPS ? s_d[lane] : 0;
@@ -1124,6 +1170,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
   }
   __syncthreads();
   int koff = s_k[warp], doff = s_d[warp];
+#endif
   int32_t *__restrict__ fn = P.f[nxt];
   int32_t *__restrict__ frsn = P.frs[nxt];
   int32_t *__restrict__ fexn = P.fex[nxt];
@@ -1571,7 +1618,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
   int32_t *cv = sex + KS_NCAP + 4;    // candidate per level-local edge (or -1)
   int32_t *cpv = cv + KS_ECAP;        // its discoverer
 #endif                                // (S3BFS_KS_ONCHIP: this space is the Owner table)
-  __shared__ int32_t s_wk[KS_THREADS / 32], s_wd[KS_THREADS / 32], s_wc[KS_THREADS / 32];
+  __shared__ int32_t s_wk[32], s_wd[32], s_wc[32];  // warp totals (entries past the warps: 0)
   __shared__ int32_t s_tot[3];
   __shared__ int32_t s_tiny[3];
 
@@ -1591,6 +1638,11 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
     sex[i] = P.fex[cur][i];
   }
   if (tid == 0) sex[n_l] = e_l;
+  if (KS_THREADS < 1024 && tid < 32 - KS_THREADS / 32) {
+    s_wk[KS_THREADS / 32 + tid] = 0;
+    s_wd[KS_THREADS / 32 + tid] = 0;
+    s_wc[KS_THREADS / 32 + tid] = 0;
+  }
   __syncthreads();
 
   for (;;) {
