@@ -30,7 +30,9 @@ def launches(path):
     agg = defaultdict(lambda: [0, 0.0])
     for r in rows(path):
         if r["Metric Name"] == "gpu__time_duration.sum":
-            k = r["Kernel Name"].split("(")[0].replace("s3bfs::", "")
+            # "void s3bfs::k_explore<0>(s3bfs::Params)" -> "k_explore"
+            k = r["Kernel Name"].split("(")[0].split("<")[0].replace("void ", "")
+            k = k.replace("s3bfs::", "").strip()
             if k not in STEP_KERNELS:
                 continue
             agg[k][0] += 1
