@@ -136,7 +136,10 @@ constexpr int KD_SLACK = 64;                    // candidate-buffer slack per CT
 constexpr int KX_GROUPS = S3BFS_KX_GROUPS;      // 32-edge groups per batch and warp
 constexpr int KC_GROUPS = S3BFS_KC_GROUPS;      // 32-candidate groups per k_compact round
 constexpr int DIST_MAX = 8;                     // NEXT-4: ranks per traversal (one node)
-constexpr int KQ_CAP = 32 + 2 * 32;            // k_explore warp queue (< 32 kept + 2 groups)
+#ifndef S3BFS_KQ_GROUPS
+#define S3BFS_KQ_GROUPS 2  // k_explore queue: flush check after this many groups
+#endif
+constexpr int KQ_CAP = 32 + S3BFS_KQ_GROUPS * 32;  // k_explore warp queue (< 32 kept + groups)
 #ifndef S3BFS_KS_THREADS
 #define S3BFS_KS_THREADS 1024
 #endif
@@ -976,7 +979,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
 #pragma unroll
         for (int g = 0; g < KX_GROUPS; ++g) {
           if ((witm >> g) & 1u) enqueue(g, (itm >> g) & 1u, (needm >> g) & 1u, v[g], xs);
-          if ((g & 1) == 1) {  // every 2 groups: at most 32 + 2 * 32 queued
+          if ((g % S3BFS_KQ_GROUPS) == S3BFS_KQ_GROUPS - 1) {  // at most 32 + KQ_GROUPS * 32 queued
             while (qn >= 32) flush(32);
           }
         }
