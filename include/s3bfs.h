@@ -99,12 +99,6 @@ typedef struct {
                               percentage of all arcs end at visited vertices (the discovery-heavy
                               levels); other levels test every target's visited bit first.
                               0 -> the default (80); > 100 -> every level; < 0 -> never */
-  int32_t owner_partition; /* discovery-heavy tier-1 levels (the tag-mode condition above) run
-                              owner-partitioned (DESIGN R28): the exploration kernel routes every
-                              arc's {target, parent} to the owner of the target's visited-bitmap
-                              word (one owner CTA per SM), which runs the visited test, the Owner
-                              race and the compaction on chip.  0 -> the default (on where
-                              eligible: top-down, single GPU); < 0 -> off; > 0 -> on */
 } s3bfs_options;
 
 /* One record per BFS level (the SPEC LevelStats analogue).  n_l = |frontier|
@@ -171,8 +165,6 @@ typedef struct {
   int32_t num_sms, p_max, edges_per_cta, tier0_max_edges;
   int32_t kd_threads, kd_tile_edges, ksmall_threads, ksmall_max_frontier;
   int32_t td_chain, bu_chain, universal_body, prologue;
-  int32_t px_parts, px_chain;  /* owner-partitioned levels (DESIGN R28): owner partitions (0:
-                                  off) and routing/resolve pairs per top-down body entry */
   int64_t workspace_bytes;
 } s3bfs_info;
 s3bfs_status s3bfs_get_info(s3bfs_handle h, s3bfs_info *out);

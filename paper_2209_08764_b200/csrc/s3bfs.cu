@@ -58,7 +58,7 @@ struct s3bfs_ctx {
   const int32_t *ro_int = nullptr;  // row offsets of the internal CSR
   size_t ws_bytes = 0;
   int64_t cand_cap = 0;
-  size_t ks_smem = 0, kc_smem = 0, px_smem = 0;
+  size_t ks_smem = 0, kc_smem = 0;
   int loop_graph = 1;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -354,12 +354,6 @@ s3bfs_status build_in_adjacency(s3bfs_ctx *h, cudaStream_t st) {
 #ifndef S3BFS_GRAPH_PROLOGUE
 #define S3BFS_GRAPH_PROLOGUE 1  // the canonical tier sequence once before the WHILE node
 #endif
-#ifndef S3BFS_PX_CHAIN
-#define S3BFS_PX_CHAIN 2  // owner-partitioned (routing, resolve) pairs before the top-down pairs
-#endif
-#ifndef S3BFS_PX_DEFAULT
-#define S3BFS_PX_DEFAULT 1  // owner_partition = 0 selects this (1: on where eligible)
-#endif
 #ifndef S3BFS_BU_CHAIN
 #define S3BFS_BU_CHAIN 3  // bottom-up (k_fb_clear, k_fb_set, k_bottom_up) triples per body
 #endif
@@ -407,8 +401,7 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
   // a (k_explore, k_compact) pair or a bottom-up triple one level).  S = k_small, C =
   // k_cluster, T = top-down pair, B = bottom-up triple.  The canonical sequence of a
   // traversal is S C T^td C S (top-down) or S C T^td B^bu T^td C S (direction-optimising).
-  const std::string seq = std::string("SC") + std::string(h->P.px_parts > 0 ? S3BFS_PX_CHAIN : 0, 'X') +
-      std::string(S3BFS_TD_CHAIN, 'T') +
+  const std::string seq = std::string("SC") + std::string(S3BFS_TD_CHAIN, 'T') +
       (h->P.direction ? std::string(S3BFS_BU_CHAIN, 'B') + std::string(S3BFS_TD_CHAIN, 'T')
                       : std::string()) + "CS";
   auto add_chain = [&](cudaGraph_t bg, const std::string &chain, cudaGraphNode_t prev,
@@ -429,9 +422,6 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
       } else if (k == 'T') {
         r = add((void *)k_explore<false>, h->P.p_max, KD_THREADS, 0);
         if (r == S3BFS_OK) r = add((void *)k_compact, h->P.p_max, KD_THREADS, 0);
-      } else if (k == 'X') {  // R28: routing + owner resolve of an owner-partitioned level
-        r = add((void *)k_explore<false, true>, h->P.p_max, KD_THREADS, 0);
-        if (r == S3BFS_OK) r = add((void *)k_px_resolve, h->P.px_parts, PR_THREADS, h->px_smem);
       } else {  // 'B'
         r = add((void *)k_fb_clear, h->num_sms * 4, 256, 0);
         if (r == S3BFS_OK) r = add((void *)k_fb_set, h->num_sms * 4, 256, 0);
@@ -468,21 +458,19 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
   // body 0 tier 0, body 1 top-down, body 2 bottom-up (NEXT-3), body 3 the cluster tier.
   // S3BFS_UNIVERSAL_BODY: body t is the canonical sequence from tier t on; otherwise body t
   // = its own tier only (S, T^td, B^bu, C).
-  const char body_tier[5] = {'S', 'T', 'B', 'C', 'X'};
+  const char body_tier[4] = {'S', 'T', 'B', 'C'};
   cudaGraphNodeParams sp = {};
   sp.type = cudaGraphNodeTypeConditional;
   sp.conditional.handle = ht;
   sp.conditional.type = cudaGraphCondTypeSwitch;
-  sp.conditional.size = 5;  // body 2 stays empty without NEXT-3, body 4 without R28
+  sp.conditional.size = 4;  // body 2 stays empty without NEXT-3
   cudaGraphNode_t snode;
   CK(h, cudaGraphAddNode(&snode, body, nullptr, 0, &sp));
-  for (int bi = 0; bi < 5; ++bi) {
+  for (int bi = 0; bi < 4; ++bi) {
     if (bi == 2 && !h->P.direction) continue;
-    if (bi == 4 && h->P.px_parts <= 0) continue;
     const char t = body_tier[bi];
     const std::string chain = S3BFS_UNIVERSAL_BODY ? seq.substr(seq.find(t))
                             : t == 'T' ? std::string(S3BFS_TD_CHAIN, 'T')
-                            : t == 'X' ? std::string(S3BFS_PX_CHAIN, 'X')
                             : t == 'B' ? std::string(S3BFS_BU_CHAIN, 'B') : std::string(1, t);
     s3bfs_status r = add_chain(sp.conditional.phGraph_out[bi], chain, nullptr, nullptr);
     if (r != S3BFS_OK) return r;
@@ -635,31 +623,6 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   while ((long long)bu_tile_w * S3BFS_BU_TILES_PER_CTA * p_max < bu_words) bu_tile_w <<= 1;
   const int bu_tiles = h->opt.direction == 1 ? (int)((bu_words + bu_tile_w - 1) / bu_tile_w) : 0;
   const size_t o_bustatus = take((size_t)(bu_tiles + 1) * 8);
-  // R28 owner-partitioned levels: one owner CTA per SM (<= P_max: the routing kernel resets
-  // their look-back words); each holds its partition's bitmap words twice in shared memory
-  int px_parts = 0, px_nw = 0;
-  long long px_cap = 0, px_rows = 0;
-  {
-    const int po = h->opt.owner_partition == 0 ? (S3BFS_PX_DEFAULT ? 1 : -1) : h->opt.owner_partition;
-    if (po > 0 && dist_size == 1 && h->opt.direction != 1 && nnz > 0) {
-      int parts = h->num_sms < p_max ? h->num_sms : p_max;
-      if (parts > PX_BMAX) parts = PX_BMAX;
-      const long long nwords = ((long long)n + 31) / 32;
-      long long nw = (nwords + parts - 1) / parts;
-      const size_t sm = (size_t)nw * 8;  // the partition's words: level start + current
-      if (parts >= 1 && sm + 8192 <= (size_t)prop.sharedMemPerBlockOptin) {
-        px_parts = parts;
-        px_nw = (int)nw;
-        h->px_smem = sm;
-        px_cap = nnz / 2 + 4096;
-        if (px_cap > nnz) px_cap = nnz;
-        // directory rows of one level: P_l x ceil(wcap / 256) <= e_l / 4096 + 2 P_l (+ rounding)
-        px_rows = px_cap / 4096 + 3LL * p_max + 64;
-      }
-    }
-  }
-  const size_t o_pxi = px_parts ? take((size_t)px_cap * 8) : 0;
-  const size_t o_pxd = px_parts ? take((size_t)px_rows * (px_parts + 1) * 4) : 0;
   const size_t o_ctl = take(sizeof(Ctl));
   const size_t o_stats = take((size_t)stats_cap * sizeof(s3bfs_level_stat));
   h->ws_bytes = off;
@@ -699,16 +662,6 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   P.bu_tiles = bu_tiles;
   P.bu_tile_w = bu_tile_w;
   P.stats = (s3bfs_level_stat *)(base + o_stats);
-  P.px_parts = px_parts;
-  if (px_parts) {
-    P.px_items = (int2 *)(base + o_pxi);
-    P.px_dir = (int32_t *)(base + o_pxd);
-    P.px_dir_rows = px_rows;
-    P.px_cap = px_cap;
-    P.px_magic = (uint32_t)((1ull << 32) / (unsigned long long)px_parts + 1ull);
-    P.px_nw = px_nw;
-    P.px_min = 0;
-  }
   P.stats_cap = stats_cap;
   P.p_max = p_max;
   P.grain = grain;
@@ -799,9 +752,6 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   h->ks_smem = (size_t)(3 * KS_NCAP + 4 + (S3BFS_KS_ONCHIP ? KS_TAB : 2 * KS_ECAP)) * 4;
   if ((e = cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->ks_smem)) != cudaSuccess)
     return bail(cuda_fail(h, e, "cudaFuncSetAttribute(k_small)"));
-  if (P.px_parts && (e = cudaFuncSetAttribute(k_px_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)h->px_smem)) != cudaSuccess)
-    return bail(cuda_fail(h, e, "cudaFuncSetAttribute(k_px_resolve)"));
   h->kc_smem = (size_t)(3 * KC_FCAP + 4 + 2 * KC_ECTA) * 4;
   if ((e = cudaFuncSetAttribute(k_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->kc_smem)) != cudaSuccess)
     return bail(cuda_fail(h, e, "cudaFuncSetAttribute(k_cluster)"));
@@ -906,11 +856,6 @@ s3bfs_status s3bfs_run(s3bfs_handle h, int32_t source, int32_t *level, int32_t *
       k_fb_set<<<h->num_sms * 4, 256, 0, stream>>>(h->P);
       k_bottom_up<<<h->P.p_max, KD_THREADS, 0, stream>>>(h->P);
       if (h->time_kernels) CK(h, cudaEventRecord(h->ev[1], stream));
-    } else if (c.tier == TIER_PX) {  // R28 (grid >= px_parts: routing resets their look-back words)
-      k_explore<false, true><<<c.p_l > h->P.px_parts ? c.p_l : h->P.px_parts, KD_THREADS, 0, stream>>>(h->P);
-      if (h->time_kernels) CK(h, cudaEventRecord(h->ev[1], stream));
-      k_px_resolve<<<h->P.px_parts, PR_THREADS, h->px_smem, stream>>>(h->P);
-      if (h->time_kernels) CK(h, cudaEventRecord(h->ev[2], stream));
     } else {
       k_explore<false><<<c.p_l, KD_THREADS, 0, stream>>>(h->P);
       if (h->time_kernels) CK(h, cudaEventRecord(h->ev[1], stream));
@@ -1138,8 +1083,6 @@ s3bfs_status s3bfs_get_info(s3bfs_handle h, s3bfs_info *out) {
   out->bu_chain = S3BFS_BU_CHAIN;
   out->universal_body = S3BFS_UNIVERSAL_BODY;
   out->prologue = graph_prologue(h) ? 1 : 0;
-  out->px_parts = h->P.px_parts;
-  out->px_chain = h->P.px_parts > 0 ? S3BFS_PX_CHAIN : 0;
   out->workspace_bytes = (int64_t)(h->ws_bytes + (h->gs ? h->gs->b2 + h->gs->b3 : 0));
   return S3BFS_OK;
 }

@@ -155,14 +155,6 @@ constexpr int SCAN_ITEMS = 8;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 
 constexpr int TIER_SMALL = 0, TIER_LARGE = 1, TIER_DONE = 2, TIER_BU = 3, TIER_CLUSTER = 4;
-constexpr int TIER_PX = 5;  // owner-partitioned tier-1 level (R28): k_explore<false, true> + k_px_resolve
-// owner-partitioned mode (R28): partitions = owner CTAs of k_px_resolve (one per SM)
-constexpr int PX_BMAX = 255;                    // max partitions (k_explore's per-round cells)
-constexpr int PX_RANK_BITS = 13;                // k_explore: rank of an item inside its round
-constexpr int PR_THREADS = 1024;                // k_px_resolve CTA (one per SM)
-constexpr int PR_WARPS = PR_THREADS / 32;
-constexpr int PR_G = 8;                         // k_px_resolve: 32-item groups per warp and step
-static_assert(KD_THREADS * KX_GROUPS <= (1 << PX_RANK_BITS), "round rank fits its field");
 // cluster tier (f, SURVEY 8(a) "optional middle tier"): one cluster of KC_CL CTAs
 constexpr int KC_CL = 8;                         // CTAs per cluster (portable size)
 constexpr int KC_THREADS = 1024;
@@ -200,8 +192,6 @@ struct Ctl {
   int32_t fb_valid;         // fb[cur] already holds the current frontier (a bottom-up product)
   int32_t probe_tags;       // k_explore's visited test of this level: tag mode (1) or bitmap
                             // mode (0), see k_explore; set by decide_tier
-  int32_t px_seen;          // an owner-partitioned level ran in this traversal: later tier-1
-                            // levels use the bitmap visited test (its discoveries carry no tag)
   long long m_visited;      // sum of the degrees of all visited vertices (Beamer's m_u = m - it)
   int32_t *level_out, *parent_out;
   unsigned long long t_prev;
@@ -266,20 +256,6 @@ struct Params {
   int2 *p_rtot[DIST_MAX];
   uint32_t *p_bm[DIST_MAX];
   int4 *p_vinfo[DIST_MAX];      // peers' vertex records (the sender stores the Owner label)
-  // owner-partitioned mode (R28; single GPU, top-down): the level's arcs are routed to
-  // px_parts owner partitions (internal id v belongs to partition (v / 32) mod px_parts, i.e.
-  // whole visited-bitmap words), then each partition's owner CTA (k_px_resolve) runs the
-  // visited test, the Owner race and the compaction on chip
-  int2 *px_items;               // k_explore's routed items {v, parent caller id}: CTA b's rounds
-                                //  in [b * chunk, (b + 1) * chunk), each round grouped by partition
-  int32_t *px_dir;              // directory rows (px_parts + 1 entries): item offset of each
-                                //  partition's run in one round of one CTA
-  long long px_dir_rows;        // directory rows allocated (a bound, see s3bfs_create)
-  long long px_cap;             // item capacity: levels with e_l <= px_cap can be partitioned
-  int32_t px_parts;             // partitions (0: mode off)
-  uint32_t px_magic;            // floor(2^32 / px_parts) + 1 (division by px_parts)
-  int32_t px_nw;                // local bitmap words of the largest partition (even)
-  int32_t px_min;               // partitioned levels: e_l >= px_min
   long long nnz;
   long long cand_cap;           // candidate buffer entries (bounds-checked build)
   long long nnz_all;            // arcs of the whole graph (= nnz on one GPU; NEXT-4: all ranks')
@@ -415,19 +391,6 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 }
 __device__ __forceinline__ int32_t *owner_of(int4 *vinfo, int v) {
   return reinterpret_cast<int32_t *>(vinfo + v) + 3;
-}
-
-// the lanes whose NB-bit key equals this lane's (valid lanes only; an invalid lane gets
-// itself): NB ballots -- __match_any_sync is microcoded and far slower on this part
-template <int NB>
-__device__ __forceinline__ unsigned match_key(uint32_t key, bool valid) {
-  unsigned peers = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-  for (int i = 0; i < NB; ++i) {
-    const unsigned b = __ballot_sync(0xffffffffu, (key >> i) & 1u);
-    peers &= ((key >> i) & 1u) ? b : ~b;
-  }
-  return valid ? peers : (1u << (threadIdx.x & 31));
 }
 
 // k_small's on-chip Owner table: round r's bijection of the 32-bit ids (odd multiplies,
@@ -571,7 +534,7 @@ __device__ void record_stat(const Params &P, Ctl *c, int32_t level, int32_t n_l,
 __device__ void steer(const Params &P, int tier) {
   if (!P.use_graph) return;
   const unsigned body = tier == TIER_SMALL ? 0u : tier == TIER_LARGE ? 1u : tier == TIER_BU ? 2u
-                      : tier == TIER_CLUSTER ? 3u : tier == TIER_PX ? 4u : 7u;
+                      : tier == TIER_CLUSTER ? 3u : 7u;
   cudaGraphSetConditional((cudaGraphConditionalHandle)P.h_tier, body);
   cudaGraphSetConditional((cudaGraphConditionalHandle)P.h_while, tier != TIER_DONE ? 1u : 0u);
 }
@@ -627,16 +590,9 @@ __device__ void decide_tier(const Params &P, Ctl *c, int32_t n_l, int32_t e_l) {
   c->e_hi = (int32_t)e_hi;
   // k_explore's visited test: tag mode while few arcs end at visited vertices (m_visited =
   // degrees of all visited vertices, the frontier included; arc ends for a symmetric graph)
-  const bool heavy_disc = P.tag_pct >= 0 &&
-                          (double)c->m_visited * 100.0 < (double)P.nnz_all * (double)P.tag_pct;
+  c->probe_tags = P.tag_pct >= 0 &&
+                  (double)c->m_visited * 100.0 < (double)P.nnz_all * (double)P.tag_pct;
   c->tier = TIER_LARGE;
-  // R28: a discovery-heavy level (the tag-mode condition) runs owner-partitioned when it fits;
-  // after one, tier-1 levels test the bitmap (owner-partitioned discoveries carry no tag)
-  if (P.px_parts > 0 && heavy_disc && e_l >= P.px_min && (long long)e_l <= P.px_cap) {
-    c->tier = TIER_PX;
-    c->px_seen = 1;
-  }
-  c->probe_tags = heavy_disc && !c->px_seen;
   c->p_l = (int32_t)p_l;
   c->chunk = (int32_t)chunk;
   c->wcap = (int32_t)((chunk + KD_WARPS - 1) / KD_WARPS);  // edges (and candidates) per warp
@@ -686,7 +642,6 @@ __global__ void k_init(Params P, int32_t s, int32_t *level, int32_t *parent) {
     c->t_dbg[1] = 0;
     c->bu = 0;
     c->fb_valid = 0;
-    c->px_seen = 0;
     c->m_visited = vs.y;
     decide(P, c, 1, vs.y);
   }
@@ -717,16 +672,14 @@ __global__ void k_policies(unsigned long long *out) {
 // duplicates; the Owner check keeps exactly one (R4).
 // DIST = NEXT-4's rank kernel (candidates routed to owners); the single-GPU kernel is
 // k_explore<false> and carries none of that code
-// PX = the owner-partitioned level (R28): the same edge split and col stream, but every target
-// is routed as {v, parent} to its owner partition (no probe here); k_px_resolve follows.
-template <bool DIST, bool PX = false>
+template <bool DIST>
 __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P) {
   Ctl *c = P.ctl;
-  if (c->tier != (PX ? TIER_PX : TIER_LARGE)) return;
+  if (c->tier != TIER_LARGE) return;
   const int b = blockIdx.x;
   const int p_l = c->p_l;
-  if ((DIST || PX) && threadIdx.x == 0)  // NEXT-4: k_dist_keep's look-back word of tile b;
-    P.status[b] = 0ull;                  // PX: k_px_resolve's (gridDim = P_max >= its tiles)
+  if (DIST && threadIdx.x == 0)  // NEXT-4: k_dist_keep's look-back word of tile b
+    P.status[b] = 0ull;                      // (gridDim = P_max in dist mode)
   if (b >= p_l) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n_l = c->n_l, chunk = c->chunk, cur = c->cur, wcap = c->wcap;
@@ -746,7 +699,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   const uint32_t tag_span = (uint32_t)(P.n - P.hub);  // ids in [hub, n): tag only
 
   if (tid == 0) {
-    if (!DIST && !PX) P.status[b] = 0ull;  // reset k_compact's look-back word
+    if (!DIST) P.status[b] = 0ull;  // reset k_compact's look-back word
     if (b == 0) c->t_kx_begin = globaltimer();
   }
   const int E0 = c->e_lo + b * chunk;
@@ -776,12 +729,12 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   // Map the batch of edges [e, e_next) onto lanes and load their targets: v[g] = col entry of
   // edge e + 32g + lane (-1 outside the batch), byte g of xs = its frontier vertex's window slot
   // (the caller id is shuffled only on discovery).
-  auto map_load = [&](int e, int eend, int (&v)[KX_GROUPS], uint32_t (&xs)[KX_GROUPS / 4]) -> int {
+  auto map_load = [&](int e, int (&v)[KX_GROUPS], uint32_t (&xs)[KX_GROUPS / 4]) -> int {
     while (lim <= e) {  // window exhausted (also skips runs of zero-degree vertices, C9)
       u0 += 32;
       load_window(u0);
     }
-    const int bend = min(eend, lim);
+    const int bend = min(e_end, lim);
     // window slot of the batch's first edge (warp-uniform): the window's row starts are
     // non-decreasing and wex_0 <= e, so it is the count of row starts <= e, minus one
     const int j0 = __popc(__ballot_sync(0xffffffffu, wex <= e)) - 1;
@@ -879,124 +832,6 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
     }
     return e_next;
   };
-  if constexpr (PX) {
-    // R28 routing, in CTA-wide rounds of (up to) 256 edges per warp: the warp maps and loads its
-    // next edges (one or more batches) and appends every target with its parent to a
-    // warp-private list; the round's items are then counted per (partition, warp) cell
-    // (__match_any_sync groups a partition's lanes, the group's first lane bumps its warp's own
-    // cell -- no atomic), the cells are scanned partition-major, the items placed in that
-    // order in shared memory and written out contiguously; directory row (b, round) records
-    // where each partition's run starts.  No probe of the target's state here: its owner tests it.
-    __shared__ int2 s_st[PX ? KD_WARPS * KX_GROUPS * 32 : 1];   // warp lists, then the sorted round
-    __shared__ uint16_t s_wh[PX ? KD_WARPS : 1][PX ? PX_BMAX + 1 : 1];  // (warp, partition) cells
-                                                                        // (counts, then offsets <= 4096)
-    __shared__ int32_t s_sc[KD_WARPS];
-    static_assert(!PX || (PX_BMAX + 1) * KD_WARPS == KD_THREADS * 8, "cell scan: 8 per thread");
-    const int B = P.px_parts;
-    const uint32_t magic = P.px_magic;
-    const int rc = (wcap + KX_GROUPS * 32 - 1) / (KX_GROUPS * 32);  // rounds of every CTA
-    for (int i = lane; i <= PX_BMAX; i += 32) s_wh[warp][i] = 0;
-    int2 *const wl = s_st + warp * (KX_GROUPS * 32);
-    long long obase = (long long)b * chunk;  // this CTA's items (<= its arcs)
-    int e = e_begin;
-    int r = 0;
-    __syncthreads();
-    for (;; ++r) {
-      // (1) the warp's next (up to) 256 edges -> its list (valid targets only, in edge order)
-      int nb = 0;
-      const int er = min(e + KX_GROUPS * 32, e_end);
-      while (e < er) {
-        int v[KX_GROUPS];
-        uint32_t xs[KX_GROUPS / 4];
-#pragma unroll
-        for (int k = 0; k < KX_GROUPS / 4; ++k) xs[k] = 0;
-        e = map_load(e, er, v, xs);
-#pragma unroll
-        for (int g = 0; g < KX_GROUPS; ++g) {
-          const int par = __shfl_sync(0xffffffffu, wx, (xs[g >> 2] >> (8 * (g & 3))) & 31u);
-          const bool ok = (uint32_t)v[g] < (uint32_t)P.n;
-          const unsigned m = __ballot_sync(0xffffffffu, ok);
-          if (ok) {
-            S3_CHK(nb + __popc(m & lanemask_lt()), KX_GROUPS * 32);
-            wl[nb + __popc(m & lanemask_lt())] = make_int2(v[g], par);
-          }
-          nb += __popc(m);
-        }
-      }
-      __syncwarp();
-      // (2) rank of each item inside its (partition, warp) cell
-      int2 it[KX_GROUPS];
-      int pk[KX_GROUPS];  // (partition << PX_RANK_BITS) | rank, -1: no item
-#pragma unroll
-      for (int g = 0; g < KX_GROUPS; ++g) {
-        const bool ok = g * 32 + lane < nb;
-        it[g] = ok ? wl[g * 32 + lane] : make_int2(-1, 0);
-        int pt = 0;
-        if (ok) {
-          const uint32_t x = (uint32_t)it[g].x >> 5;
-          uint32_t qd = __umulhi(x, magic);
-          if (qd * (uint32_t)B > x) --qd;
-          pt = (int)(x - qd * (uint32_t)B);
-        }
-        const unsigned peers = match_key<8>((uint32_t)pt, ok);  // lanes of partition pt
-        const int leader = __ffs(peers) - 1;
-        int old = 0;
-        if (ok && lane == leader) {
-          old = s_wh[warp][pt];
-          s_wh[warp][pt] = (uint16_t)(old + __popc(peers));
-        }
-        old = __shfl_sync(0xffffffffu, old, leader);
-        pk[g] = ok ? (pt << PX_RANK_BITS) | (old + __popc(peers & lanemask_lt())) : -1;
-        __syncwarp();
-      }
-      __syncthreads();
-      {  // (3) exclusive scan of the cells, partition-major (cell i = partition i / 16, warp i % 16)
-        int cv[8], sum = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int ci = tid * 8 + j;
-          cv[j] = s_wh[ci % KD_WARPS][ci / KD_WARPS];
-          sum += cv[j];
-        }
-        const int inc = warp_incl_scan(sum);
-        if (lane == 31) s_sc[warp] = inc;
-        __syncthreads();
-        const int wv = lane < KD_WARPS ? s_sc[lane] : 0;
-        const int wi = warp_incl_scan(wv);
-        int ex = __shfl_sync(0xffffffffu, wi - wv, warp) + inc - sum;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int ci = tid * 8 + j;
-          s_wh[ci % KD_WARPS][ci / KD_WARPS] = (uint16_t)ex;
-          ex += cv[j];
-        }
-      }
-      __syncthreads();
-      // (4) directory row (b, r) and the round's items in partition order
-      S3_CHK((long long)b * rc + r, P.px_dir_rows);
-      int32_t *drow = P.px_dir + ((long long)b * rc + r) * (B + 1);
-      const int tot = s_wh[0][B];  // cell (B, 0) = all items of partitions < B
-      for (int i = tid; i <= B; i += KD_THREADS) drow[i] = (int32_t)(obase + s_wh[0][i]);
-#pragma unroll
-      for (int g = 0; g < KX_GROUPS; ++g) {
-        if (pk[g] >= 0) {
-          const int at = s_wh[warp][pk[g] >> PX_RANK_BITS] + (pk[g] & ((1 << PX_RANK_BITS) - 1));
-          S3_CHK(at, KD_WARPS * KX_GROUPS * 32);
-          s_st[at] = it[g];
-        }
-      }
-      __syncthreads();
-      S3_CHK(obase + tot - 1, P.px_cap);
-      for (int i = tid; i < tot; i += KD_THREADS) P.px_items[obase + i] = s_st[i];
-      obase += tot;
-      for (int i = lane; i <= PX_BMAX; i += 32) s_wh[warp][i] = 0;
-      if (!__syncthreads_or(e < e_end)) break;
-    }
-    // rounds this CTA did not need: empty runs (k_px_resolve reads rc rows of every CTA)
-    for (long long k = (long long)(r + 1) * (B + 1) + tid; k < (long long)rc * (B + 1); k += KD_THREADS)
-      P.px_dir[(long long)b * rc * (B + 1) + k] = (int32_t)obase;
-    return;
-  }
 #if !S3BFS_KX_QUEUE
   // Discovery of the batch's groups flagged in discm (Fig1 L18-L22): plain stores -- the tag,
   // {d, parent}, Owner = the candidate slot, and the candidate itself (benign race, R4).
@@ -1115,7 +950,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
       uint32_t xs[KX_GROUPS / 4];  // window slots of the groups' frontier vertices, a byte each
 #pragma unroll
       for (int k = 0; k < KX_GROUPS / 4; ++k) xs[k] = 0;
-      e = map_load(e, e_end, v, xs);
+      e = map_load(e, v, xs);
       uint32_t needm = 0;  // targets whose discovery tag decides (bit clear at level start)
       uint32_t discm = 0;  // targets found undiscovered: candidates (Fig1 L19-L22)
       if constexpr (TAGS) {
@@ -1372,222 +1207,6 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
     const unsigned long long t = globaltimer();
     record_stat(P, c, c->level, c->n_l, c->e_l, TIER_LARGE, p_l, ld_volatile(&c->cand_acc),
                 n_next, c->t_prev, t, *(volatile unsigned long long *)&c->t_kx_begin,
-                *(volatile unsigned long long *)&c->t_kx_end);
-    c->cand_acc = 0;
-    c->done_ctr = 0;
-    c->tile_ctr = 0;
-    c->t_prev = t;
-    c->level = c->level + 1;  // Fig1 L10
-    c->cur = nxt;
-    c->m_visited += e_next;
-    c->fb_valid = 0;
-    decide(P, c, n_next, e_next);
-  }
-}
-
-// ---- R28: k_px_resolve, the owner side of an owner-partitioned level ---------------------------
-// CTA p owns partition p: the internal ids v with (v / 32) mod B == p, i.e. the visited-bitmap
-// words p, p + B, p + 2B, ... (local word k = (v / 32) div B).  It loads those words into
-// shared memory twice -- `old`, exact at level start, and `cur` -- then its warps stream every
-// run the routing rounds wrote for it (warp w: directory rows w, w + 32, ...), 8 runs of up
-// to 32 items in flight per warp, with no barrier:
-//   Fig1 L18 "if d[v] = infinity": the bit of v in `cur` (the level-start set plus this
-//   level's discoveries published so far);
-//   d[v] <- l + 1, parent[v] <- x: plain stores -- items of one v handled at the same moment
-//   all see the bit clear and store the same d and valid parents (the paper's benign race);
-//   the bit is then published into `cur` with a shared-memory OR (publication of a discovery,
-//   as k_compact's bitmap OR -- R17; its result is not read).
-// Fig1 L19-L29's dedup + compaction: the partition's next-level vertices are exactly the bits
-// set in `cur` and clear in `old` -- each once, whatever the number of racing discoverers --
-// compacted in id order into the next frontier (with L12-L15 of the next level: degree gather
-// and scan) behind the same one-round-trip look-back over (kept, degree-sum) pairs as
-// k_compact; the words are written back to the bitmap, and the last CTA advances the control
-// block.  The owner CTA is every one of its vertices' Owner (R28).
-__global__ void __launch_bounds__(PR_THREADS, 1) k_px_resolve(Params P) {
-  Ctl *c = P.ctl;
-  if (c->tier != TIER_PX) return;
-  extern __shared__ uint32_t s_dyn[];
-  __shared__ int32_t s_k[PR_WARPS], s_d[PR_WARPS], s_la[PR_WARPS], s_ld[PR_WARPS];
-  __shared__ int s_last, s_tile;
-  const int B = P.px_parts, NW = P.px_nw;
-  const uint32_t magic = P.px_magic;
-  uint32_t *s_old = s_dyn, *s_cur = s_dyn + NW;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int p = blockIdx.x;
-  const int nxt = c->cur ^ 1;
-  const int nwords = (P.n + 31) >> 5;
-  const int nwp = p < nwords ? (nwords - 1 - p) / B + 1 : 0;  // local words of partition p
-  S3_CHK(nwp, NW + 1);
-  for (int k = tid; k < nwp; k += PR_THREADS) {
-    const uint32_t w = P.bm[p + (long long)k * B];
-    s_old[k] = w;
-    s_cur[k] = w;
-  }
-  if (tid == 0) s_tile = (int)atomicAdd(&c->tile_ctr, 1u);  // look-back order = start order
-  if (p == 0 && tid == 0) c->t_kx_end = globaltimer();
-  const int new_level = c->level + 1;
-  // directory: rc rows per routing CTA (its rounds; unused ones hold empty runs)
-  const int nrows = c->p_l * ((c->wcap + KX_GROUPS * 32 - 1) / (KX_GROUPS * 32));
-  int2 *__restrict__ lp = P.lp;
-  const int2 *__restrict__ items = P.px_items;
-  int cand_cnt = 0;
-  __syncthreads();
-  // the warp's directory window: rows rbase + 32 i (lane i holds that row's run [rs, re))
-  for (int rbase = warp; rbase < nrows; rbase += 32 * PR_WARPS) {
-    int rs = 0, re = 0;
-    {
-      const long long row = rbase + 32LL * lane;
-      if (row < nrows) {
-        const int32_t *d = P.px_dir + row * (B + 1) + p;
-        rs = d[0];
-        re = d[1];
-      }
-    }
-    int cur = 0, off = 0;
-    for (;;) {
-      int2 it[PR_G];
-#pragma unroll
-      for (int g = 0; g < PR_G; ++g) {  // group g: up to 32 items of the current run
-        int len = cur < 32 ? __shfl_sync(0xffffffffu, re - rs, cur & 31) - off : 0;
-        while (cur < 32 && len <= 0) {
-          ++cur;
-          off = 0;
-          len = cur < 32 ? __shfl_sync(0xffffffffu, re - rs, cur & 31) : 0;
-        }
-        it[g] = make_int2(-1, 0);
-        if (cur < 32) {
-          const int st = __shfl_sync(0xffffffffu, rs, cur) + off;
-          if (lane < len) {
-            S3_CHK(st + lane, P.px_cap);
-            it[g] = items[st + lane];
-          }
-          off += min(32, len);
-        }
-      }
-#pragma unroll
-      for (int g = 0; g < PR_G; ++g) {
-        const int v = it[g].x;
-        if (v >= 0) {
-          const uint32_t x = (uint32_t)v >> 5;
-          uint32_t k = __umulhi(x, magic);
-          if (k * (uint32_t)B > x) --k;
-          S3_CHK(k, nwp);
-          const uint32_t bit = 1u << (v & 31);
-          if (!(s_cur[k] & bit)) {  // Fig1 L18
-            ++cand_cnt;
-            S3_CHK(v, P.n);
-            st_weak_v2(lp + v, new_level, it[g].y);  // d[v] <- l + 1, parent (benign race)
-            atomicOr(&s_cur[k], bit);                // publication (R17), result unused
-          }
-        }
-      }
-      if (cur >= 32) break;
-    }
-  }
-  __syncthreads();
-  // (4) the partition's new vertices in id order: warp w takes local words [w W, (w+1) W);
-  // the CTA's output order starts at warp p mod 32 (rotated), so that the next level's
-  // consecutive CTAs, each reading about one partition's run, start at different id (degree)
-  // ranges instead of sweeping the hubs' rows all at once
-  const int W = (nwp + PR_WARPS - 1) / PR_WARPS;
-  const int opos = (warp - p + 32 * PR_WARPS) % PR_WARPS;  // this warp's place in the order
-  const int k0 = min(warp * W, nwp), k1 = min(k0 + W, nwp);
-  const int4 *__restrict__ vinfo = P.vinfo;
-  int kept = 0, dsum = 0;
-  for (int k = k0; k < k1; k += 4) {
-    int dg[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int kk = k + j;
-      const uint32_t nb = kk < k1 ? s_cur[kk] & ~s_old[kk] : 0u;
-      const int v = ((p + kk * B) << 5) + lane;
-      dg[j] = (nb >> lane) & 1u ? __ldg(&vinfo[v].y) : -1;
-      if (kk < k1 && nb && lane == 0) P.bm[p + (long long)kk * B] = s_cur[kk];  // exact (R17)
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      kept += __popc(__ballot_sync(0xffffffffu, dg[j] >= 0));
-      dsum += dg[j] >= 0 ? dg[j] : 0;
-    }
-  }
-  dsum = warp_sum(dsum);
-  if (lane == 0) { s_k[opos] = kept; s_d[opos] = dsum; }
-  if (P.collect_stats) {
-    const int tot = warp_sum(cand_cnt);
-    if (lane == 0 && tot) atomicAdd(&c->cand_acc, tot);  // statistics only
-  }
-  __syncthreads();
-  const int b = s_tile;
-  int koff, doff;
-  {  // (b) across the partition CTAs in one round trip (as k_compact, S3BFS_LB_WIDE)
-    const int kk = s_k[lane], dd = s_d[lane];
-    const int ik = warp_incl_scan(kk), id = warp_incl_scan(dd);
-    const Pair agg{(uint32_t)__shfl_sync(0xffffffffu, ik, 31),
-                   (uint32_t)__shfl_sync(0xffffffffu, id, 31)};
-    if (tid == 0) st_relaxed_u64(P.status + b, FLAG_A | pack<true>(agg));
-    Pair ex{0, 0};
-    for (unsigned ns = 32;;) {
-      const unsigned long long sv = tid < b ? ld_relaxed_u64(P.status + tid) : FLAG_A;
-      const Pair v = unpack<true>(sv);
-      const int sa = warp_sum((int)v.a), sd = warp_sum((int)v.b);
-      if (lane == 0) { s_la[warp] = sa; s_ld[warp] = sd; }
-      if (!__syncthreads_or((sv >> 62) == 0)) {
-        ex.a = (uint32_t)warp_sum(s_la[lane]);
-        ex.b = (uint32_t)warp_sum(s_ld[lane]);
-        break;
-      }
-      __nanosleep(ns);
-      if (ns < S3BFS_LB_MAX_NS) ns <<= 1;
-    }
-    koff = (int)ex.a + __shfl_sync(0xffffffffu, ik - kk, opos);
-    doff = (int)ex.b + __shfl_sync(0xffffffffu, id - dd, opos);
-    if (b == B - 1 && tid == 0) {  // the level's totals: n_{l+1}, e_{l+1} (Fig1 L15)
-      const int n_next = (int)(ex.a + agg.a), e_next = (int)(ex.b + agg.b);
-      c->n_next = n_next;
-      c->e_next = e_next;
-      P.fex[nxt][n_next] = e_next;
-    }
-  }
-  int32_t *__restrict__ fn = P.f[nxt];
-  int32_t *__restrict__ frsn = P.frs[nxt];
-  int32_t *__restrict__ fexn = P.fex[nxt];
-  for (int k = k0; k < k1; k += 4) {
-    int4 vi[4];
-    bool has[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int kk = k + j;
-      const uint32_t nb = kk < k1 ? s_cur[kk] & ~s_old[kk] : 0u;
-      has[j] = (nb >> lane) & 1u;
-      vi[j] = has[j] ? __ldg(vinfo + ((p + kk * B) << 5) + lane) : make_int4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const unsigned m = __ballot_sync(0xffffffffu, has[j]);
-      const int d = has[j] ? vi[j].y : 0;
-      const int inc = warp_incl_scan(d);
-      if (has[j]) {
-        const int at = koff + __popc(m & lanemask_lt());
-        S3_CHK(at, P.n);
-        fn[at] = vi[j].z;
-        frsn[at] = vi[j].x;
-        fexn[at] = doff + inc - d;
-      }
-      koff += __popc(m);
-      doff += __shfl_sync(0xffffffffu, inc, 31);
-    }
-  }
-  // last-CTA election (as k_compact)
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) s_last = atomicAdd(&c->done_ctr, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (s_last && tid == 0) {
-    __threadfence();
-    const int n_next = ld_volatile(&c->n_next), e_next = ld_volatile(&c->e_next);
-    const unsigned long long t = globaltimer();
-    record_stat(P, c, c->level, c->n_l, c->e_l, TIER_PX, B, ld_volatile(&c->cand_acc), n_next,
-                c->t_prev, t, *(volatile unsigned long long *)&c->t_kx_begin,
                 *(volatile unsigned long long *)&c->t_kx_end);
     c->cand_acc = 0;
     c->done_ctr = 0;

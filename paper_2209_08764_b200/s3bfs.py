@@ -48,8 +48,7 @@ class Options(ctypes.Structure):
                 ("direction", ctypes.c_int32), ("do_alpha", ctypes.c_int32),
                 ("do_beta", ctypes.c_int32), ("dist_size", ctypes.c_int32),
                 ("dist_rank", ctypes.c_int32), ("cluster_max_edges", ctypes.c_int32),
-                ("hub_vertices", ctypes.c_int32), ("tag_mode_pct", ctypes.c_int32),
-                ("owner_partition", ctypes.c_int32)]
+                ("hub_vertices", ctypes.c_int32), ("tag_mode_pct", ctypes.c_int32)]
 
 
 class DistPeer(ctypes.Structure):
@@ -84,7 +83,6 @@ class Info(ctypes.Structure):
                 ("ksmall_threads", ctypes.c_int32), ("ksmall_max_frontier", ctypes.c_int32),
                 ("td_chain", ctypes.c_int32), ("bu_chain", ctypes.c_int32),
                 ("universal_body", ctypes.c_int32), ("prologue", ctypes.c_int32),
-                ("px_parts", ctypes.c_int32), ("px_chain", ctypes.c_int32),
                 ("workspace_bytes", ctypes.c_int64)]
 
 

@@ -67,7 +67,7 @@ for rnd in range(ROUNDS):
             num = ctypes.c_int32()
             lib.s3bfs_get_level_stats(h, buf, 256, ctypes.byref(num))
             levels[key][s] = [(r.level, r.e_l, r.tier, (r.t_explore_end_ns - r.t_explore_begin_ns) / 1e3,
-                               (r.t_end_ns - r.t_explore_end_ns) / 1e3 if r.tier in (1, 5) else 0.0,
+                               (r.t_end_ns - r.t_explore_end_ns) / 1e3 if r.tier == 1 else 0.0,
                                r.candidates, r.kept) for r in buf[: min(num.value, 256)]]
 for key, lib, h in handles:
     lib.s3bfs_destroy(h)
@@ -76,7 +76,7 @@ for key, lib, h in handles:
     tot_ms = sum(p["ms"] for p in per)
     tot_e = sum(edges[s] for s in srcs)
     results[key] = {"gteps": tot_e / tot_ms / 1e6, "per": per}
-    t1 = [x for s in srcs for x in levels[key][s] if x[2] in (1, 5)]
+    t1 = [x for s in srcs for x in levels[key][s] if x[2] == 1]
     kx_us = sum(x[3] for x in t1)
     kc_us = sum(x[4] for x in t1)
     alg = sum(8 * x[1] + 16 * x[5] for x in t1)
@@ -86,6 +86,6 @@ for key, lib, h in handles:
           flush=True)
     worst = max(per, key=lambda p: p["ms"])
     for p in per[:2] + ([worst] if worst not in per[:2] else []):
-        print("    src", p["src"], " ".join(f"[{'X' if x[2] == 5 else 'T'} e={x[1]/1e6:.1f}M kx={x[3]:.0f} kc={x[4]:.0f} c={x[5]/1e6:.2f}M k={x[6]/1e6:.2f}M]"
+        print("    src", p["src"], " ".join(f"[e={x[1]/1e6:.1f}M kx={x[3]:.0f} kc={x[4]:.0f} c={x[5]/1e6:.2f}M k={x[6]/1e6:.2f}M]"
                                            for x in p["heavy"]), flush=True)
 json.dump(results, open(os.environ.get("VARIANT_OUT", "gpurun_out/variants.json"), "w"))

@@ -40,26 +40,15 @@ SETTINGS = [
     # k_explore's tag mode (ids >= hub_vertices tested by their discovery tag alone): tiny
     # graphs are below the default 2^20 hub ids, so these force it -- on every level, on a mix
     # of levels (50 %), after tier-0 / cluster / bottom-up levels (tags written by every tier)
-    # (owner partitioning off: it takes the tag-mode levels when on)
     ("tags-hub1-tier1", dict(debug_poison=1, hub_vertices=1, tag_mode_pct=101,
-                             tier0_max_edges=-1, owner_partition=-1)),
+                             tier0_max_edges=-1)),
     ("tags-hub5-T0-16", dict(debug_poison=1, hub_vertices=5, tag_mode_pct=101,
-                             tier0_max_edges=16, owner_partition=-1)),
+                             tier0_max_edges=16)),
     ("tags-hub3-mixed-levels", dict(debug_poison=1, hub_vertices=3, tag_mode_pct=50,
-                                    tier0_max_edges=-1, owner_partition=-1)),
+                                    tier0_max_edges=-1)),
     ("tags-hub3-bu-mixed", dict(debug_poison=1, hub_vertices=3, tag_mode_pct=101,
                                 tier0_max_edges=16, direction=1, do_alpha=64, do_beta=3)),
     ("tags-never", dict(debug_poison=1, tag_mode_pct=-1, tier0_max_edges=-1)),
-    # R28 owner-partitioned levels: every tier-1 level / the discovery-heavy half of them,
-    # after tier-0 levels, in the host loop, with 3 partitions, and off
-    ("px-every-tier1", dict(debug_poison=1, tag_mode_pct=101, tier0_max_edges=-1)),
-    ("px-mixed-levels", dict(debug_poison=1, tag_mode_pct=50, tier0_max_edges=-1)),
-    ("px-T0-16", dict(debug_poison=1, tag_mode_pct=101, tier0_max_edges=16)),
-    ("px-host-loop", dict(debug_poison=1, tag_mode_pct=101, tier0_max_edges=-1, loop_mode=2)),
-    ("px-3-parts", dict(debug_poison=1, tag_mode_pct=101, tier0_max_edges=-1, max_ctas=3,
-                        edges_per_cta=64)),
-    ("px-grain1", dict(debug_poison=1, tag_mode_pct=101, tier0_max_edges=-1, edges_per_cta=1)),
-    ("px-off", dict(debug_poison=1, owner_partition=-1, tier0_max_edges=-1)),
 ]
 
 
@@ -382,22 +371,3 @@ def test_bounds_checked_build():
     r = subprocess.run([sys.executable, os.path.join(root, "tests", "check_suite.py"), "--quick"],
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "no bounds violation" in r.stdout, (r.stdout[-3000:], r.stderr[-3000:])
-
-
-# ---- R28: owner-partitioned levels run (stats tier 5) and match the oracle ------------------
-@pytest.mark.parametrize("kw", [dict(debug_poison=1), dict(debug_poison=1, loop_mode=2),
-                                dict(debug_poison=1, tier0_max_edges=-1, tag_mode_pct=101,
-                                     max_ctas=7, edges_per_cta=256)])
-def test_owner_partitioned_levels(kw):
-    g = graphgen.rmat(16, 16, seed=9)
-    g.name = "rmat16"
-    ro, col = to_dev(g)
-    bfs = pkg.S3BFS(ro, col, pkg.Options(**kw))
-    assert bfs.info()["px_parts"] >= 1
-    seen = 0
-    for s in graphgen.pick_sources(g, 4, seed=3):
-        check_traversal(g, bfs, int(s))
-        st = bfs.level_stats()
-        seen += int((st["tier"] == 5).sum())
-    bfs.close()
-    assert seen > 0, "no owner-partitioned level ran"
