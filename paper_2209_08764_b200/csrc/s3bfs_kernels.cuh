@@ -102,6 +102,12 @@ namespace s3bfs {
 #ifndef S3BFS_KX_QUEUE
 #define S3BFS_KX_QUEUE 1  // k_explore: claim checks + discoveries via a warp-private queue
 #endif
+#ifndef S3BFS_KX_TAG2
+#define S3BFS_KX_TAG2 1   // k_explore tag mode: hub rechecks as a second in-batch probe round
+#endif
+#ifndef S3BFS_KX_TAG2_MIN_WCAP
+#define S3BFS_KX_TAG2_MIN_WCAP 8192  // ... on levels with at least this many edges per warp
+#endif
 #ifndef S3BFS_KS_ONCHIP
 #define S3BFS_KS_ONCHIP 1  // k_small: Owner race in a shared-memory table (no L2 round trip)
 #endif
@@ -695,6 +701,9 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   const uint32_t *__restrict__ bm = P.bm;
   uint8_t *__restrict__ claim = P.claim;
   const int vs = P.v_sent;  // masked lanes' target: its visited bit is always set
+  // tag mode's second probe round pays on long slices (R-MAT 24: +1.6 %); on short ones the
+  // extra dependent round trip per batch costs more than the queue it spares (R-MAT 20: -1.7 %)
+  const bool tag2 = S3BFS_KX_TAG2 && wcap >= S3BFS_KX_TAG2_MIN_WCAP;
   const int hub = P.hub;                              // ids < hub: bitmap first
   const uint32_t tag_span = (uint32_t)(P.n - P.hub);  // ids in [hub, n): tag only
 
@@ -964,6 +973,23 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
           needm |= (via_tag ? 0u : (~rotr32(r, v[g]) & 1u)) << g;
           discm |= (via_tag ? (uint32_t)(r == 0u) : 0u) << g;
         }
+#if S3BFS_KX_TAG2
+        // Second probe round of tag mode: a hub whose bit is clear at level start is, in a
+        // discovery-heavy level, most often already claimed by an earlier arc of this level
+        // (ncu: 72 % of the level's arcs, each a queue item whose claim load stalled its flush:
+        // 5.8 serial flushes per batch).  Their tags are read here, all groups' loads in flight
+        // at once, and only true discoveries reach the queue (220 M -> 146 M warp instructions
+        // on R-MAT 24's first discovery level; the big mixed levels gain 4-5 %).
+        if (tag2 && __reduce_or_sync(0xffffffffu, needm)) {  // warp-uniform
+          int cl[KX_GROUPS];
+#pragma unroll
+          for (int g = 0; g < KX_GROUPS; ++g)
+            cl[g] = ((needm >> g) & 1u) ? ld_cg_u8_hint(claim + claim_slot(P, v[g]), pol_status) : 1;
+#pragma unroll
+          for (int g = 0; g < KX_GROUPS; ++g) discm |= (uint32_t)(cl[g] == 0) << g;
+          needm = 0;
+        }
+#endif
       } else {
 #pragma unroll
         for (int g = 0; g < KX_GROUPS; ++g) {
