@@ -180,7 +180,7 @@ s3bfs_status build_reordered(s3bfs_ctx *h, cudaStream_t st) {
   CK(h, cudaMemsetAsync(status, 0, (size_t)(tiles + 1) * 8, st));
   k_scan_u32<<<tiles, SCAN_THREADS, 0, st>>>(deg, ro2, n, status);
   k_relabel_rows<<<h->num_sms * 16, 256, 0, st>>>(h->ro, h->col, n2o, o2n, ro2, n, col2);
-  k_build_vinfo<<<grid, 256, 0, st>>>(ro2, n2o, n, h->P.vinfo);
+  k_build_vinfo<<<grid, 256, 0, st>>>(ro2, n2o, n, h->P.vinfo, const_cast<int4 *>(h->P.vs16));
   int h_nz = 0;
   CK(h, nz_b.alloc(4));
   int *d_nz = nz_b.as<int>();
@@ -251,7 +251,7 @@ s3bfs_status build_dist(s3bfs_ctx *h, cudaStream_t st, int nloc) {
   const size_t o_recv = take((size_t)ofs * 8), o_rcnt = take((size_t)G * nwmax * 4);
   const size_t o_rmeta = take((size_t)G * 8), o_rtot = take((size_t)G * 8);
   const size_t o_bm = take(bm_bytes + 16);
-  const size_t o_vinfo = take((size_t)(nloc + 32) * 16);  // the records senders write Owner into
+  const size_t o_vinfo = take((size_t)(nloc + 32) * 32);  // the records senders write Owner into
   h->xws_bytes = off;
   CK(h, cudaMalloc(&h->xws, off));
   char *x = (char *)h->xws;
@@ -600,8 +600,8 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   const size_t nb = (size_t)nv * 4, nb1 = (size_t)(nv + 1) * 4;
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return o; };
-  const size_t o_vinfo = take((size_t)nv * 16);
-  const size_t o_lp = take((size_t)nv * 8);
+  const size_t o_vinfo = take((size_t)nv * 32);  // 32-byte vertex records (Params::vinfo)
+  const size_t o_vs16 = take((size_t)nv * 16);   // dense copy of their static halves
   size_t o_f[2], o_frs[2], o_fex[2];
   for (int i = 0; i < 2; ++i) { o_f[i] = take(nb); o_frs[i] = take(nb); o_fex[i] = take(nb1 + 16); }
   const size_t o_cand = take((size_t)h->cand_cap * 4);
@@ -633,7 +633,7 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   P.n = n;
   P.ctl = (Ctl *)(base + o_ctl);
   P.vinfo = (int4 *)(base + o_vinfo);
-  P.lp = (int2 *)(base + o_lp);
+  P.vs16 = (const int4 *)(base + o_vs16);
   for (int i = 0; i < 2; ++i) {
     P.f[i] = (int32_t *)(base + o_f[i]);
     P.frs[i] = (int32_t *)(base + o_frs[i]);
@@ -690,8 +690,10 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
     P.tro = share->P.tro;
     P.tcol = share->P.tcol;
     h->ro_int = share->ro_int;
-    if ((e = cudaMemcpyAsync(P.vinfo, share->P.vinfo, (size_t)n * 16, cudaMemcpyDeviceToDevice,
-                             stream)) != cudaSuccess)
+    if ((e = cudaMemcpyAsync(P.vinfo, share->P.vinfo, (size_t)n * 32, cudaMemcpyDeviceToDevice,
+                             stream)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(const_cast<int4 *>(P.vs16), share->P.vs16, (size_t)n * 16,
+                             cudaMemcpyDeviceToDevice, stream)) != cudaSuccess)
       return bail(cuda_fail(h, e, "copy vertex records"));
   }
   if (!share && h->opt.validate_csr) {
@@ -717,7 +719,8 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
     s3bfs_status rs = build_reordered(h, stream);
     if (rs != S3BFS_OK) return bail(rs);
   } else {
-    k_build_vinfo<<<h->num_sms * 8, 256, 0, stream>>>(row_offsets, nullptr, n, P.vinfo);
+    k_build_vinfo<<<h->num_sms * 8, 256, 0, stream>>>(row_offsets, nullptr, n, P.vinfo,
+                                                      const_cast<int4 *>(P.vs16));
     if ((e = cudaGetLastError()) != cudaSuccess) return bail(cuda_fail(h, e, "k_build_vinfo"));
     h->ro_int = row_offsets;
   }
@@ -745,7 +748,6 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   if ((e = cudaMemsetAsync(P.status, 0, (size_t)p_max * dist_size * 8 + 8, stream)) != cudaSuccess) return bail(cuda_fail(h, e, "memset(status)"));
   if (h->opt.debug_poison) {
     k_poison<<<h->num_sms * 4, 256, 0, stream>>>(P.vinfo, n, (int)h->cand_cap);
-    cudaMemsetAsync(P.lp, 0x5a, (size_t)n * 8, stream);  // {d, parent} garbage until written
     if ((e = cudaGetLastError()) != cudaSuccess) return bail(cuda_fail(h, e, "k_poison"));
   }
 

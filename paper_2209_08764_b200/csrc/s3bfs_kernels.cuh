@@ -207,10 +207,17 @@ struct Ctl {
 
 struct Params {
   const int32_t *col;           // internal adjacency (degree-ordered copy, or the caller's)
-  int4 *vinfo;                  // per internal vertex: {row start, degree, caller id, Owner
-                                //  (Fig1 L3; never initialised, R3)} -- one sector per probe
-  int2 *lp;                     // per internal vertex: {d, parent (caller id)}, valid where
-                                //  the visited bit is set
+  int4 *vinfo;                  // vertex records, 32 B (one sector) per internal vertex v:
+                                //  vinfo[2v]   = {row start, degree, caller id, 0} (static)
+                                //  vinfo[2v+1] = {d, parent (caller id), Owner, 0}: d/parent
+                                //  valid where the visited bit is set; Owner (Fig1 L3) never
+                                //  initialised (R3).  A discovery is ONE 16-byte store into
+                                //  the sector k_compact's Owner check reads (see vdyn)
+  const int4 *vs16;             // dense copy of the records' static halves, 16 B per vertex
+                                //  ({row start, degree, caller id, 0}, read-only): the small
+                                //  tiers and the bottom-up step read it -- frontiers of
+                                //  near-consecutive ids (paths, grid diagonals, the bottom-up
+                                //  sweep over id order) share its sectors
   const int32_t *n2o, *o2n;     // internal -> caller ids and back (NULL: identity)
   int32_t n;
   Ctl *ctl;
@@ -395,8 +402,51 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
 }
+// vertex record accessors (layout: Params::vinfo)
+__device__ __forceinline__ const int4 *vstat(const int4 *vinfo, int v) {
+  return vinfo + 2 * (long long)v;
+}
+__device__ __forceinline__ int4 *vdyn(int4 *vinfo, int v) { return vinfo + 2 * (long long)v + 1; }
+__device__ __forceinline__ int2 *lp_of(int4 *vinfo, int v) {
+  return reinterpret_cast<int2 *>(vdyn(vinfo, v));
+}
 __device__ __forceinline__ int32_t *owner_of(int4 *vinfo, int v) {
-  return reinterpret_cast<int32_t *>(vinfo + v) + 3;
+  return reinterpret_cast<int32_t *>(vdyn(vinfo, v)) + 2;
+}
+// {row start, degree, caller id, Owner} of v: the static half plus the Owner word of the
+// dynamic half -- both in v's one sector (nc: a kernel that does not write the records;
+// cg: L2-coherent; weak: plain loads, the same SM wrote the Owner)
+__device__ __forceinline__ int4 ld_vrec_nc(const int4 *vinfo, int v) {
+  int4 r = __ldg(vstat(vinfo, v));
+  r.w = __ldg(reinterpret_cast<const int32_t *>(vstat(vinfo, v)) + 6);
+  return r;
+}
+// the same through one 256-bit load (k_compact: one request per candidate)
+__device__ __forceinline__ int4 ld_vrec256_nc(const int4 *vinfo, int v) {
+  int4 r;
+  int d0, d1, d2, d3;
+  asm("ld.global.nc.v8.s32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(d0), "=r"(d1), "=r"(d2), "=r"(r.w), "=r"(d3)
+      : "l"(vstat(vinfo, v)));
+  return r;
+}
+__device__ __forceinline__ int4 ld_vrec_cg(const int4 *vs16, const int4 *vinfo, int v) {
+  int4 r = __ldcg(vs16 + v);  // static half from the dense copy
+  r.w = __ldcg(reinterpret_cast<const int32_t *>(vstat(vinfo, v)) + 6);
+  return r;
+}
+__device__ __forceinline__ int4 ld_vrec_weak(const int4 *vinfo, int v) {
+  int4 r;
+  asm volatile("ld.global.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(vstat(vinfo, v)));
+  asm volatile("ld.global.s32 %0, [%1];"
+               : "=r"(r.w) : "l"(reinterpret_cast<const int32_t *>(vstat(vinfo, v)) + 6));
+  return r;
+}
+// EXPLORE-VERTEX's labelling (Fig1 L18, L22) in one plain 16-byte store: {d, parent, Owner}
+__device__ __forceinline__ void st_discovery(int4 *vinfo, int v, int d, int parent, int owner) {
+  asm volatile("st.global.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(vdyn(vinfo, v)), "r"(d),
+               "r"(parent), "r"(owner), "r"(0) : "memory");
 }
 
 // k_small's on-chip Owner table: round r's bijection of the 32-bit ids (odd multiplies,
@@ -628,8 +678,8 @@ __global__ void k_init(Params P, int32_t s, int32_t *level, int32_t *parent) {
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     Ctl *c = P.ctl;
-    const int4 vs = P.vinfo[si];
-    P.lp[si] = make_int2(0, s);
+    const int4 vs = *vstat(P.vinfo, si);
+    *lp_of(P.vinfo, si) = make_int2(0, s);
     P.f[0][0] = s;        // Fig1 L7: CurLevelVertices <- [s]
     P.frs[0][0] = vs.x;
     P.fex[0][0] = 0;      // exclusive degree scan of the frontier (R5)
@@ -696,7 +746,6 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
   const int32_t *__restrict__ fex = P.fex[cur];
   const int32_t *__restrict__ col = P.col;
   int4 *__restrict__ vinfo = P.vinfo;
-  int2 *__restrict__ lp = P.lp;
   int32_t *__restrict__ cand = P.cand;
   const uint32_t *__restrict__ bm = P.bm;
   uint8_t *__restrict__ claim = P.claim;
@@ -858,8 +907,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
       if (disc) {
         const int slot = segbase + wcount + __popc(m & lanemask_lt());
         st_u8(claim + claim_slot(P, v[g]), tag);
-        st_weak_v2(lp + v[g], new_level, par);     // d[v] <- l, parent (Fig1 L18)
-        st_weak(owner_of(vinfo, v[g]), slot);      // Owner[v] <- i (benign race)
+        st_discovery(vinfo, v[g], new_level, par, slot);  // d[v] <- l, parent, Owner[v] <- i
         cand[slot] = v[g];                         // Q[i].Enqueue(v)
       }
       wcount += __popc(m);
@@ -906,8 +954,8 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
         S3_CHK(v, P.n);
         S3_CHK(slot, (long long)(b * KD_WARPS + warp + 1) * wcap);
         st_u8(claim + cs, tag);
-        st_weak_v2(lp + v, new_level, it.y);   // d[v] <- l, parent (Fig1 L18)
-        st_weak(owner_of(vinfo, v), slot);     // Owner[v] <- i (benign race)
+        st_discovery(vinfo, v, new_level, it.y, slot);  // d[v] <- l, parent (Fig1 L18),
+                                                        // Owner[v] <- i (benign race)
         cand[slot] = v;                        // Q[i].Enqueue(v)
       }
       wcount += __popc(m);
@@ -1116,7 +1164,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
     int4 vi[KC_GROUPS];  // {row start, degree, caller id, Owner}: one sector per candidate
 #pragma unroll
     for (int g = 0; g < KC_GROUPS; ++g)
-      vi[g] = (v[g] >= 0) ? __ldg(vinfo + v[g]) : make_int4(0, 0, 0, -1);
+      vi[g] = (v[g] >= 0) ? ld_vrec256_nc(vinfo, v[g]) : make_int4(0, 0, 0, -1);
 #pragma unroll
     for (int g = 0; g < KC_GROUPS; ++g) {
       const int k = k0 + g * 32 + lane;
@@ -1288,8 +1336,8 @@ __global__ void k_dist_init(Params P, int32_t s) {
     int n_l = 0, e_l = 0;
     if ((si >> 5) % P.dist_size == P.dist_rank) {  // the source's owner seeds its frontier
       const int ls = dist_local(P, si);
-      const int4 vs = P.vinfo[ls];
-      P.lp[ls] = make_int2(0, s);
+      const int4 vs = *vstat(P.vinfo, ls);
+      *lp_of(P.vinfo, ls) = make_int2(0, s);
       P.f[0][0] = s;
       P.frs[0][0] = vs.x;
       P.fex[0][0] = 0;
@@ -1355,13 +1403,13 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_dist_keep(Params 
         if (k < cnt) {
           it = P.recv[base + k];
           lv = dist_local(P, it.x);
-          vi = ld_weak_v4(P.vinfo + lv);  // Owner written by the senders' k_explore
+          vi = ld_vrec_weak(P.vinfo, lv);  // Owner written by the senders' k_explore
         }
         // the surviving label's copy, unless v was visited in an earlier level: a sender's tag
         // mode knows only its own sends, so it may send a vertex another rank found before
         const bool keep = k < cnt && vi.w == (int)(base + k) &&
                           !((__ldcg(P.bm + (it.x >> 5)) >> (it.x & 31)) & 1u);
-        if (keep) P.lp[lv] = make_int2(new_level, it.y);  // d[v] <- l, parent (Fig1 L18)
+        if (keep) *lp_of(P.vinfo, lv) = make_int2(new_level, it.y);  // d[v] <- l, parent (Fig1 L18)
         for (int d = 0; d < P.dist_size; ++d)             // the owner's bitmap words, in its own
           bm_publish(P.p_bm[d], keep, it.x, lane);         // replica and every peer's
         const unsigned mk = __ballot_sync(0xffffffffu, keep);
@@ -1403,7 +1451,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_dist_keep(Params 
         int4 vi = make_int4(0, 0, 0, 0);
         if (k < ks) {
           v = P.recv[base + k].x;
-          vi = __ldg(P.vinfo + dist_local(P, v));
+          vi = __ldg(vstat(P.vinfo, dist_local(P, v)));
         }
         const int d = k < ks ? vi.y : 0;
         const int inc = warp_incl_scan(d);
@@ -1484,7 +1532,7 @@ __global__ void k_dist_finalize(Params P, int32_t *level, int32_t *parent) {
     if (v >= P.n) continue;
     if ((__ldg(P.bm + (v >> 5)) >> (v & 31)) & 1u) {
       const int o = P.n2o ? __ldg(P.n2o + v) : v;
-      const int2 r = P.lp[lv];
+      const int2 r = *lp_of(P.vinfo, lv);
       level[o] = r.x;
       parent[o] = r.y;
     }
@@ -1526,7 +1574,8 @@ __global__ void k_dist_build_vinfo(Params P, const int32_t *ro_l, const int32_t 
        lv += (long long)gridDim.x * blockDim.x) {
     const int v = dist_global(P, (int)lv);
     const int cid = v < P.n ? (n2o ? n2o[v] : v) : -1;
-    vinfo_l[lv] = make_int4(ro_l[lv], ro_l[lv + 1] - ro_l[lv], cid, -1);
+    vinfo_l[2 * lv] = make_int4(ro_l[lv], ro_l[lv + 1] - ro_l[lv], cid, 0);
+    vinfo_l[2 * lv + 1] = make_int4(-1, -1, -1, 0);
   }
 }
 
@@ -1565,7 +1614,7 @@ __device__ void tiny_levels(const Params &P, Ctl *c, int32_t *sf, int32_t *srs, 
     const uint32_t w = __ldcg(P.bm + (v >> 5));      // published by atomicOr at L2
     // issued together with the bitmap word; through L2 (ld.global.cg), never the read-only
     // path: k_small's block levels store Owner into the same 16-byte record in this launch
-    const int4 vi = __ldcg(P.vinfo + v);
+    const int4 vi = __ldcg(P.vs16 + v);
     const bool fresh = has && !((w >> (v & 31)) & 1u);
     const unsigned fm = __ballot_sync(0xffffffffu, fresh);
     const int ncand = __popc(fm);
@@ -1576,7 +1625,7 @@ __device__ void tiny_levels(const Params &P, Ctl *c, int32_t *sf, int32_t *srs, 
     }
     const unsigned km = ncand > 1 ? __ballot_sync(0xffffffffu, keep) : fm;
     if (keep) {
-      P.lp[v] = make_int2(L + 1, px);                 // d[v] <- l, parent (Fig1 L18)
+      *lp_of(P.vinfo, v) = make_int2(L + 1, px);      // d[v] <- l, parent (Fig1 L18)
       atomicOr(P.bm + (v >> 5), 1u << (v & 31));      // exact visited bit
       mark_tag(P, v);
     }
@@ -1723,7 +1772,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
 #pragma unroll
     for (int i = 0; i < KS_IPT; ++i) {
       wv[i] = ev[i] >= 0 ? __ldcg(bm + (ev[i] >> 5)) : 0xffffffffu;
-      rv[i] = ev[i] >= 0 ? __ldcg(vinfo + ev[i]) : make_int4(0, 0, 0, 0);
+      rv[i] = ev[i] >= 0 ? __ldcg(P.vs16 + ev[i]) : make_int4(0, 0, 0, 0);
     }
     uint32_t open = 0;  // this thread's candidates (visited bit clear) not yet decided
 #pragma unroll
@@ -1769,7 +1818,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
       if ((km >> i) & 1u) {
         const int v = ev[i];
         kv[i] = rv[i].z; kr[i] = rv[i].x; kd[i] = rv[i].y;
-        P.lp[v] = make_int2(L + 1, ux[i]);          // d[v] <- l, parent (Fig1 L18)
+        *lp_of(vinfo, v) = make_int2(L + 1, ux[i]);  // d[v] <- l, parent (Fig1 L18)
         atomicOr(P.bm + (v >> 5), 1u << (v & 31));  // exact visited bit (not discovery)
         mark_tag(P, v);
       }
@@ -1809,7 +1858,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
       const int e = e0 + i;
       const int v = (i < ipt && e < e_l) ? cv[e] : -1;
       kv[i] = v;
-      vis[i] = v >= 0 ? ld_weak_v4(vinfo + v) : make_int4(0, 0, 0, -1);  // same-SM: coherent
+      vis[i] = v >= 0 ? ld_vrec_weak(vinfo, v) : make_int4(0, 0, 0, -1);  // same-SM: coherent
     }
 #pragma unroll
     for (int i = 0; i < KS_IPT; ++i) {
@@ -1820,7 +1869,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1) k_small(Params P) {
       kd[i] = 0;
       if (v >= 0 && vis[i].w == e) {
         kv[i] = vis[i].z; kr[i] = vis[i].x; kd[i] = vis[i].y;
-        P.lp[v] = make_int2(L + 1, cpv[e]);         // d[v] <- l, parent (Fig1 L18)
+        *lp_of(vinfo, v) = make_int2(L + 1, cpv[e]);  // d[v] <- l, parent (Fig1 L18)
         atomicOr(P.bm + (v >> 5), 1u << (v & 31));  // exact visited bit (not discovery)
         mark_tag(P, v);
       }
@@ -2014,7 +2063,7 @@ __global__ void __cluster_dims__(KC_CL, 1, 1) __launch_bounds__(KC_THREADS, 1) k
       const int k = k0 + i;
       const int v = (i < ipt && k < ne) ? cv[k] : -1;
       kv[i] = v;
-      vis[i] = v >= 0 ? __ldcg(vinfo + v) : make_int4(0, 0, 0, -1);
+      vis[i] = v >= 0 ? ld_vrec_cg(P.vs16, vinfo, v) : make_int4(0, 0, 0, -1);
     }
     int cnt = 0, dsum = 0;
 #pragma unroll
@@ -2026,7 +2075,7 @@ __global__ void __cluster_dims__(KC_CL, 1, 1) __launch_bounds__(KC_THREADS, 1) k
       kd[i] = 0;
       if (v >= 0 && vis[i].w == lo + k) {
         kv[i] = vis[i].z; kr[i] = vis[i].x; kd[i] = vis[i].y;
-        P.lp[v] = make_int2(L + 1, cpv[k]);          // d[v] <- l, parent (Fig1 L18)
+        *lp_of(vinfo, v) = make_int2(L + 1, cpv[k]);  // d[v] <- l, parent (Fig1 L18)
         atomicOr(P.bm + (v >> 5), 1u << (v & 31));   // exact visited bit (not discovery)
         mark_tag(P, v);
         ++cnt;
@@ -2198,7 +2247,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params 
       const bool act = w < w1 && v < nscan && !((bw[i] >> lane) & 1u);
       r0[i] = act ? __ldg(P.tro + v) : 0;
       r1[i] = act ? __ldg(P.tro + v + 1) : 0;
-      dg[i] = act ? __ldg(vinfo + v).y : 0;  // out-degree: the next level's e_l (Fig1 L13)
+      dg[i] = act ? __ldg(P.vs16 + v).y : 0;  // out-degree: the next level's e_l (Fig1 L13)
       pu[i] = -1;
     }
     for (;;) {  // rounds until every vertex found a frontier in-neighbour or ran out of them
@@ -2241,7 +2290,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params 
       const int v = (w << 5) + lane;
       const bool found = pu[i] >= 0;
       if (found) {
-        P.lp[v] = make_int2(new_level, __ldg(vinfo + pu[i]).z);  // d, parent (caller)
+        *lp_of(P.vinfo, v) = make_int2(new_level, __ldg(P.vs16 + pu[i]).z);  // d, parent (caller)
         mark_tag(P, v);
       }
       const unsigned m = __ballot_sync(0xffffffffu, found);
@@ -2282,7 +2331,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params 
     const uint32_t m = fbn[w];
     if (!m) continue;
     const bool mine = (m >> lane) & 1u;
-    const int4 vi = mine ? __ldg(vinfo + (w << 5) + lane) : make_int4(0, 0, 0, 0);
+    const int4 vi = mine ? __ldg(P.vs16 + (w << 5) + lane) : make_int4(0, 0, 0, 0);
     const int d = mine ? vi.y : 0;
     const int inc = warp_incl_scan(d);
     const int pos = koff + __popc(m & lanemask_lt());
@@ -2333,7 +2382,7 @@ __global__ void k_finalize(Params P) {
     S3_CHK(i, P.n);
     int lv = -1, pa = -1;
     if ((__ldg(P.bm + (i >> 5)) >> (i & 31)) & 1u) {
-      const int2 r = __ldg(P.lp + i);
+      const int2 r = __ldg(reinterpret_cast<const int2 *>(vstat(P.vinfo, i) + 1));
       lv = r.x;
       pa = r.y;
     }
@@ -2421,11 +2470,16 @@ __global__ void k_count_nonzero(const int32_t *deg, int n, int *out) {
   c = warp_sum(c);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
-// vinfo[i] = {row start, degree, caller id, Owner = 0} over a CSR's row offsets
-__global__ void k_build_vinfo(const int32_t *ro, const int32_t *n2o, int n, int4 *vinfo) {
+// the vertex records (Params::vinfo) over a CSR's row offsets: static half, dynamic half reset
+__global__ void k_build_vinfo(const int32_t *ro, const int32_t *n2o, int n, int4 *vinfo,
+                              int4 *vs16) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    vinfo[i] = make_int4(ro[i], ro[i + 1] - ro[i], n2o ? n2o[i] : (int)i, 0);
+       i += (long long)gridDim.x * blockDim.x) {
+    const int4 st = make_int4(ro[i], ro[i + 1] - ro[i], n2o ? n2o[i] : (int)i, 0);
+    vinfo[2 * i] = st;
+    vinfo[2 * i + 1] = make_int4(-1, -1, 0, 0);
+    vs16[i] = st;
+  }
 }
 
 // ---- test entry kernels ---------------------------------------------------------------------
@@ -2509,7 +2563,8 @@ __global__ void k_validate(const int32_t *ro, const int32_t *col, int n, long lo
 __global__ void k_poison(int4 *vinfo, int n, int range) {
   const long long gs = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gs)
-    vinfo[i].w = (int32_t)(((unsigned)i * 2654435761u) % (unsigned)max(range, 1));
+    vinfo[2 * i + 1] = make_int4(0x5a5a5a5a, 0x5a5a5a5a,  // {d, parent} garbage until written
+                                 (int32_t)(((unsigned)i * 2654435761u) % (unsigned)max(range, 1)), 0);
 }
 
 }  // namespace s3bfs
