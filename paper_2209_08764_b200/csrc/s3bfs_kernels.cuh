@@ -108,6 +108,9 @@ namespace s3bfs {
 #ifndef S3BFS_KX_TAG2_MIN_WCAP
 #define S3BFS_KX_TAG2_MIN_WCAP 8192  // ... on levels with at least this many edges per warp
 #endif
+#ifndef S3BFS_KC_REVERSE
+#define S3BFS_KC_REVERSE 1  // k_compact walks every candidate segment newest entry first
+#endif
 #ifndef S3BFS_KS_ONCHIP
 #define S3BFS_KS_ONCHIP 1  // k_small: Owner race in a shared-memory table (no L2 round trip)
 #endif
@@ -1152,7 +1155,16 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
   if (b == 0 && tid == 0) c->t_kx_end = globaltimer();
 
   int kept = 0, dsum = 0;
+  // S3BFS_KC_REVERSE: newest candidates first -- their records are the ones k_explore's
+  // discovery stores left in L2; walking oldest first, the gathers that miss push exactly
+  // those out before they are read.  The kept entries are then compacted towards the
+  // segment's end (write position >= every unread entry), pass 2 reads them from there.
+#if S3BFS_KC_REVERSE
+  for (int k0 = cnt > 0 ? ((cnt - 1) / (32 * KC_GROUPS)) * (32 * KC_GROUPS) : -1; k0 >= 0;
+       k0 -= 32 * KC_GROUPS) {
+#else
   for (int k0 = 0; k0 < cnt; k0 += 32 * KC_GROUPS) {
+#endif
     int v[KC_GROUPS];
 #pragma unroll
     for (int g = 0; g < KC_GROUPS; ++g) {
@@ -1173,7 +1185,11 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
       bm_publish(P.bm, keep, v[g], lane);  // exact visited bit (R17)
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       if (keep) {
+#if S3BFS_KC_REVERSE
+        const int q = seg + cnt - 1 - kept - __popc(m & lanemask_lt());
+#else
         const int q = seg + kept + __popc(m & lanemask_lt());
+#endif
         S3_CHK(q, P.cand_cap);
         cand[q] = vi[g].z;
         crd[q] = make_int2(vi[g].x, d);
@@ -1255,8 +1271,9 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
     const int k = k0 + lane;
     int v = 0, r0 = 0, d = 0;
     if (k < kept) {
-      v = cand[seg + k];
-      const int2 rd = crd[seg + k];
+      const int kk = S3BFS_KC_REVERSE ? cnt - kept + k : k;  // kept entries: the segment's end
+      v = cand[seg + kk];
+      const int2 rd = crd[seg + kk];
       r0 = rd.x;
       d = rd.y;
     }
