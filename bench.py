@@ -133,7 +133,15 @@ def launches_from_stats(st, td_chain: int = 1, bu_chain: int = 1, universal: int
     or, universal, the sequence S C T^td [B^bu T^td] C S from its tier on; with prologue that
     whole sequence first runs once between k_init and the loop; every kernel of a chain
     launches (idle ones return at once); then k_finalize."""
-    tiers = [{0: "S", 1: "T", 3: "B", 4: "C"}[int(t)] for t in st["tier"] if t in (0, 1, 3, 4)]
+    # a tier-1 level that ran as p passes (level passes, `pad` of its record) is p T entries
+    try:
+        passes = [int(p) for p in st["pad"]]
+    except (KeyError, ValueError, IndexError):
+        passes = [1] * len(st["tier"])
+    tiers = []
+    for t, p in zip(st["tier"], passes):
+        if t in (0, 1, 3, 4):
+            tiers += [{0: "S", 1: "T", 3: "B", 4: "C"}[int(t)]] * (max(1, p) if int(t) == 1 else 1)
     seq = "SC" + "T" * td_chain + ("B" * bu_chain + "T" * td_chain if direction else "") + "CS"
     cost = {"S": 1, "C": 1, "T": 2, "B": 3}
     n, i, first = 1, 0, bool(prologue)

@@ -99,6 +99,15 @@ typedef struct {
                               percentage of all arcs end at visited vertices (the discovery-heavy
                               levels); other levels test every target's visited bit first.
                               0 -> the default (80); > 100 -> every level; < 0 -> never */
+  int32_t split_min_edges; /* level passes (Fig1 L18's "d[v] = infinity" state refreshed inside a
+                              level): a tier-1 level of at least this many edges whose visited
+                              test is in tag mode runs as consecutive passes over its edge range,
+                              each a complete explore + dedup that publishes its discoveries'
+                              visited bits and appends its survivors to the next frontier; the
+                              level's result is the same.  0 -> the default; < 0 -> never */
+  int32_t split_first_pct; /* the first pass's share of the level's edges, percent (0 -> default) */
+  int32_t split_passes;    /* passes per such level (the rest of the edges is divided evenly
+                              over the later passes).  0 -> the default; 1 -> never split */
 } s3bfs_options;
 
 /* One record per BFS level (the SPEC LevelStats analogue).  n_l = |frontier|

@@ -653,6 +653,11 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
     P.hub = (int32_t)(hub < n ? hub : n);
     const int tp = h->opt.tag_mode_pct;
     P.tag_pct = tp == 0 ? S3BFS_TAG_MODE_PCT : tp < 0 ? -1 : tp;
+    // level passes (plan_pass): defaults from the R-MAT 24 sweep (profiles/r02_level_passes.log)
+    const int sm = h->opt.split_min_edges, sp = h->opt.split_first_pct, sn = h->opt.split_passes;
+    P.split_min = sm == 0 ? S3BFS_SPLIT_MIN_EDGES : sm;
+    P.split_pct = sp <= 0 ? S3BFS_SPLIT_FIRST_PCT : sp > 99 ? 99 : sp;
+    P.split_passes = sn == 0 ? S3BFS_SPLIT_PASSES : sn;
   }
   P.fb[0] = (uint32_t *)(base + o_fb0);
   P.fb[1] = (uint32_t *)(base + o_fb1);

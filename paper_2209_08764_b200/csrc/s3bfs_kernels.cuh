@@ -111,6 +111,24 @@ namespace s3bfs {
 #ifndef S3BFS_KC_REVERSE
 #define S3BFS_KC_REVERSE 1  // k_compact walks every candidate segment newest entry first
 #endif
+#ifndef S3BFS_SPLIT_MIN_EDGES
+#define S3BFS_SPLIT_MIN_EDGES (32 << 20)  // level passes: default of opts.split_min_edges
+#endif
+#ifndef S3BFS_SPLIT_FIRST_PCT
+#define S3BFS_SPLIT_FIRST_PCT 6           // default of opts.split_first_pct
+#endif
+#ifndef S3BFS_SPLIT_PASSES
+#define S3BFS_SPLIT_PASSES 2              // default of opts.split_passes
+#endif
+#ifndef S3BFS_KX_TRANSPOSE
+#define S3BFS_KX_TRANSPOSE 1  // k_explore: a CTA's warps take slices spread over the whole range
+#endif
+#ifndef S3BFS_KX_PIECES
+#define S3BFS_KX_PIECES 4  // k_explore: pieces per worker's share (with S3BFS_KX_TRANSPOSE)
+#endif
+#ifndef S3BFS_KX_PIECES_MIN_EDGES
+#define S3BFS_KX_PIECES_MIN_EDGES 4096  // ... on shares of at least this many edges
+#endif
 #ifndef S3BFS_KS_ONCHIP
 #define S3BFS_KS_ONCHIP 1  // k_small: Owner race in a shared-memory table (no L2 round trip)
 #endif
@@ -188,7 +206,12 @@ struct Ctl {
   int32_t p_l;        // P_l = CTAs of this level (Fig1 L16)
   int32_t chunk;      // edges per CTA (ceil(e_l / P_l))
   int32_t wcap;       // edges (= candidate capacity) per warp
-  int32_t e_lo, e_hi; // the level's edge range explored here (0, e_l)
+  int32_t e_lo, e_hi; // the edge range [e_lo, e_hi) of the level this pass explores: the
+                      // whole level, or one of its passes (see plan_pass)
+  int32_t pieces;     // pieces per worker's share of the pass (k_explore)
+  int32_t pass;       // passes of the current level already done
+  int32_t n_acc, e_acc;  // next frontier entries / degree sum the level's earlier passes wrote
+  unsigned long long t_kx_first, kx_ns;  // stats: first pass's k_explore start, summed k_explore ns
   int32_t g_n_next, g_e_next;  // NEXT-4: the next level's frontier size / edges over all ranks
   int32_t n_next, e_next;   // written by the last k_compact CTA in tile order
   uint32_t done_ctr;        // last-CTA election in k_compact (not the discovery path)
@@ -241,6 +264,9 @@ struct Params {
   int32_t hub;                  // k_explore tag mode: ids < hub are tested in the bitmap
                                 //  first, the others by their discovery tag alone (one probe)
   int32_t tag_pct;              // tag mode while m_visited < tag_pct % of nnz (< 0: never)
+  int32_t split_min, split_pct, split_passes;  // level passes (plan_pass): levels of at least
+                                //  split_min edges in tag mode run in up to split_passes passes,
+                                //  the first over split_pct % of the level's edges (<= 0: off)
   uint32_t *fb[2];              // NEXT-3: frontier bitmaps (bottom-up levels only)
   const int32_t *tro, *tcol;    // NEXT-3: in-adjacency (internal ids) the bottom-up step scans
   int32_t *wcnt;
@@ -574,13 +600,14 @@ __device__ __forceinline__ void record_stat_at(const Params &P, int &k, int32_t 
 __device__ void record_stat(const Params &P, Ctl *c, int32_t level, int32_t n_l, int32_t e_l,
                             int32_t tier, int32_t grid, int32_t cand, int32_t kept,
                             unsigned long long t0, unsigned long long t1,
-                            unsigned long long tx0 = 0, unsigned long long tx1 = 0) {
+                            unsigned long long tx0 = 0, unsigned long long tx1 = 0,
+                            int32_t passes = 0) {
   if (!P.collect_stats) return;
   const int k = c->num_levels;
   if (k < P.stats_cap) {
     s3bfs_level_stat r;
     r.level = level; r.n_l = n_l; r.e_l = e_l; r.tier = tier; r.grid = grid;
-    r.candidates = cand; r.kept = kept; r.pad = 0; r.t_begin_ns = t0; r.t_end_ns = t1;
+    r.candidates = cand; r.kept = kept; r.pad = passes; r.t_begin_ns = t0; r.t_end_ns = t1;
     r.t_explore_begin_ns = tx0; r.t_explore_end_ns = tx1;
     P.stats[k] = r;
   }
@@ -599,6 +626,7 @@ __device__ void steer(const Params &P, int tier) {
 }
 
 __device__ void decide_tier(const Params &P, Ctl *c, int32_t n_l, int32_t e_l);
+__device__ void plan_pass(const Params &P, Ctl *c);
 __device__ void decide(const Params &P, Ctl *c, int32_t n_l, int32_t e_l) {
   decide_tier(P, c, n_l, e_l);
   steer(P, c->tier);
@@ -638,7 +666,41 @@ __device__ void decide_tier(const Params &P, Ctl *c, int32_t n_l, int32_t e_l) {
     c->p_l = KC_CL;
     return;
   }
-  const long long e_lo = 0, e_hi = e_l, es = e_l;
+  c->tier = TIER_LARGE;
+  c->pass = 0;
+  c->n_acc = 0;
+  c->e_acc = 0;
+  c->kx_ns = 0;
+  plan_pass(P, c);
+}
+// The next pass of the tier-1 level in ctl: its edge range, visited-test mode and grid.
+// Level passes.  A discovery-heavy level reaches each new vertex many times (R-MAT 24: ~16
+// arcs per discovered vertex on the mixed levels, ~90 per hub on the first discovery level);
+// only the first is a discovery, every later one must ask L2 for the claim tag because the
+// visited bitmap is exact at level START only (measured 4.5 us per 10^6 such re-checks
+// against 1.46 us per 10^6 plain arcs: the largest term of those levels).  Such a level runs
+// as passes over consecutive edge ranges [e_lo, e_hi) of the same frontier and degree scan:
+// every pass is a complete k_explore + k_compact (Owner dedup, visited bits published,
+// survivors APPENDED to the next frontier), so the later passes find the vertices of the
+// earlier ones in the bitmap.  Same level number, same result: a pass boundary is just a point
+// where the level's "d[v] = infinity" state is refreshed; P_l is sized per pass (Fig1 L16).
+// A small first pass pays most: after 1/8 of the edges ~88 % of the level's new vertices
+// (those with many arcs) are already found.
+__device__ void plan_pass(const Params &P, Ctl *c) {
+  const long long e_l = c->e_l;
+  const long long e_lo = c->pass == 0 ? 0 : c->e_hi;
+  // k_explore's visited test: tag mode while few arcs end at visited vertices (m_visited =
+  // degrees of all visited vertices, the frontier included; arc ends for a symmetric graph)
+  c->probe_tags = P.tag_pct >= 0 &&
+                  (double)c->m_visited * 100.0 < (double)P.nnz_all * (double)P.tag_pct;
+  long long e_hi = e_l;
+  if (P.variant == 0 && P.dist_size == 1 && P.split_passes > 1 && P.split_min > 0 &&
+      e_l >= P.split_min && c->probe_tags && c->pass + 1 < P.split_passes) {
+    const long long first = max(e_l * P.split_pct / 100, 1LL);
+    const long long rest = (e_l - first + P.split_passes - 2) / (P.split_passes - 1);
+    e_hi = min(e_l, c->pass == 0 ? first : e_lo + max(rest, 1LL));
+  }
+  const long long es = e_hi - e_lo;
   long long pt = P.variant ? (long long)P.p_max
                            : min((long long)P.p_max, (es + P.grain - 1) / P.grain);
   if (pt < 1) pt = 1;
@@ -647,14 +709,20 @@ __device__ void decide_tier(const Params &P, Ctl *c, int32_t n_l, int32_t e_l) {
   if (p_l < 1) p_l = 1;  // an empty slice still runs one (idle) CTA: k_compact reports 0
   c->e_lo = (int32_t)e_lo;
   c->e_hi = (int32_t)e_hi;
-  // k_explore's visited test: tag mode while few arcs end at visited vertices (m_visited =
-  // degrees of all visited vertices, the frontier included; arc ends for a symmetric graph)
-  c->probe_tags = P.tag_pct >= 0 &&
-                  (double)c->m_visited * 100.0 < (double)P.nnz_all * (double)P.tag_pct;
-  c->tier = TIER_LARGE;
   c->p_l = (int32_t)p_l;
   c->chunk = (int32_t)chunk;
+#if S3BFS_KX_TRANSPOSE
+  {  // edges (= candidate capacity) per worker: `pieces` pieces of equal length
+    const long long w = max((es + p_l * KD_WARPS - 1) / (p_l * KD_WARPS), 1LL);
+    const int pieces = w >= S3BFS_KX_PIECES_MIN_EDGES ? S3BFS_KX_PIECES : 1;
+    const long long plen = (w + pieces - 1) / pieces;
+    c->pieces = pieces;
+    c->wcap = (int32_t)(plen * pieces);
+  }
+#else
+  c->pieces = 1;
   c->wcap = (int32_t)((chunk + KD_WARPS - 1) / KD_WARPS);  // edges (and candidates) per warp
+#endif
 }
 
 // ---- init (Fig1 L1-L8) ----------------------------------------------------------------------
@@ -763,10 +831,33 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
     if (!DIST) P.status[b] = 0ull;  // reset k_compact's look-back word
     if (b == 0) c->t_kx_begin = globaltimer();
   }
+#if S3BFS_KX_TRANSPOSE
+  // Worker (b, warp) takes slice warp * P_l + b of the pass's P_l * KD_WARPS equal slices: a
+  // CTA's warps sample the whole edge range, so every CTA sees the same mix of long and short
+  // rows whatever the order of the frontier (a frontier whose first part holds the
+  // high-degree vertices -- the survivors of an earlier pass -- left the CTAs of the
+  // short-row part 20 % behind the others with contiguous chunks)
+  // ... and each worker's share is `pieces` equal pieces spread over the range the same way
+  // (piece j of worker t = piece j * P_l * KD_WARPS + t): every WARP then walks the same mix,
+  // and the kernel does not end on the warps whose one slice held only short rows
+  (void)chunk;
+  const int pieces = c->pieces, plen = wcap / pieces;
+  int e_begin = 0, e_end = 0;
+  auto set_piece = [&](int j) {
+    const long long es0 = (long long)c->e_lo +
+                          ((long long)j * p_l * KD_WARPS + (warp * p_l + b)) * plen;
+    e_begin = (int)min(es0, (long long)c->e_hi);
+    e_end = (int)min((long long)e_begin + plen, (long long)c->e_hi);
+  };
+  set_piece(0);
+#else
+  const int pieces = 1;
+  auto set_piece = [&](int) {};
   const int E0 = c->e_lo + b * chunk;
   const int E1 = min(E0 + chunk, c->e_hi);
   const int e_begin = min(E0 + warp * wcap, E1);
   const int e_end = min(e_begin + wcap, E1);
+#endif
   const int segbase = (b * KD_WARPS + warp) * wcap;
   const unsigned long long pol_stream = P.pol_first;
   const unsigned long long pol_status = P.pol_last;
@@ -1080,8 +1171,16 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_explore(Params P)
     }
   };
 #endif
-  if (c->probe_tags) run(std::true_type{});
-  else run(std::false_type{});
+  for (int j = 0;;) {
+    if (c->probe_tags) run(std::true_type{});
+    else run(std::false_type{});
+    if (++j >= pieces) break;
+    set_piece(j);
+    if (e_begin < e_end) {
+      u0 = warp_search(fex, n_l, e_begin);
+      load_window(u0);
+    }
+  }
 #if S3BFS_KX_QUEUE
   if (qn > 0) flush(qn);  // warp-uniform: the slice's remaining items
 #endif
@@ -1152,6 +1251,7 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
   int2 *__restrict__ crd = P.cand_rd;
   const int seg = (b * KD_WARPS + warp) * c->wcap;
   const int cnt = P.wcnt[b * KD_WARPS + warp];
+  const int n_acc = c->n_acc, e_acc = c->e_acc;  // written by the level's earlier passes
   if (b == 0 && tid == 0) c->t_kx_end = globaltimer();
 
   int kept = 0, dsum = 0;
@@ -1233,13 +1333,14 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
       __nanosleep(ns);
       if (ns < S3BFS_LB_MAX_NS) ns <<= 1;
     }
-    koff = (int)ex.a + __shfl_sync(0xffffffffu, ik - kk, warp);
-    doff = (int)ex.b + __shfl_sync(0xffffffffu, id - dd, warp);
-    if (b == p_l - 1 && tid == 0) {  // the level's totals: n_{l+1}, e_{l+1} (Fig1 L15)
+    // (the level's earlier passes already wrote n_acc entries with degree sum e_acc)
+    koff = n_acc + (int)ex.a + __shfl_sync(0xffffffffu, ik - kk, warp);
+    doff = e_acc + (int)ex.b + __shfl_sync(0xffffffffu, id - dd, warp);
+    if (b == p_l - 1 && tid == 0) {  // the pass's totals -> n_{l+1}, e_{l+1} (Fig1 L15)
       const int n_next = (int)(ex.a + agg.a), e_next = (int)(ex.b + agg.b);
       c->n_next = n_next;
       c->e_next = e_next;
-      P.fex[nxt][n_next] = e_next;
+      P.fex[nxt][n_acc + n_next] = e_acc + e_next;
     }
   }
 #else
@@ -1251,14 +1352,14 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
                    (uint32_t)__shfl_sync(0xffffffffu, id, 31)};
     const Pair ex = lookback<true>(P.status, b, agg);
     if (lane < KD_WARPS) {
-      s_k[lane] = (int)ex.a + ik - kk;
-      s_d[lane] = (int)ex.b + id - dd;
+      s_k[lane] = n_acc + (int)ex.a + ik - kk;
+      s_d[lane] = e_acc + (int)ex.b + id - dd;
     }
-    if (b == p_l - 1 && lane == 0) {  // the level's totals: n_{l+1}, e_{l+1} (Fig1 L15)
+    if (b == p_l - 1 && lane == 0) {  // the pass's totals -> n_{l+1}, e_{l+1} (Fig1 L15)
       const int n_next = (int)(ex.a + agg.a), e_next = (int)(ex.b + agg.b);
       c->n_next = n_next;
       c->e_next = e_next;
-      P.fex[nxt][n_next] = e_next;
+      P.fex[nxt][n_acc + n_next] = e_acc + e_next;
     }
   }
   __syncthreads();
@@ -1294,20 +1395,34 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_compact(Params P)
   __syncthreads();
   if (s_last && tid == 0) {
     __threadfence();
-    const int n_next = ld_volatile(&c->n_next), e_next = ld_volatile(&c->e_next);
+    const int n_pass = ld_volatile(&c->n_next), e_pass = ld_volatile(&c->e_next);
     const unsigned long long t = globaltimer();
-    record_stat(P, c, c->level, c->n_l, c->e_l, TIER_LARGE, p_l, ld_volatile(&c->cand_acc),
-                n_next, c->t_prev, t, *(volatile unsigned long long *)&c->t_kx_begin,
-                *(volatile unsigned long long *)&c->t_kx_end);
-    c->cand_acc = 0;
+    const unsigned long long kb = *(volatile unsigned long long *)&c->t_kx_begin;
+    const unsigned long long ke = *(volatile unsigned long long *)&c->t_kx_end;
+    if (c->pass == 0) c->t_kx_first = kb;
+    c->kx_ns += ke - kb;
     c->done_ctr = 0;
     c->tile_ctr = 0;
-    c->t_prev = t;
-    c->level = c->level + 1;  // Fig1 L10
-    c->cur = nxt;
-    c->m_visited += e_next;
-    c->fb_valid = 0;
-    decide(P, c, n_next, e_next);
+    c->m_visited += e_pass;
+    c->n_acc += n_pass;
+    c->e_acc += e_pass;
+    c->pass += 1;
+    if (c->e_hi < c->e_l) {  // the level's next pass (plan_pass): same frontier, next edges
+      plan_pass(P, c);
+      steer(P, TIER_LARGE);
+    } else {
+      const int n_next = c->n_acc, e_next = c->e_acc;
+      // one record per level: candidates and kept summed over its passes, k_explore's time
+      // as [first pass's start, + the passes' summed durations], passes in `pad`
+      record_stat(P, c, c->level, c->n_l, c->e_l, TIER_LARGE, p_l, ld_volatile(&c->cand_acc),
+                  n_next, c->t_prev, t, c->t_kx_first, c->t_kx_first + c->kx_ns, c->pass);
+      c->cand_acc = 0;
+      c->t_prev = t;
+      c->level = c->level + 1;  // Fig1 L10
+      c->cur = nxt;
+      c->fb_valid = 0;
+      decide(P, c, n_next, e_next);
+    }
   }
 }
 
@@ -1383,6 +1498,7 @@ __global__ void k_dist_init(Params P, int32_t s) {
       c->p_l = 1;
       c->chunk = 1;
       c->wcap = 1;
+      c->pieces = 1;
       c->e_lo = 0;
       c->e_hi = 0;
     }
@@ -1536,6 +1652,7 @@ __global__ void k_dist_advance(Params P, long long *flag) {
     c->p_l = 1;
     c->chunk = 1;
     c->wcap = 1;
+    c->pieces = 1;
     c->e_lo = 0;
     c->e_hi = 0;
   }

@@ -48,7 +48,9 @@ class Options(ctypes.Structure):
                 ("direction", ctypes.c_int32), ("do_alpha", ctypes.c_int32),
                 ("do_beta", ctypes.c_int32), ("dist_size", ctypes.c_int32),
                 ("dist_rank", ctypes.c_int32), ("cluster_max_edges", ctypes.c_int32),
-                ("hub_vertices", ctypes.c_int32), ("tag_mode_pct", ctypes.c_int32)]
+                ("hub_vertices", ctypes.c_int32), ("tag_mode_pct", ctypes.c_int32),
+                ("split_min_edges", ctypes.c_int32), ("split_first_pct", ctypes.c_int32),
+                ("split_passes", ctypes.c_int32)]
 
 
 class DistPeer(ctypes.Structure):

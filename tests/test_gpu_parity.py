@@ -49,6 +49,25 @@ SETTINGS = [
     ("tags-hub3-bu-mixed", dict(debug_poison=1, hub_vertices=3, tag_mode_pct=101,
                                 tier0_max_edges=16, direction=1, do_alpha=64, do_beta=3)),
     ("tags-never", dict(debug_poison=1, tag_mode_pct=-1, tier0_max_edges=-1)),
+    # level passes (a tier-1 level in tag mode explored as consecutive edge ranges, each a
+    # complete explore + dedup appending to the next frontier): forced on every tier-1 level --
+    # two passes with a 1 % / 50 % first pass, five passes, with the small tiers and with the
+    # host loop, and next to bottom-up levels
+    ("passes-2-tier1", dict(debug_poison=1, tag_mode_pct=101, hub_vertices=3, tier0_max_edges=-1,
+                            cluster_max_edges=-1, split_min_edges=1, split_first_pct=1,
+                            split_passes=2)),
+    ("passes-2-half-grain1", dict(debug_poison=1, tag_mode_pct=101, tier0_max_edges=-1,
+                                  cluster_max_edges=-1, edges_per_cta=1, split_min_edges=1,
+                                  split_first_pct=50, split_passes=2)),
+    ("passes-5-T0-16", dict(debug_poison=1, tag_mode_pct=101, hub_vertices=5, tier0_max_edges=16,
+                            split_min_edges=2, split_first_pct=12, split_passes=5)),
+    ("passes-3-host-loop", dict(debug_poison=1, tag_mode_pct=101, loop_mode=2,
+                                tier0_max_edges=64, split_min_edges=8, split_first_pct=30,
+                                split_passes=3)),
+    ("passes-2-bu-mixed", dict(debug_poison=1, tag_mode_pct=101, hub_vertices=3,
+                               tier0_max_edges=16, direction=1, do_alpha=64, do_beta=3,
+                               split_min_edges=4, split_first_pct=25, split_passes=2)),
+    ("passes-off", dict(debug_poison=1, split_passes=1)),
 ]
 
 

@@ -72,6 +72,11 @@ def test_launch_count_from_tier_sequence():
     five = {"tier": np.array([0, 1, 1, 1, 1, 1, 0, 2])}  # one run of 5: 2 entries of 3 pairs
     assert bench.launches_from_stats(five, td_chain=3) == 1 + 2 + 2 * 3 * 2 + 1
     assert bench.launches_from_stats(five, td_chain=1) == 1 + 2 + 2 * 5 + 1
+    # a tier-1 level that ran as p passes (the record's `pad`) takes p (k_explore, k_compact)
+    # pairs of the chain: two levels of 3 and 2 passes = five pairs
+    passes = {"tier": np.array([1, 1]), "pad": np.array([3, 2])}
+    assert bench.launches_from_stats(passes, td_chain=1) == 1 + 2 * 5 + 1
+    assert bench.launches_from_stats(passes, td_chain=3) == 1 + 2 * 3 * 2 + 1
     # one bottom-up run of one level, 3 triples per entry: 1 entry x 3 x 3 launches
     assert bench.launches_from_stats(st, td_chain=4, bu_chain=3) == 1 + 2 + 2 + 16 + 9 + 1
     bu4 = {"tier": np.array([1, 3, 3, 3, 3, 1, 2])}  # bottom-up run of 4: 2 entries of 3
