@@ -117,7 +117,10 @@ typedef struct {
  * discoveries incl. benign-race duplicates, kept = n_{l+1} after owner dedup.  Times are
  * %globaltimer ns: level start (= previous level's end, so launch gaps count) and end; for
  * tier 1 also k_explore's start (its CTA 0) and k_compact's start (its CTA 0), whose
- * difference is the exploration kernel's duration inside the captured loop (0 for tier 0). */
+ * difference is the exploration kernel's duration inside the captured loop (0 for tier 0).
+ * A tier-1 level that ran as several passes (s3bfs_options.split_*) is still ONE record:
+ * candidates and kept summed over the passes, grid = the last pass's P_l, pad = the number of
+ * passes, t_explore_end_ns - t_explore_begin_ns = the passes' summed k_explore durations. */
 typedef struct {
   int32_t level, n_l, e_l, tier, grid, candidates, kept, pad;
   uint64_t t_begin_ns, t_end_ns;
