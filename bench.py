@@ -601,7 +601,8 @@ def main():
                     xb, xe = int(r["t_explore_begin_ns"]), int(r["t_explore_end_ns"])
                     rec = {"l": int(r["level"]), "n_l": int(r["n_l"]), "e_l": int(r["e_l"]),
                            "tier": int(r["tier"]), "grid": int(r["grid"]),
-                           "candidates": int(r["candidates"]), "kept": int(r["kept"])}
+                           "candidates": int(r["candidates"]), "kept": int(r["kept"]),
+                           "passes": max(1, int(r["pad"])) if int(r["tier"]) == 1 else 1}
                     if int(r["tier"]) in (1, 3) and xb > 0:
                         rec.update(gap_us=(xb - t0_) / 1e3, work_us=(t1_ - xb) / 1e3,
                                    explore_us=(xe - xb) / 1e3 if xe > xb else None,

@@ -360,6 +360,32 @@ def test_maximum_size_sparse(kw):
     bfs.close()
 
 
+@pytest.mark.gpu
+def test_level_passes_recorded():
+    """Level passes (DESIGN R29): a tier-1 level forced into 3 passes is still one stats
+    record -- n_l, e_l, kept as the oracle's profile, candidates summed over the passes
+    (>= kept), `pad` = the passes it ran (3 where the level has at least 3 edges), and the
+    default settings never split a small graph (pad = 1 on every tier-1 level)."""
+    g = graphgen.rmat(14, 16, seed=11)
+    ro, col = to_dev(g)
+    s = graphgen.pick_sources(g, 1, seed=7)[0]
+    forced = pkg.S3BFS(ro, col, pkg.Options(debug_poison=1, tag_mode_pct=101, tier0_max_edges=-1,
+                                            cluster_max_edges=-1, split_min_edges=1,
+                                            split_first_pct=10, split_passes=3))
+    check_traversal(g, forced, s)
+    st = forced.level_stats()
+    t1 = st[st["tier"] == 1]
+    assert len(t1) > 0 and np.all(t1["pad"][t1["e_l"] >= 64] == 3), t1["pad"]
+    assert np.all((t1["pad"] >= 1) & (t1["pad"] <= 3))
+    forced.close()
+    plain = pkg.S3BFS(ro, col, pkg.Options(debug_poison=1, tier0_max_edges=-1,
+                                           cluster_max_edges=-1))
+    check_traversal(g, plain, s)
+    st = plain.level_stats()
+    assert np.all(st["pad"][st["tier"] == 1] == 1)
+    plain.close()
+
+
 @pytest.mark.parametrize("kw", [dict(collect_stats=-1), dict(collect_stats=-1, loop_mode=2),
                                 dict(collect_stats=-1, tier0_max_edges=16)],
                          ids=["graph", "host-loop", "cluster-T0-16"])
