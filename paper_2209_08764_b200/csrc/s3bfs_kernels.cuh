@@ -26,7 +26,8 @@
 //   k_cluster  (f) middle   one 8-CTA thread-block cluster runs consecutive mid-size levels,
 //                           frontier replicated through distributed shared memory.
 //   k_fb_clear/k_fb_set/k_bottom_up   NEXT-3 bottom-up levels (direction-optimising option).
-//   k_merge_min/k_merge_keep          NEXT-4 cross-rank merge (one traversal over G ranks).
+//   k_dist_init/k_dist_keep/k_dist_advance/k_dist_finalize   NEXT-4: one traversal over G ranks
+//                           (1-D vertex partition; k_explore<true> routes candidates to owners).
 //   k_finalize              d[0:n-1] and parent in caller ids ("Returns d[0:n-1]").
 //   k_scan_u32 (b) alone    test entry: the same look-back scan over a plain int32 array.
 //   k_find_start (c) alone  test entry: the same warp search, one warp per worker.
