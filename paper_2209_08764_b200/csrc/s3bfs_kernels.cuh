@@ -56,7 +56,7 @@ namespace s3bfs {
 
 // ---- compile-time geometry (the -D switches exist for scripts/kx_micro.py experiments) -----
 #ifndef S3BFS_KD_THREADS
-#define S3BFS_KD_THREADS 512
+#define S3BFS_KD_THREADS 1024
 #endif
 #ifndef S3BFS_KD_MINB
 #define S3BFS_KD_MINB (1024 / S3BFS_KD_THREADS)
