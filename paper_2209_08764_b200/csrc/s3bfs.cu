@@ -614,6 +614,8 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   while (claim_n < (size_t)n || claim_n < (size_t)S3BFS_CLAIM_MIN_BYTES) claim_n <<= 1;
   const size_t o_claim = take(claim_n);
   const size_t o_fb0 = take(bm_bytes), o_fb1 = take(bm_bytes);
+  const bool bu_on = h->opt.direction == 1;  // NEXT-3: dense labels of bottom-up finds
+  const size_t o_lpd = take(bu_on ? (size_t)nv * 8 : 0), o_bub = take(bu_on ? bm_bytes : 0);
   const size_t o_wcnt = take((size_t)p_max * KD_WARPS * 4);
   const size_t o_status = take((size_t)p_max * (dist_size > 1 ? dist_size : 1) * 8 + 8);
   // NEXT-3 bottom-up tiles: width = the power of two >= words / (tiles-per-CTA x P_max), at
@@ -659,6 +661,8 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
     P.split_pct = sp <= 0 ? S3BFS_SPLIT_FIRST_PCT : sp > 99 ? 99 : sp;
     P.split_passes = sn == 0 ? S3BFS_SPLIT_PASSES : sn;
   }
+  P.lpd = bu_on ? (int2 *)(base + o_lpd) : nullptr;
+  P.bub = bu_on ? (uint32_t *)(base + o_bub) : nullptr;
   P.fb[0] = (uint32_t *)(base + o_fb0);
   P.fb[1] = (uint32_t *)(base + o_fb1);
   P.wcnt = (int32_t *)(base + o_wcnt);

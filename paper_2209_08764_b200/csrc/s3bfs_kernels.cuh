@@ -269,6 +269,12 @@ struct Params {
                                 //  split_min edges in tag mode run in up to split_passes passes,
                                 //  the first over split_pct % of the level's edges (<= 0: off)
   uint32_t *fb[2];              // NEXT-3: frontier bitmaps (bottom-up levels only)
+  int2 *lpd;                    // NEXT-3: {d, parent} of the vertices a bottom-up level found,
+  uint32_t *bub;                //  dense (8 B per id), and the bitmap of those vertices: the
+                                //  sweep owns 32 consecutive ids per warp, so its labels
+                                //  coalesce here (into the 32-byte records they are 32 partial
+                                //  sectors); k_finalize reads them where bub's bit is set
+                                //  (NULL without direction optimisation)
   const int32_t *tro, *tcol;    // NEXT-3: in-adjacency (internal ids) the bottom-up step scans
   int32_t *wcnt;
   unsigned long long *status;
@@ -740,6 +746,7 @@ __global__ void k_init(Params P, int32_t s, int32_t *level, int32_t *parent) {
     uint4 w = i == nw4 ? make_uint4(~0u, ~0u, ~0u, ~0u) : make_uint4(0, 0, 0, 0);
     if (i == (si >> 7)) (&w.x)[(si >> 5) & 3] = 1u << (si & 31);
     reinterpret_cast<uint4 *>(P.bm)[i] = w;
+    if (P.bub && i < nw4) reinterpret_cast<uint4 *>(P.bub)[i] = make_uint4(0, 0, 0, 0);
   }
   const long long nc = ((long long)P.claim_mask + 16) >> 4;  // claim tags <- 0 (all slots),
   const uint32_t ss = claim_slot(P, si);                       // but the source's (discovered)
@@ -2425,12 +2432,17 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params 
       const int v = (w << 5) + lane;
       const bool found = pu[i] >= 0;
       if (found) {
-        *lp_of(P.vinfo, v) = make_int2(new_level, __ldg(P.vs16 + pu[i]).z);  // d, parent (caller)
+        P.lpd[v] = make_int2(new_level, __ldg(P.vs16 + pu[i]).z);  // d, parent (caller id)
         mark_tag(P, v);
       }
       const unsigned m = __ballot_sync(0xffffffffu, found);
       if (lane == 0 && w < w1) {
-        if (m) bm[w] = bw[i] | m;  // this warp owns word w
+        if (m) {
+          bm[w] = bw[i] | m;        // this warp owns word w
+          atomicOr(P.bub + w, m);   // these vertices' labels are in lpd (fire-and-forget OR:
+                                    // earlier bottom-up levels' bits stay; no discovery race
+                                    // exists in this step, R17 concerns the top-down path)
+        }
         fbn[w] = m;
       }
       kept += __popc(m);
@@ -2517,7 +2529,9 @@ __global__ void k_finalize(Params P) {
     S3_CHK(i, P.n);
     int lv = -1, pa = -1;
     if ((__ldg(P.bm + (i >> 5)) >> (i & 31)) & 1u) {
-      const int2 r = __ldg(reinterpret_cast<const int2 *>(vstat(P.vinfo, i) + 1));
+      const bool bu = P.bub && ((__ldg(P.bub + (i >> 5)) >> (i & 31)) & 1u);  // NEXT-3 label
+      const int2 r = bu ? __ldg(P.lpd + i)
+                        : __ldg(reinterpret_cast<const int2 *>(vstat(P.vinfo, i) + 1));
       lv = r.x;
       pa = r.y;
     }
