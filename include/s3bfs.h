@@ -57,7 +57,7 @@ typedef enum {
  * paper's tunables: P (max cores) and GRAINSIZE, and the work-insensitive
  * comparison variant. */
 typedef struct {
-  int32_t edges_per_cta;   /* grain of (f): P_l = min(P_max, ceil(e_l / grain)).  0 -> 2048 */
+  int32_t edges_per_cta;   /* grain of (f): P_l = min(P_max, ceil(e_l / grain)).  0 -> 1024 */
   int32_t tier0_max_edges; /* T0: a level with e_l <= T0 (and n_l <= 8192) runs in the
                               single-CTA tier.  0 -> 8192 (the maximum); < 0 -> tier 0 off */
   int32_t loop_mode;       /* 0/1: level loop captured in a CUDA graph (WHILE + SWITCH nodes);

@@ -562,7 +562,7 @@ s3bfs_status create_impl(s3bfs_handle *out, int32_t n, int64_t nnz, const int32_
   int p_max = h->num_sms * occ;  // every CTA resident: the look-back never waits on a CTA
   if (h->opt.max_ctas > 0 && h->opt.max_ctas < p_max) p_max = h->opt.max_ctas;
   if (p_max > KD_THREADS) p_max = KD_THREADS;  // k_compact's one-round-trip prefix: a thread per tile
-  const int grain = h->opt.edges_per_cta > 0 ? h->opt.edges_per_cta : 2048;
+  const int grain = h->opt.edges_per_cta > 0 ? h->opt.edges_per_cta : 1024;
   // cluster tier: T0 < e_l <= tc_max (one 8-CTA cluster); tier 0 keeps the small levels
   int tc_max = h->opt.cluster_max_edges == 0 ? KC_CL * KC_ECTA : h->opt.cluster_max_edges;
   if (tc_max > KC_CL * KC_ECTA) tc_max = KC_CL * KC_ECTA;
