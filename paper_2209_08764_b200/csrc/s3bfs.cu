@@ -447,7 +447,7 @@ s3bfs_status build_graph(s3bfs_ctx *h) {
 
   {  // after the loop: d[0:n-1] and parent in caller ids
     cudaKernelNodeParams kf = {};
-    kf.func = (void *)k_finalize;
+    kf.func = h->P.bub ? (void *)k_finalize<true> : (void *)k_finalize<false>;
     kf.gridDim = dim3(finalize_grid(h));
     kf.blockDim = dim3(256);
     kf.kernelParams = args;
@@ -851,7 +851,8 @@ s3bfs_status s3bfs_run(s3bfs_handle h, int32_t source, int32_t *level, int32_t *
     }
     const Ctl c = *h->h_ctl;
     if (c.tier == TIER_DONE) {
-      k_finalize<<<finalize_grid(h), 256, 0, stream>>>(h->P);
+      if (h->P.bub) k_finalize<true><<<finalize_grid(h), 256, 0, stream>>>(h->P);
+      else k_finalize<false><<<finalize_grid(h), 256, 0, stream>>>(h->P);
       CK(h, cudaGetLastError());
       break;
     }

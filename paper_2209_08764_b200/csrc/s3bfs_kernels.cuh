@@ -2518,6 +2518,10 @@ __global__ void __launch_bounds__(KD_THREADS, KD_MIN_BLOCKS) k_bottom_up(Params 
 // level[o] = d of internal vertex o2n[o] if its visited bit is set, else -1 (unreachable, R1);
 // parent[o] = its recorded parent (a caller id, R2).  Reads the internal records in caller
 // order; the caller's arrays are written exactly once, coalesced.
+// BU = the direction-optimising handle's instance (NEXT-3: vertices a bottom-up level found
+// carry their labels in the dense lpd array, bub says which); the top-down handle's instance
+// has none of it
+template <bool BU>
 __global__ void k_finalize(Params P) {
   const Ctl *c = P.ctl;
   int32_t *__restrict__ level = c->level_out;
@@ -2529,7 +2533,7 @@ __global__ void k_finalize(Params P) {
     S3_CHK(i, P.n);
     int lv = -1, pa = -1;
     if ((__ldg(P.bm + (i >> 5)) >> (i & 31)) & 1u) {
-      const bool bu = P.bub && ((__ldg(P.bub + (i >> 5)) >> (i & 31)) & 1u);  // NEXT-3 label
+      const bool bu = BU && ((__ldg(P.bub + (i >> 5)) >> (i & 31)) & 1u);  // NEXT-3 label
       const int2 r = bu ? __ldg(P.lpd + i)
                         : __ldg(reinterpret_cast<const int2 *>(vstat(P.vinfo, i) + 1));
       lv = r.x;
